@@ -1,0 +1,180 @@
+/*
+ * dear.h — C ABI of the B200-native DeAR decoupled all-reduce runtime.
+ *
+ * The reference (/root/reference/proj, a C++20 simulator + fp64 oracle) has no
+ * runtime FFI; its interface for this path is the value-type C++ API in
+ * proj/include/dearsim/{model,fusion,policy,collective,task_graph}.hpp, and
+ * the paper describes the runtime as "a communication library using C/C++
+ * based on NCCL [exposing] APIs for high-level scripts in Python" wrapped by a
+ * DistOptim. Each entry point below cites the reference
+ * interface it realises. INTEGRATION.md shows the ctypes binding.
+ *
+ * Conventions (mirroring the reference's error model):
+ *   return 0 (DEAR_OK), 1 (DEAR_EINVAL: std::invalid_argument in the
+ *   reference, e.g. "build_fusion_plan: empty model", fusion.cpp:33) or
+ *   2 (DEAR_EINTERNAL: CUDA/NCCL failure; std::runtime_error in the
+ *   reference). dear_last_error() returns the calling thread's last message.
+ *   Layers are 1-based: layer 1 is the input side, layer L the output side
+ *   (model.hpp:24-34). A context is not thread-safe; serialise calls.
+ *   Streams are cudaStream_t passed as void* (NULL = legacy default stream).
+ */
+#ifndef DEAR_H_
+#define DEAR_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DEAR_OK 0
+#define DEAR_EINVAL 1
+#define DEAR_EINTERNAL 2
+
+/* PolicyKind (policy.hpp:34), same numbering. PRIORITY_PARTITION (2) is out of
+ * scope for the runtime and rejected with DEAR_EINVAL. */
+#define DEAR_POLICY_WFBP 0
+#define DEAR_POLICY_WFBP_FUSED 1
+#define DEAR_POLICY_DEAR 3
+#define DEAR_POLICY_DEAR_FUSED 4
+
+typedef struct dear_ctx dear_ctx;
+typedef struct dear_local_group dear_local_group;
+
+/* PolicySpec (policy.hpp:36-45) + the optimizer of SgdState
+ * (collective.hpp:77-80). momentum / dampening / weight_decay / nesterov
+ * follow torch.optim.SGD and are an UNPINNED extension (the reference's
+ * update is plain lr-SGD, collective.cpp:190-192). */
+typedef struct {
+  int32_t policy;               /* DEAR_POLICY_* */
+  int64_t fusion_buffer_bytes;  /* > 0 for *_FUSED (policy.cpp:53-66) */
+  int32_t dear_group_dependency;/* policy.hpp:44: AG_g waits on RS_g only */
+  double lr;
+  double momentum;
+  double dampening;
+  double weight_decay;
+  int32_t nesterov;
+  int32_t defer_allgather;      /* 1: AGs are enqueued by the next
+                                   dear_param_wait (CUDA-graph friendly);
+                                   0: by dear_step */
+} dear_cfg;
+
+/* ---------------------------------------------------------------------------
+ * Pure host functions (no GPU needed).
+ * ------------------------------------------------------------------------ */
+
+/* build_fusion_plan (fusion.cpp:29-57); buffer_bytes == 0 selects
+ * per_layer_plan (fusion.cpp:59-70). layer_bytes[0] is layer 1. Groups are
+ * written in backprop issue order (low[0]/high[0] hold layer L); low/high
+ * need room for L entries. Bit-exact with the reference. */
+int dear_plan_build(const int64_t* layer_bytes, int32_t L, int64_t buffer_bytes,
+                    int32_t* low, int32_t* high, int32_t* n_groups);
+
+/* chunk_ranges (collective.cpp:39-57): begin[0..P] (P+1 entries), chunk c is
+ * [begin[c], begin[c+1]). *slot_elems = ceil(d/P), the per-rank NCCL count
+ * before alignment padding. Chunk c is owned (fully reduced) by rank
+ * (c-1) mod P (collective.cpp:94), so NCCL slot r carries chunk (r+1) mod P. */
+int dear_chunk_layout(int64_t d, int32_t P, int64_t* begin, int64_t* slot_elems);
+
+/* Stride (elements) between rank slots in a bucket buffer: ceil(d/P) rounded
+ * up to a multiple of 64 elements (256 B). */
+int64_t dear_slot_stride(int64_t d, int32_t P);
+
+const char* dear_last_error(void);
+
+/* ---------------------------------------------------------------------------
+ * Communicators. NCCL over NVLink/NVSwitch for one process per GPU; a local
+ * group emulates P ranks inside one process (one device), with collectives
+ * executed as ring-order kernels over all ranks' buffers — used to exercise
+ * the P > 1 path on a single GPU.
+ * ------------------------------------------------------------------------ */
+int dear_comm_unique_id(uint8_t id[128]);
+int dear_comm_init(void** comm, int32_t nranks, const uint8_t id[128], int32_t rank);
+int dear_comm_destroy(void* comm);
+int dear_local_group_create(int32_t P, dear_local_group** group);
+int dear_local_group_destroy(dear_local_group* group);
+
+/* ---------------------------------------------------------------------------
+ * Runtime context (the DistOptim of PAPER.md:183-188).
+ * ------------------------------------------------------------------------ */
+
+/* nccl_comm: an ncclComm_t from dear_comm_init (NULL allowed when P == 1).
+ * compute_stream: the stream forward/backward run on (recorded for joins).
+ * Validates cfg like validate(PolicySpec) (policy.cpp:53-66). */
+int dear_create(void* nccl_comm, int32_t rank, int32_t P, void* compute_stream,
+                const dear_cfg* cfg, dear_ctx** out);
+/* Same, as rank `rank` of a local group. */
+int dear_create_local(dear_local_group* group, int32_t rank, void* compute_stream,
+                      const dear_cfg* cfg, dear_ctx** out);
+
+/* Tensor registration: LayerSpec (model.hpp:26-34). `layer` must end up
+ * exactly 1..L (model.cpp:50-56). param/grad are caller-owned device fp32
+ * buffers of `numel` elements. */
+int dear_register_tensor(dear_ctx* ctx, int32_t layer, float* param, float* grad,
+                         int64_t numel);
+/* Optional bf16 compute copy of a layer's parameters; the fused unpack
+ * kernel refreshes it together with the fp32 parameters. */
+int dear_register_shadow(dear_ctx* ctx, int32_t layer, void* bf16_copy);
+/* Builds the fusion plan, bucket buffers, unit tables, events; checks (when
+ * P > 1) that every rank registered the same model. */
+int dear_finalize(dear_ctx* ctx);
+
+/* Backward hook: layer's gradient is complete on `stream`. When the bucket
+ * holding it is complete (all its layers reported), its pack -> RS -> update
+ * is enqueued on the comm stream, in plan order (task_graph.cpp:186-194,
+ * RS_g deps = BP of g's layers :148-154). WFBP kinds also enqueue AG + unpack
+ * right behind (task_graph.cpp:163-176). */
+int dear_grad_ready(dear_ctx* ctx, int32_t layer, void* stream);
+
+/* Forward pre-hook: `stream` waits for the all-gather + unpack of the bucket
+ * holding `layer` (FF_l <- AG_{g(l)}, task_graph.cpp:207) — never a global
+ * barrier. Enqueues deferred all-gathers first when defer_allgather = 1. */
+int dear_param_wait(dear_ctx* ctx, int32_t layer, void* stream);
+
+/* End of backprop: the BARRIER of task_graph.cpp:195-198. All layers must
+ * have been reported. DEAR kinds enqueue AG_g + unpack in feed-forward order
+ * (reverse plan order, :199-206) unless deferred. `stream` (the caller's
+ * compute stream) is fenced both ways: the comm stream's all-gathers wait for
+ * work already on `stream`, and `stream` waits until every gradient has been
+ * packed (so gradients may be zeroed / overwritten afterwards). */
+int dear_step(dear_ctx* ctx, void* stream);
+
+/* `stream` waits for all comm-stream work enqueued so far (graph capture
+ * join point). */
+int dear_join(dear_ctx* ctx, void* stream);
+
+/* Host-blocking: flush deferred all-gathers and wait until parameters are
+ * fully updated ("forced to synchronize ... before evaluating"). */
+int dear_synchronize(dear_ctx* ctx);
+
+int dear_destroy(dear_ctx* ctx);
+
+/* Learning-rate change (device-resident; CUDA-graph safe). */
+int dear_set_lr(dear_ctx* ctx, double lr);
+
+/* ---------------------------------------------------------------------------
+ * Introspection, timing and checks.
+ * ------------------------------------------------------------------------ */
+int dear_num_buckets(dear_ctx* ctx, int32_t* n);
+/* Bucket g (0-based, plan order): layers low..high, d elements, slot stride. */
+int dear_bucket_info(dear_ctx* ctx, int32_t g, int32_t* low, int32_t* high, int64_t* elems,
+                     int64_t* slot_stride);
+/* Collective issue log of the current/last iteration, reference task labels
+ * (task_graph.cpp:51-58), e.g. "RS g1\nRS g2\nAG g2\nAG g1\n". Writes at most
+ * cap bytes (NUL-terminated); *needed gets the full length + 1. */
+int dear_trace(dear_ctx* ctx, char* buf, int64_t cap, int64_t* needed);
+/* Enable per-bucket CUDA-event timing of pack / RS / update / AG / unpack. */
+int dear_set_timing(dear_ctx* ctx, int32_t enable);
+/* After dear_synchronize: milliseconds per bucket and stage for the last
+ * timed iteration; out is n_buckets x 5 (pack, rs, update, ag, unpack),
+ * -1 where a stage did not run. */
+int dear_get_timings(dear_ctx* ctx, float* out, int32_t n_buckets);
+/* Replica check — the GPU analogue of sgd_step's "replica divergence"
+ * rejection (collective.cpp:172-181): hashes every registered parameter
+ * and compares across ranks. *identical = 1 when all ranks agree. */
+int dear_check_replicas(dear_ctx* ctx, int32_t* identical);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DEAR_H_ */

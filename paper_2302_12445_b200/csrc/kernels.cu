@@ -1,0 +1,335 @@
+// sm_100a kernels for the DeAR bucket pipeline: pack (grad -> NCCL slot
+// layout, fused 1/P scale), shard-local SGD update (between reduce-scatter
+// and all-gather), unpack (slot layout -> fp32 params + bf16 compute copy).
+//
+// All three are HBM-streaming kernels: pack and unpack move
+// 8 B/elem (+2 B/elem for the bf16 copy), update 12 B/shard-elem (20 with a
+// momentum buffer). Work is pre-cut on the host into Units of <= 8192
+// elements (one layer x chunk intersection each), one CTA per unit in a
+// grid-stride loop. Inside a unit the destination is peeled to 16 B alignment
+// and every access is a 128-bit vector; when the source is misaligned
+// relative to the destination (layer boundaries fall anywhere inside a
+// bucket), each lane loads its aligned float4 and takes the next lane's via
+// __shfl_down_sync, so both sides stay 128-bit and fully coalesced.
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "dear_kernels.h"
+
+namespace dear {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kUnroll = 4;
+constexpr int kMaxCtasPerSm = 8;
+constexpr int kSms = 148;
+
+__device__ __forceinline__ float4 shfl_down4(float4 v) {
+  v.x = __shfl_down_sync(0xffffffffu, v.x, 1);
+  v.y = __shfl_down_sync(0xffffffffu, v.y, 1);
+  v.z = __shfl_down_sync(0xffffffffu, v.z, 1);
+  v.w = __shfl_down_sync(0xffffffffu, v.w, 1);
+  return v;
+}
+
+template <int M>
+__device__ __forceinline__ float4 realign(float4 a, float4 b) {
+  if constexpr (M == 0) {
+    return a;
+  } else if constexpr (M == 1) {
+    return make_float4(a.y, a.z, a.w, b.x);
+  } else if constexpr (M == 2) {
+    return make_float4(a.z, a.w, b.x, b.y);
+  } else {
+    return make_float4(a.w, b.x, b.y, b.z);
+  }
+}
+
+enum class Hint { kStream, kKeep };
+
+template <Hint H>
+__device__ __forceinline__ float4 ld4(const float4* p) {
+  if constexpr (H == Hint::kStream) {
+    return __ldcs(p);
+  } else {
+    return __ldg(p);
+  }
+}
+
+// Warp-cooperative walk over destination vectors q in [0, n4). The source
+// element for destination element 4q+e is src_floor[M + 4q + e]; src_floor is
+// 16 B aligned and vectors up to index qmax hold at least one valid element.
+// body(q, v) runs on every lane whose q < n4.
+template <int M, Hint H, typename Body>
+__device__ __forceinline__ void warp_stream(const float* src_floor, int64_t n4, int64_t qmax,
+                                            Body&& body) {
+  const float4* s4 = reinterpret_cast<const float4*>(src_floor);
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  constexpr int kWarps = kThreads / 32;
+  for (int64_t base = static_cast<int64_t>(warp) * 32 * kUnroll; base < n4;
+       base += static_cast<int64_t>(kWarps) * 32 * kUnroll) {
+    float4 a[kUnroll], b[kUnroll];
+#pragma unroll
+    for (int k = 0; k < kUnroll; ++k) {
+      const int64_t q = base + k * 32 + lane;
+      a[k] = q <= qmax ? ld4<H>(s4 + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    if constexpr (M != 0) {
+#pragma unroll
+      for (int k = 0; k < kUnroll; ++k) {
+        b[k] = shfl_down4(a[k]);
+        const int64_t q = base + k * 32 + lane;
+        if (lane == 31 && q + 1 <= qmax) b[k] = ld4<H>(s4 + q + 1);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kUnroll; ++k) {
+      const int64_t q = base + k * 32 + lane;
+      if (q < n4) body(q, realign<M>(a[k], M != 0 ? b[k] : a[k]));
+    }
+  }
+}
+
+// Peels `dst` to 16 B alignment (scalar head via head_fn), then dispatches the
+// vector walk on the source misalignment, then the scalar tail.
+template <Hint H, typename HeadFn, typename VecFn>
+__device__ __forceinline__ void run_unit(const float* src, const float* dst, int64_t len,
+                                         HeadFn&& scalar_fn, VecFn&& vec_fn) {
+  int64_t head = ((16 - (reinterpret_cast<uintptr_t>(dst) & 15)) & 15) >> 2;
+  if (head > len) head = len;
+  if (threadIdx.x < head) scalar_fn(static_cast<int64_t>(threadIdx.x));
+  const int64_t rest = len - head;
+  const int64_t n4 = rest >> 2;
+  if (n4 > 0) {
+    const float* s = src + head;
+    const int m = static_cast<int>((reinterpret_cast<uintptr_t>(s) & 15) >> 2);
+    const float* floor = s - m;
+    const int64_t qmax = (m + rest - 1) >> 2;
+    switch (m) {
+      case 0:
+        warp_stream<0, H>(floor, n4, qmax, [&](int64_t q, float4 v) { vec_fn(head, q, v); });
+        break;
+      case 1:
+        warp_stream<1, H>(floor, n4, qmax, [&](int64_t q, float4 v) { vec_fn(head, q, v); });
+        break;
+      case 2:
+        warp_stream<2, H>(floor, n4, qmax, [&](int64_t q, float4 v) { vec_fn(head, q, v); });
+        break;
+      default:
+        warp_stream<3, H>(floor, n4, qmax, [&](int64_t q, float4 v) { vec_fn(head, q, v); });
+        break;
+    }
+  }
+  for (int64_t i = head + n4 * 4 + threadIdx.x; i < len; i += kThreads) scalar_fn(i);
+}
+
+// ---------------------------------------------------------------- pack ----
+__global__ void __launch_bounds__(kThreads) pack_kernel(const Unit* __restrict__ units,
+                                                        int n_units, float scale) {
+  for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+    const Unit U = units[u];
+    const float* src = U.a;
+    float* dst = U.b;
+    run_unit<Hint::kStream>(
+        src, dst, U.len, [&](int64_t i) { dst[i] = __fmul_rn(src[i], scale); },
+        [&](int64_t head, int64_t q, float4 v) {
+          v.x = __fmul_rn(v.x, scale);
+          v.y = __fmul_rn(v.y, scale);
+          v.z = __fmul_rn(v.z, scale);
+          v.w = __fmul_rn(v.w, scale);
+          reinterpret_cast<float4*>(dst + head)[q] = v;
+        });
+  }
+}
+
+// -------------------------------------------------------------- update ----
+// torch.optim.SGD per element on the averaged gradient; with momentum = wd = 0
+// it is exactly w - lr * (sum * 1/P) (collective.cpp:159-164, :190-192). Each
+// operation is separately rounded (no FMA contraction), in the order of
+// oracle/dear_oracle.c:or_sgd_step_f32.
+template <bool kMom, bool kWd>
+__device__ __forceinline__ float sgd_elem(float g, float w, float& m, const HyperParams& hp,
+                                          bool has_buf) {
+  float dp = hp.prescaled ? g : __fmul_rn(g, hp.inv_p);
+  if (kWd) dp = __fadd_rn(dp, __fmul_rn(hp.weight_decay, w));
+  if (kMom) {
+    m = has_buf ? __fadd_rn(__fmul_rn(m, hp.momentum), __fmul_rn(hp.one_minus_dampening, dp))
+                : dp;
+    dp = hp.nesterov ? __fadd_rn(dp, __fmul_rn(hp.momentum, m)) : m;
+  }
+  return __fsub_rn(w, __fmul_rn(hp.lr, dp));
+}
+
+template <bool kMom, bool kWd>
+__global__ void __launch_bounds__(kThreads) update_kernel(const Unit* __restrict__ units,
+                                                          int n_units,
+                                                          const HyperParams* __restrict__ hpp,
+                                                          int has_buf) {
+  const HyperParams hp = *hpp;
+  for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+    const Unit U = units[u];
+    const float* w = U.a;
+    float* g = U.b;
+    float* mom = static_cast<float*>(U.c);
+    run_unit<Hint::kKeep>(
+        w, g, U.len,
+        [&](int64_t i) {
+          float m = kMom ? mom[i] : 0.f;
+          g[i] = sgd_elem<kMom, kWd>(g[i], w[i], m, hp, has_buf);
+          if (kMom) mom[i] = m;
+        },
+        [&](int64_t head, int64_t q, float4 wv) {
+          float4* g4 = reinterpret_cast<float4*>(g + head);
+          float4* m4 = reinterpret_cast<float4*>(mom + head);
+          float4 gv = __ldcs(g4 + q);
+          float4 mv = kMom && has_buf ? m4[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+          gv.x = sgd_elem<kMom, kWd>(gv.x, wv.x, mv.x, hp, has_buf);
+          gv.y = sgd_elem<kMom, kWd>(gv.y, wv.y, mv.y, hp, has_buf);
+          gv.z = sgd_elem<kMom, kWd>(gv.z, wv.z, mv.z, hp, has_buf);
+          gv.w = sgd_elem<kMom, kWd>(gv.w, wv.w, mv.w, hp, has_buf);
+          g4[q] = gv;
+          if (kMom) m4[q] = mv;
+        });
+  }
+}
+
+// -------------------------------------------------------------- unpack ----
+template <bool kShadow>
+__global__ void __launch_bounds__(kThreads) unpack_kernel(const Unit* __restrict__ units,
+                                                          int n_units) {
+  for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+    const Unit U = units[u];
+    const float* src = U.a;
+    float* dst = U.b;
+    __nv_bfloat16* sh = static_cast<__nv_bfloat16*>(U.c);
+    run_unit<Hint::kStream>(
+        src, dst, U.len,
+        [&](int64_t i) {
+          const float v = src[i];
+          dst[i] = v;
+          if (kShadow) sh[i] = __float2bfloat16_rn(v);
+        },
+        [&](int64_t head, int64_t q, float4 v) {
+          reinterpret_cast<float4*>(dst + head)[q] = v;
+          if (kShadow) {
+            __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y);
+            __nv_bfloat162 hi = __floats2bfloat162_rn(v.z, v.w);
+            uint2 packed;
+            packed.x = *reinterpret_cast<uint32_t*>(&lo);
+            packed.y = *reinterpret_cast<uint32_t*>(&hi);
+            reinterpret_cast<uint2*>(sh + head)[q] = packed;
+          }
+        });
+  }
+}
+
+// ---------------------------------------------------- local collectives ----
+__global__ void local_rs_kernel(float* const* __restrict__ bufs, int P, int64_t stride,
+                                int64_t count) {
+  const int64_t total = static_cast<int64_t>(P) * count;
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(t / count);
+    const int64_t off = static_cast<int64_t>(r) * stride + (t - static_cast<int64_t>(r) * count);
+    int k = (r + 1) % P;
+    float acc = bufs[k][off];
+    for (int j = 1; j < P; ++j) {
+      k = (k + 1) % P;
+      acc = __fadd_rn(acc, bufs[k][off]);
+    }
+    bufs[r][off] = acc;
+  }
+}
+
+__global__ void local_ag_kernel(float* const* __restrict__ bufs, int P, int64_t stride,
+                                int64_t count) {
+  const int64_t total = static_cast<int64_t>(P) * P * count;
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t pair = t / count;
+    const int r = static_cast<int>(pair / P), s = static_cast<int>(pair % P);
+    if (r == s) continue;
+    const int64_t off = static_cast<int64_t>(s) * stride + (t - pair * count);
+    bufs[r][off] = bufs[s][off];
+  }
+}
+
+// ---------------------------------------------------------------- hash ----
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+__global__ void hash_kernel(const float* __restrict__ x, int64_t n, uint64_t salt,
+                            unsigned long long* acc) {
+  uint64_t h = 0;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t bits = __float_as_uint(x[i]);
+    h += mix64(bits ^ mix64(static_cast<uint64_t>(i) + salt));
+  }
+  for (int o = 16; o > 0; o >>= 1) h += __shfl_down_sync(0xffffffffu, h, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(acc, static_cast<unsigned long long>(h));
+}
+
+int grid_for(int n_units) {
+  const int cap = kSms * kMaxCtasPerSm;
+  return n_units < cap ? n_units : cap;
+}
+
+}  // namespace
+
+cudaError_t launch_pack(const Unit* units, int n_units, float scale, cudaStream_t s) {
+  if (n_units <= 0) return cudaSuccess;
+  pack_kernel<<<grid_for(n_units), kThreads, 0, s>>>(units, n_units, scale);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_update(const Unit* units, int n_units, const HyperParams* hp,
+                          int has_momentum_buf, int use_momentum, int use_wd, cudaStream_t s) {
+  if (n_units <= 0) return cudaSuccess;
+  const int g = grid_for(n_units);
+  if (use_momentum && use_wd)
+    update_kernel<true, true><<<g, kThreads, 0, s>>>(units, n_units, hp, has_momentum_buf);
+  else if (use_momentum)
+    update_kernel<true, false><<<g, kThreads, 0, s>>>(units, n_units, hp, has_momentum_buf);
+  else if (use_wd)
+    update_kernel<false, true><<<g, kThreads, 0, s>>>(units, n_units, hp, has_momentum_buf);
+  else
+    update_kernel<false, false><<<g, kThreads, 0, s>>>(units, n_units, hp, has_momentum_buf);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_unpack(const Unit* units, int n_units, int with_shadow, cudaStream_t s) {
+  if (n_units <= 0) return cudaSuccess;
+  if (with_shadow)
+    unpack_kernel<true><<<grid_for(n_units), kThreads, 0, s>>>(units, n_units);
+  else
+    unpack_kernel<false><<<grid_for(n_units), kThreads, 0, s>>>(units, n_units);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_local_reduce_scatter(float* const* bufs_dev, int P, int64_t stride,
+                                        int64_t count, cudaStream_t s) {
+  if (count <= 0) return cudaSuccess;
+  local_rs_kernel<<<kSms * 4, 256, 0, s>>>(bufs_dev, P, stride, count);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_local_all_gather(float* const* bufs_dev, int P, int64_t stride,
+                                    int64_t count, cudaStream_t s) {
+  if (count <= 0) return cudaSuccess;
+  local_ag_kernel<<<kSms * 4, 256, 0, s>>>(bufs_dev, P, stride, count);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_hash(const float* x, int64_t n, uint64_t salt, unsigned long long* acc,
+                        cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  hash_kernel<<<kSms * 2, 256, 0, s>>>(x, n, salt, acc);
+  return cudaGetLastError();
+}
+
+}  // namespace dear

@@ -1,0 +1,1014 @@
+// DeAR runtime: tensor registration, bucket layout in HBM, the BackPipe /
+// FeedPipe schedule on a dedicated high-priority comm stream, and the two
+// collective backends (NCCL over NVLink/NVSwitch; a local group emulating P
+// ranks on one device).
+//
+// Schedule contract (the reference's task DAG, task_graph.cpp:127-210, with
+// the two-stream semantics of simulate.cpp:65-159):
+//   BackPipe  : bucket g complete (all its layers' grads reported)
+//               -> [comm] wait grad events, pack_g, RS_g, update_g
+//               buckets are issued strictly in plan order (:186-194); NCCL
+//               additionally requires every rank to issue collectives in the
+//               same order, which plan order guarantees.
+//   BARRIER   : dear_step — comm stream waits for the caller's stream.
+//   FeedPipe  : AG_g + unpack_g in reverse plan order (:199-206); FF_l waits
+//               on ag_done[g(l)] only (:207).
+//   WFBP      : RS_g, update_g, AG_g, unpack_g back to back during BackPipe
+//               (all-reduce as RS + AG).
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <deque>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "dear.h"
+#include "dear_internal.h"
+#include "dear_kernels.h"
+
+namespace dear {
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+namespace {
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    throw Error(DEAR_EINTERNAL, std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) {
+    throw Error(DEAR_EINTERNAL, std::string(what) + ": " + ncclGetErrorString(r));
+  }
+}
+
+void invalid(const std::string& m) { throw Error(DEAR_EINVAL, m); }
+
+bool is_fused(int policy) {
+  return policy == DEAR_POLICY_WFBP_FUSED || policy == DEAR_POLICY_DEAR_FUSED;
+}
+bool is_dear(int policy) {
+  return policy == DEAR_POLICY_DEAR || policy == DEAR_POLICY_DEAR_FUSED;
+}
+
+enum OpKind { OP_FENCE_READY, OP_FENCE_STEP, OP_PACK, OP_RS, OP_UPDATE, OP_AG, OP_UNPACK,
+              OP_AG_DONE, OP_CALLER_WAIT_PACKED };
+
+struct Op {
+  OpKind kind;
+  int bucket;
+  cudaStream_t stream;  // OP_CALLER_WAIT_PACKED
+  bool collective() const { return kind == OP_RS || kind == OP_AG; }
+};
+
+enum TimingEv { T_PACK0, T_PACK1, T_RS1, T_UPD1, T_AG0, T_AG1, T_UNPACK1, T_COUNT };
+
+struct LayerReg {
+  float* param = nullptr;
+  float* grad = nullptr;
+  void* shadow = nullptr;
+  int64_t numel = -1;
+  int bucket = -1;
+  int64_t off = 0;  // offset of the layer inside its bucket's flat order
+  bool ready = false;
+};
+
+struct Bucket {
+  int low = 0, high = 0;
+  int64_t d = 0, stride = 0;
+  float* buf = nullptr;  // P * stride: slot r holds chunk (r+1)%P
+  float* mom = nullptr;  // stride (own shard's momentum), or null
+  int layers_left = 0;
+  bool complete = false;
+  std::vector<cudaStream_t> ready_streams;
+  std::vector<cudaEvent_t> ready_events;
+  Unit *pack_u = nullptr, *upd_u = nullptr, *unpack_u = nullptr;
+  int n_pack = 0, n_upd = 0, n_unpack = 0;
+  bool any_shadow = false;
+  bool mom_init = false;
+  cudaEvent_t ag_done = nullptr;
+  bool ag_live = false;          // an AG for this bucket is enqueued
+  cudaStream_t waited = nullptr; // last stream that waited on ag_done
+  bool waited_valid = false;
+  cudaEvent_t t[T_COUNT] = {};
+  bool t_rec[T_COUNT] = {};
+};
+
+}  // namespace
+}  // namespace dear
+
+using namespace dear;
+
+struct dear_local_group {
+  int P = 0;
+  std::vector<dear_ctx*> ranks;
+  std::map<int, float**> bufs_dev;  // bucket -> device array of P buffers
+  cudaEvent_t arrive[64] = {};
+  cudaEvent_t done = nullptr;
+  bool draining = false;
+  ~dear_local_group();
+  void drain();
+  void run_collective(const Op& op);
+};
+
+struct dear_ctx {
+  bool local = false;
+  ncclComm_t comm = nullptr;
+  dear_local_group* group = nullptr;
+  int rank = 0, P = 1;
+  int device = 0;
+  cudaStream_t compute = nullptr;
+  cudaStream_t comm_stream = nullptr;
+  dear_cfg cfg{};
+  bool finalized = false;
+  std::vector<LayerReg> layers;  // index layer-1
+  std::vector<Bucket> buckets;   // plan order
+  int rs_cursor = 0;
+  int reported = 0;
+  bool ags_deferred = false;
+  int64_t iteration = 0;
+  HyperParams hp_host{};
+  HyperParams* hp_dev = nullptr;
+  char* arena = nullptr;
+  float pack_scale = 1.f;
+  cudaEvent_t packed_ev = nullptr;
+  cudaEvent_t step_ev = nullptr;
+  cudaEvent_t join_ev = nullptr;
+  unsigned long long* hash_dev = nullptr;
+  bool timing = false;
+  std::vector<std::string> trace;
+  std::deque<Op> queue;  // local mode: ops not yet executed
+
+  ~dear_ctx();
+  void enqueue(Op op);
+  void exec(const Op& op);
+  void complete_bucket(int b);
+  void enqueue_backpipe(int b);
+  void enqueue_feedpipe();
+  void record_t(int b, int which);
+  std::string label(const char* kind, int b) const;
+};
+
+namespace {
+
+void free_events(std::vector<cudaEvent_t>& evs) {
+  for (cudaEvent_t e : evs)
+    if (e) cudaEventDestroy(e);
+  evs.clear();
+}
+
+cudaEvent_t new_event(bool timing) {
+  cudaEvent_t e;
+  cuda_check(cudaEventCreateWithFlags(&e, timing ? cudaEventDefault : cudaEventDisableTiming),
+             "cudaEventCreate");
+  return e;
+}
+
+// Units for one bucket op: the intersections of the bucket's layers (in
+// ascending layer order, the flatten order) with chunk range [cb, ce), cut at
+// kUnitElems. emit(layer, j0, len, pos) where pos is the offset inside the
+// chunk.
+template <typename Emit>
+void for_each_piece(const dear_ctx& ctx, const Bucket& B, int64_t cb, int64_t ce, Emit&& emit) {
+  for (int l = B.low; l <= B.high; ++l) {
+    const LayerReg& L = ctx.layers[static_cast<size_t>(l - 1)];
+    const int64_t lb = L.off, le = L.off + L.numel;
+    const int64_t s = std::max(lb, cb), e = std::min(le, ce);
+    for (int64_t p = s; p < e; p += kUnitElems) {
+      const int64_t len = std::min(kUnitElems, e - p);
+      emit(l, p - lb, len, p - cb);
+    }
+  }
+}
+
+}  // namespace
+
+dear_local_group::~dear_local_group() {
+  for (auto& kv : bufs_dev) cudaFree(kv.second);
+  for (cudaEvent_t e : arrive)
+    if (e) cudaEventDestroy(e);
+  if (done) cudaEventDestroy(done);
+}
+
+void dear_local_group::run_collective(const Op& op) {
+  dear_ctx* c0 = ranks[0];
+  const Bucket& B0 = c0->buckets[static_cast<size_t>(op.bucket)];
+  auto it = bufs_dev.find(op.bucket);
+  if (it == bufs_dev.end()) {
+    std::vector<float*> h(static_cast<size_t>(P));
+    for (int r = 0; r < P; ++r) h[static_cast<size_t>(r)] = ranks[static_cast<size_t>(r)]->buckets[static_cast<size_t>(op.bucket)].buf;
+    float** d = nullptr;
+    cuda_check(cudaMalloc(&d, sizeof(float*) * static_cast<size_t>(P)), "cudaMalloc");
+    cuda_check(cudaMemcpy(d, h.data(), sizeof(float*) * static_cast<size_t>(P), cudaMemcpyHostToDevice),
+               "cudaMemcpy");
+    it = bufs_dev.emplace(op.bucket, d).first;
+  }
+  for (int r = 0; r < P; ++r) {
+    if (!arrive[r]) arrive[r] = new_event(false);
+    cuda_check(cudaEventRecord(arrive[r], ranks[static_cast<size_t>(r)]->comm_stream), "cudaEventRecord");
+    cuda_check(cudaStreamWaitEvent(c0->comm_stream, arrive[r], 0), "cudaStreamWaitEvent");
+  }
+  const int64_t count = B0.stride;
+  if (op.kind == OP_RS) {
+    cuda_check(launch_local_reduce_scatter(it->second, P, B0.stride, count, c0->comm_stream),
+               "local reduce-scatter");
+  } else {
+    cuda_check(launch_local_all_gather(it->second, P, B0.stride, count, c0->comm_stream),
+               "local all-gather");
+  }
+  if (!done) done = new_event(false);
+  cuda_check(cudaEventRecord(done, c0->comm_stream), "cudaEventRecord");
+  for (int r = 1; r < P; ++r)
+    cuda_check(cudaStreamWaitEvent(ranks[static_cast<size_t>(r)]->comm_stream, done, 0), "cudaStreamWaitEvent");
+}
+
+// Executes every rank's queued ops up to its next collective; a collective
+// runs once all P ranks have it at the head of their queues (the lock-step
+// rounds of collective.cpp:70-90, with the host as the round driver).
+void dear_local_group::drain() {
+  if (draining) return;
+  draining = true;
+  try {
+    for (;;) {
+      bool progress = false;
+      for (dear_ctx* c : ranks) {
+        if (!c) continue;
+        while (!c->queue.empty() && !c->queue.front().collective()) {
+          const Op op = c->queue.front();
+          c->queue.pop_front();
+          c->exec(op);
+          progress = true;
+        }
+      }
+      bool all_head = true;
+      for (dear_ctx* c : ranks) {
+        if (!c || c->queue.empty()) {
+          all_head = false;
+          break;
+        }
+      }
+      if (all_head) {
+        const Op& h = ranks[0]->queue.front();
+        for (dear_ctx* c : ranks) {
+          const Op& o = c->queue.front();
+          if (o.kind != h.kind || o.bucket != h.bucket) {
+            invalid("local group: ranks issued different collectives (out of lock-step)");
+          }
+        }
+        const Op op = h;
+        run_collective(op);
+        for (dear_ctx* c : ranks) {
+          c->queue.pop_front();
+          c->exec(op);  // post-collective bookkeeping (timing, trace)
+        }
+        progress = true;
+      }
+      if (!progress) break;
+    }
+  } catch (...) {
+    draining = false;
+    throw;
+  }
+  draining = false;
+}
+
+dear_ctx::~dear_ctx() {
+  if (comm_stream) cudaStreamSynchronize(comm_stream);
+  for (Bucket& b : buckets) {
+    free_events(b.ready_events);
+    if (b.ag_done) cudaEventDestroy(b.ag_done);
+    for (cudaEvent_t e : b.t)
+      if (e) cudaEventDestroy(e);
+  }
+  if (packed_ev) cudaEventDestroy(packed_ev);
+  if (step_ev) cudaEventDestroy(step_ev);
+  if (join_ev) cudaEventDestroy(join_ev);
+  if (arena) cudaFree(arena);
+  if (comm_stream) cudaStreamDestroy(comm_stream);
+  if (group) {
+    for (auto& r : group->ranks)
+      if (r == this) r = nullptr;
+  }
+}
+
+std::string dear_ctx::label(const char* kind, int b) const {
+  // task_label (task_graph.cpp:51-58): fused tasks name the group (gi+1);
+  // per-layer WFBP names the layer (subject = high_layer, :170).
+  const Bucket& B = buckets[static_cast<size_t>(b)];
+  if (!is_fused(cfg.policy) && !is_dear(cfg.policy)) {
+    return std::string(kind) + " l" + std::to_string(B.high);
+  }
+  return std::string(kind) + " g" + std::to_string(b + 1);
+}
+
+void dear_ctx::record_t(int b, int which) {
+  if (!timing) return;
+  Bucket& B = buckets[static_cast<size_t>(b)];
+  cuda_check(cudaEventRecord(B.t[which], comm_stream), "cudaEventRecord");
+  B.t_rec[which] = true;
+}
+
+void dear_ctx::exec(const Op& op) {
+  Bucket* B = op.bucket >= 0 ? &buckets[static_cast<size_t>(op.bucket)] : nullptr;
+  switch (op.kind) {
+    case OP_FENCE_READY:
+      for (cudaEvent_t e : B->ready_events)
+        cuda_check(cudaStreamWaitEvent(comm_stream, e, 0), "cudaStreamWaitEvent");
+      break;
+    case OP_FENCE_STEP:
+      cuda_check(cudaStreamWaitEvent(comm_stream, step_ev, 0), "cudaStreamWaitEvent");
+      break;
+    case OP_PACK:
+      record_t(op.bucket, T_PACK0);
+      cuda_check(launch_pack(B->pack_u, B->n_pack, pack_scale, comm_stream), "pack kernel");
+      cuda_check(cudaEventRecord(packed_ev, comm_stream), "cudaEventRecord");
+      record_t(op.bucket, T_PACK1);
+      break;
+    case OP_RS:
+      if (!local && P > 1 && B->stride > 0) {
+        nccl_check(ncclReduceScatter(B->buf, B->buf + static_cast<int64_t>(rank) * B->stride,
+                                     static_cast<size_t>(B->stride), ncclFloat32, ncclSum, comm,
+                                     comm_stream),
+                   "ncclReduceScatter");
+      }
+      record_t(op.bucket, T_RS1);
+      break;
+    case OP_UPDATE:
+      cuda_check(launch_update(B->upd_u, B->n_upd, hp_dev, B->mom_init ? 1 : 0,
+                               cfg.momentum != 0.0, cfg.weight_decay != 0.0, comm_stream),
+                 "update kernel");
+      if (cfg.momentum != 0.0) B->mom_init = true;
+      record_t(op.bucket, T_UPD1);
+      break;
+    case OP_AG:
+      if (!local) record_t(op.bucket, T_AG0);
+      if (!local && P > 1 && B->stride > 0) {
+        nccl_check(ncclAllGather(B->buf + static_cast<int64_t>(rank) * B->stride, B->buf,
+                                 static_cast<size_t>(B->stride), ncclFloat32, comm, comm_stream),
+                   "ncclAllGather");
+      }
+      record_t(op.bucket, T_AG1);
+      break;
+    case OP_UNPACK:
+      cuda_check(launch_unpack(B->unpack_u, B->n_unpack, B->any_shadow ? 1 : 0, comm_stream),
+                 "unpack kernel");
+      record_t(op.bucket, T_UNPACK1);
+      break;
+    case OP_AG_DONE:
+      cuda_check(cudaEventRecord(B->ag_done, comm_stream), "cudaEventRecord");
+      break;
+    case OP_CALLER_WAIT_PACKED:
+      cuda_check(cudaStreamWaitEvent(op.stream, packed_ev, 0), "cudaStreamWaitEvent");
+      break;
+  }
+}
+
+void dear_ctx::enqueue(Op op) {
+  if (!local) {
+    exec(op);
+    return;
+  }
+  queue.push_back(op);
+}
+
+void dear_ctx::enqueue_backpipe(int b) {
+  Bucket& B = buckets[static_cast<size_t>(b)];
+  enqueue({OP_FENCE_READY, b, nullptr});
+  enqueue({OP_PACK, b, nullptr});
+  enqueue({OP_RS, b, nullptr});
+  enqueue({OP_UPDATE, b, nullptr});
+  if (is_dear(cfg.policy)) {
+    trace.push_back(label("RS", b));
+  } else {
+    trace.push_back(label("AR", b));
+    enqueue({OP_AG, b, nullptr});
+    enqueue({OP_UNPACK, b, nullptr});
+    enqueue({OP_AG_DONE, b, nullptr});
+    B.ag_live = true;
+    B.waited_valid = false;
+  }
+  if (local) group->drain();
+}
+
+void dear_ctx::enqueue_feedpipe() {
+  // Reverse plan order = feed-forward order (task_graph.cpp:199-206).
+  enqueue({OP_FENCE_STEP, -1, nullptr});
+  for (int g = static_cast<int>(buckets.size()) - 1; g >= 0; --g) {
+    Bucket& B = buckets[static_cast<size_t>(g)];
+    enqueue({OP_AG, g, nullptr});
+    enqueue({OP_UNPACK, g, nullptr});
+    enqueue({OP_AG_DONE, g, nullptr});
+    trace.push_back(label("AG", g));
+    B.ag_live = true;
+    B.waited_valid = false;
+  }
+  ags_deferred = false;
+  if (local) group->drain();
+}
+
+void dear_ctx::complete_bucket(int b) {
+  Bucket& B = buckets[static_cast<size_t>(b)];
+  B.complete = true;
+  // Issue RS in plan order only (task_graph.cpp:186-194; NCCL ordering).
+  while (rs_cursor < static_cast<int>(buckets.size()) &&
+         buckets[static_cast<size_t>(rs_cursor)].complete) {
+    enqueue_backpipe(rs_cursor);
+    ++rs_cursor;
+  }
+}
+
+extern "C" {
+
+const char* dear_last_error(void) { return g_last_error.c_str(); }
+
+int dear_comm_unique_id(uint8_t id[128]) {
+  DEAR_API_BEGIN
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  ncclUniqueId u;
+  nccl_check(ncclGetUniqueId(&u), "ncclGetUniqueId");
+  memcpy(id, &u, 128);
+  DEAR_API_END
+}
+
+int dear_comm_init(void** comm, int32_t nranks, const uint8_t id[128], int32_t rank) {
+  DEAR_API_BEGIN
+  if (!comm || !id || nranks < 1 || rank < 0 || rank >= nranks) invalid("dear_comm_init: bad args");
+  ncclUniqueId u;
+  memcpy(&u, id, 128);
+  ncclComm_t c = nullptr;
+  nccl_check(ncclCommInitRank(&c, nranks, u, rank), "ncclCommInitRank");
+  *comm = c;
+  DEAR_API_END
+}
+
+int dear_comm_destroy(void* comm) {
+  DEAR_API_BEGIN
+  if (comm) nccl_check(ncclCommDestroy(static_cast<ncclComm_t>(comm)), "ncclCommDestroy");
+  DEAR_API_END
+}
+
+int dear_local_group_create(int32_t P, dear_local_group** group) {
+  DEAR_API_BEGIN
+  if (P < 1 || P > 64 || !group) invalid("dear_local_group_create: P must be in 1..64");
+  auto* g = new dear_local_group();
+  g->P = P;
+  g->ranks.assign(static_cast<size_t>(P), nullptr);
+  *group = g;
+  DEAR_API_END
+}
+
+int dear_local_group_destroy(dear_local_group* group) {
+  DEAR_API_BEGIN
+  if (group) {
+    for (dear_ctx* c : group->ranks)
+      if (c) invalid("dear_local_group_destroy: destroy the rank contexts first");
+    delete group;
+  }
+  DEAR_API_END
+}
+
+static void validate_cfg(const dear_cfg* cfg) {
+  if (!cfg) invalid("dear_create: cfg is null");
+  const int k = cfg->policy;
+  if (k == 2) invalid("PRIORITY_PARTITION is not supported by the runtime");
+  if (k != DEAR_POLICY_WFBP && k != DEAR_POLICY_WFBP_FUSED && k != DEAR_POLICY_DEAR &&
+      k != DEAR_POLICY_DEAR_FUSED)
+    invalid("unknown policy kind " + std::to_string(k));
+  if (is_fused(k) && cfg->fusion_buffer_bytes <= 0) {
+    invalid(std::string(k == DEAR_POLICY_WFBP_FUSED ? "WFBP_FUSED" : "DEAR_FUSED") +
+            " requires fusion_buffer_bytes > 0");
+  }
+  if (!(cfg->lr >= 0.0)) invalid("lr must be >= 0");
+  if (!(cfg->momentum >= 0.0)) invalid("momentum must be >= 0");
+  if (!(cfg->weight_decay >= 0.0)) invalid("weight_decay must be >= 0");
+  if (cfg->nesterov && (cfg->momentum <= 0.0 || cfg->dampening != 0.0))
+    invalid("Nesterov momentum requires a momentum and zero dampening");
+}
+
+static int create_common(dear_ctx* c, int32_t rank, int32_t P, void* compute_stream,
+                         const dear_cfg* cfg) {
+  validate_cfg(cfg);
+  if (P < 1 || rank < 0 || rank >= P) invalid("dear_create: rank must be in [0, P)");
+  c->rank = rank;
+  c->P = P;
+  c->cfg = *cfg;
+  c->compute = static_cast<cudaStream_t>(compute_stream);
+  cuda_check(cudaGetDevice(&c->device), "cudaGetDevice");
+  int lo = 0, hi = 0;
+  cuda_check(cudaDeviceGetStreamPriorityRange(&lo, &hi), "cudaDeviceGetStreamPriorityRange");
+  cuda_check(cudaStreamCreateWithPriority(&c->comm_stream, cudaStreamNonBlocking, hi),
+             "cudaStreamCreateWithPriority");
+  return DEAR_OK;
+}
+
+int dear_create(void* nccl_comm, int32_t rank, int32_t P, void* compute_stream, const dear_cfg* cfg,
+                dear_ctx** out) {
+  DEAR_API_BEGIN
+  if (!out) invalid("dear_create: out is null");
+  if (P > 1 && !nccl_comm) invalid("dear_create: an NCCL communicator is required when P > 1");
+  std::unique_ptr<dear_ctx> c(new dear_ctx());
+  create_common(c.get(), rank, P, compute_stream, cfg);
+  c->comm = static_cast<ncclComm_t>(nccl_comm);
+  if (c->comm) {
+    int n = 0, r = 0;
+    nccl_check(ncclCommCount(c->comm, &n), "ncclCommCount");
+    nccl_check(ncclCommUserRank(c->comm, &r), "ncclCommUserRank");
+    if (n != P || r != rank) invalid("dear_create: communicator size/rank do not match P/rank");
+  }
+  *out = c.release();
+  DEAR_API_END
+}
+
+int dear_create_local(dear_local_group* group, int32_t rank, void* compute_stream,
+                      const dear_cfg* cfg, dear_ctx** out) {
+  DEAR_API_BEGIN
+  if (!group || !out) invalid("dear_create_local: null argument");
+  if (rank < 0 || rank >= group->P) invalid("dear_create_local: rank out of range");
+  if (group->ranks[static_cast<size_t>(rank)]) invalid("dear_create_local: rank already created");
+  std::unique_ptr<dear_ctx> c(new dear_ctx());
+  create_common(c.get(), rank, group->P, compute_stream, cfg);
+  c->local = true;
+  c->group = group;
+  group->ranks[static_cast<size_t>(rank)] = c.get();
+  *out = c.release();
+  DEAR_API_END
+}
+
+static dear_ctx* need(dear_ctx* ctx, bool finalized) {
+  if (!ctx) invalid("null context");
+  if (finalized && !ctx->finalized) invalid("context is not finalized (call dear_finalize)");
+  if (!finalized && ctx->finalized) invalid("context is already finalized");
+  return ctx;
+}
+
+static void check_aligned(const void* p, const char* what, int32_t layer) {
+  if (reinterpret_cast<uintptr_t>(p) & 15) {
+    invalid(std::string(what) + " of layer " + std::to_string(layer) +
+            " must be 16-byte aligned");
+  }
+}
+
+int dear_register_tensor(dear_ctx* ctx, int32_t layer, float* param, float* grad, int64_t numel) {
+  DEAR_API_BEGIN
+  need(ctx, false);
+  if (layer < 1) invalid("dear_register_tensor: layer indices are 1-based");
+  if (numel < 0) invalid("model: param_count must be >= 0");
+  if (numel > 0 && (!param || !grad)) invalid("dear_register_tensor: null param/grad");
+  check_aligned(param, "param", layer);
+  check_aligned(grad, "grad", layer);
+  if (static_cast<size_t>(layer) > ctx->layers.size()) ctx->layers.resize(static_cast<size_t>(layer));
+  LayerReg& L = ctx->layers[static_cast<size_t>(layer - 1)];
+  if (L.numel >= 0) invalid("dear_register_tensor: layer " + std::to_string(layer) + " registered twice");
+  L.param = param;
+  L.grad = grad;
+  L.numel = numel;
+  DEAR_API_END
+}
+
+int dear_register_shadow(dear_ctx* ctx, int32_t layer, void* bf16_copy) {
+  DEAR_API_BEGIN
+  need(ctx, false);
+  if (layer < 1 || static_cast<size_t>(layer) > ctx->layers.size() ||
+      ctx->layers[static_cast<size_t>(layer - 1)].numel < 0)
+    invalid("dear_register_shadow: register the tensor first");
+  check_aligned(bf16_copy, "bf16 copy", layer);
+  ctx->layers[static_cast<size_t>(layer - 1)].shadow = bf16_copy;
+  DEAR_API_END
+}
+
+static uint64_t fnv(uint64_t h, uint64_t v) {
+  for (int i = 0; i < 8; ++i) {
+    h ^= (v >> (8 * i)) & 0xff;
+    h *= 1099511628211ULL;
+  }
+  return h;
+}
+
+int dear_finalize(dear_ctx* ctx) {
+  DEAR_API_BEGIN
+  need(ctx, false);
+  dear_ctx& c = *ctx;
+  const int L = static_cast<int>(c.layers.size());
+  if (L == 0) invalid("build_fusion_plan: empty model");
+  for (int i = 0; i < L; ++i) {
+    if (c.layers[static_cast<size_t>(i)].numel < 0) {
+      invalid("model: layer indices must be exactly 1..L; layer " + std::to_string(i + 1) +
+              " was not registered");
+    }
+  }
+  std::vector<int64_t> bytes(static_cast<size_t>(L));
+  for (int i = 0; i < L; ++i) bytes[static_cast<size_t>(i)] = c.layers[static_cast<size_t>(i)].numel * 4;
+  const auto plan = build_plan(bytes, is_fused(c.cfg.policy) ? c.cfg.fusion_buffer_bytes : 0);
+
+  // Bucket geometry and HBM layout: one arena holding every bucket buffer
+  // (P slots of `stride` fp32 each), the momentum shards and the unit tables.
+  c.buckets.resize(plan.size());
+  const bool mom = c.cfg.momentum != 0.0;
+  size_t floats = 0, units = 0;
+  for (size_t g = 0; g < plan.size(); ++g) {
+    Bucket& B = c.buckets[g];
+    B.low = plan[g].low;
+    B.high = plan[g].high;
+    int64_t off = 0;
+    for (int l = B.low; l <= B.high; ++l) {
+      LayerReg& R = c.layers[static_cast<size_t>(l - 1)];
+      R.bucket = static_cast<int>(g);
+      R.off = off;
+      off += R.numel;
+      if (R.shadow) B.any_shadow = true;
+    }
+    B.d = off;
+    B.stride = slot_stride(B.d, c.P);
+    floats += static_cast<size_t>(B.stride) * static_cast<size_t>(c.P) + (mom ? static_cast<size_t>(B.stride) : 0);
+  }
+  // Unit tables.
+  std::vector<Unit> host_units;
+  struct Span { size_t pack, upd, unpack; };
+  std::vector<Span> spans(plan.size());
+  std::vector<std::vector<int64_t>> begins(plan.size());
+  for (size_t g = 0; g < plan.size(); ++g) begins[g] = chunk_begins(c.buckets[g].d, c.P);
+  // First pass only counts; pointers are filled once the arena exists.
+  for (size_t g = 0; g < plan.size(); ++g) {
+    const Bucket& B = c.buckets[g];
+    const auto& bg = begins[g];
+    size_t n = 0;
+    for (int ch = 0; ch < c.P; ++ch)
+      for_each_piece(c, B, bg[static_cast<size_t>(ch)], bg[static_cast<size_t>(ch) + 1],
+                     [&](int, int64_t, int64_t, int64_t) { ++n; });
+    const int own = (c.rank + 1) % c.P;
+    size_t nu = 0;
+    for_each_piece(c, B, bg[static_cast<size_t>(own)], bg[static_cast<size_t>(own) + 1],
+                   [&](int, int64_t, int64_t, int64_t) { ++nu; });
+    units += 2 * n + nu;
+  }
+  const size_t float_bytes = (floats * sizeof(float) + 255) / 256 * 256;
+  const size_t unit_bytes = (units * sizeof(Unit) + 255) / 256 * 256;
+  const size_t total = float_bytes + unit_bytes + 256 + 256;
+  cuda_check(cudaMalloc(&c.arena, total), "cudaMalloc(bucket arena)");
+  cuda_check(cudaMemset(c.arena, 0, float_bytes), "cudaMemset");
+  float* fp = reinterpret_cast<float*>(c.arena);
+  Unit* up = reinterpret_cast<Unit*>(c.arena + float_bytes);
+  c.hp_dev = reinterpret_cast<HyperParams*>(c.arena + float_bytes + unit_bytes);
+  c.hash_dev = reinterpret_cast<unsigned long long*>(c.arena + float_bytes + unit_bytes + 256);
+  for (size_t g = 0; g < plan.size(); ++g) {
+    Bucket& B = c.buckets[g];
+    B.buf = fp;
+    fp += B.stride * c.P;
+    if (mom) {
+      B.mom = fp;
+      fp += B.stride;
+    }
+  }
+  host_units.reserve(units);
+  for (size_t g = 0; g < plan.size(); ++g) {
+    Bucket& B = c.buckets[g];
+    const auto& bg = begins[g];
+    // pack: every chunk c to slot owner(c) = (c-1) mod P.
+    B.pack_u = up + host_units.size();
+    for (int ch = 0; ch < c.P; ++ch) {
+      const int slot = (ch - 1 + c.P) % c.P;
+      for_each_piece(c, B, bg[static_cast<size_t>(ch)], bg[static_cast<size_t>(ch) + 1],
+                     [&](int l, int64_t j, int64_t len, int64_t pos) {
+                       const LayerReg& R = c.layers[static_cast<size_t>(l - 1)];
+                       host_units.push_back({R.grad + j, B.buf + slot * B.stride + pos, nullptr, len});
+                     });
+    }
+    B.n_pack = static_cast<int>(host_units.size() - static_cast<size_t>(B.pack_u - up));
+    // update: own chunk (rank+1) mod P, in slot `rank`.
+    B.upd_u = up + host_units.size();
+    const int own = (c.rank + 1) % c.P;
+    for_each_piece(c, B, bg[static_cast<size_t>(own)], bg[static_cast<size_t>(own) + 1],
+                   [&](int l, int64_t j, int64_t len, int64_t pos) {
+                     const LayerReg& R = c.layers[static_cast<size_t>(l - 1)];
+                     host_units.push_back({R.param + j, B.buf + c.rank * B.stride + pos,
+                                           B.mom ? static_cast<void*>(B.mom + pos) : nullptr, len});
+                   });
+    B.n_upd = static_cast<int>(host_units.size() - static_cast<size_t>(B.upd_u - up));
+    // unpack: every slot back to the layers (and their bf16 copies).
+    B.unpack_u = up + host_units.size();
+    for (int ch = 0; ch < c.P; ++ch) {
+      const int slot = (ch - 1 + c.P) % c.P;
+      for_each_piece(c, B, bg[static_cast<size_t>(ch)], bg[static_cast<size_t>(ch) + 1],
+                     [&](int l, int64_t j, int64_t len, int64_t pos) {
+                       const LayerReg& R = c.layers[static_cast<size_t>(l - 1)];
+                       void* sh = R.shadow ? static_cast<void*>(static_cast<uint16_t*>(R.shadow) + j) : nullptr;
+                       host_units.push_back({B.buf + slot * B.stride + pos, R.param + j, sh, len});
+                     });
+    }
+    B.n_unpack = static_cast<int>(host_units.size() - static_cast<size_t>(B.unpack_u - up));
+    B.ag_done = new_event(false);
+    for (int k = 0; k < T_COUNT; ++k) B.t[k] = new_event(true);
+    B.layers_left = B.high - B.low + 1;
+  }
+  if (!host_units.empty()) {
+    cuda_check(cudaMemcpy(up, host_units.data(), host_units.size() * sizeof(Unit), cudaMemcpyHostToDevice),
+               "cudaMemcpy(units)");
+  }
+  // Hyper-parameters; 1/P folded into pack when it is exact (P = 2^k).
+  const bool pow2 = (c.P & (c.P - 1)) == 0;
+  c.pack_scale = pow2 ? 1.0f / static_cast<float>(c.P) : 1.0f;
+  c.hp_host.lr = static_cast<float>(c.cfg.lr);
+  c.hp_host.momentum = static_cast<float>(c.cfg.momentum);
+  c.hp_host.one_minus_dampening = 1.0f - static_cast<float>(c.cfg.dampening);
+  c.hp_host.weight_decay = static_cast<float>(c.cfg.weight_decay);
+  c.hp_host.inv_p = 1.0f / static_cast<float>(c.P);
+  c.hp_host.nesterov = c.cfg.nesterov ? 1 : 0;
+  c.hp_host.prescaled = pow2 ? 1 : 0;
+  cuda_check(cudaMemcpy(c.hp_dev, &c.hp_host, sizeof(HyperParams), cudaMemcpyHostToDevice), "cudaMemcpy(hp)");
+  c.packed_ev = new_event(false);
+  c.step_ev = new_event(false);
+  c.join_ev = new_event(false);
+
+  // Every rank must have registered the same model (the precondition the
+  // reference checks as vector-length / replica equality, collective.cpp:172-186).
+  uint64_t h = 1469598103934665603ULL;
+  h = fnv(h, static_cast<uint64_t>(L));
+  for (const LayerReg& R : c.layers) h = fnv(h, static_cast<uint64_t>(R.numel));
+  h = fnv(h, static_cast<uint64_t>(c.cfg.policy));
+  h = fnv(h, static_cast<uint64_t>(c.cfg.fusion_buffer_bytes));
+  if (c.local) {
+    for (dear_ctx* o : c.group->ranks) {
+      if (o && o != &c && o->finalized) {
+        if (o->buckets.size() != c.buckets.size())
+          invalid("dear_finalize: ranks registered different models");
+        for (size_t g = 0; g < c.buckets.size(); ++g)
+          if (o->buckets[g].d != c.buckets[g].d || o->buckets[g].low != c.buckets[g].low)
+            invalid("dear_finalize: ranks registered different models");
+      }
+    }
+  } else if (c.P > 1) {
+    unsigned long long hv[2] = {h, ~h};
+    cuda_check(cudaMemcpy(c.hash_dev, hv, sizeof hv, cudaMemcpyHostToDevice), "cudaMemcpy");
+    nccl_check(ncclAllReduce(c.hash_dev, c.hash_dev, 2, ncclUint64, ncclMax, c.comm, c.comm_stream),
+               "ncclAllReduce(registration check)");
+    cuda_check(cudaMemcpyAsync(hv, c.hash_dev, sizeof hv, cudaMemcpyDeviceToHost, c.comm_stream), "cudaMemcpyAsync");
+    cuda_check(cudaStreamSynchronize(c.comm_stream), "cudaStreamSynchronize");
+    if (hv[0] != h || hv[1] != ~h) invalid("dear_finalize: ranks registered different models");
+  }
+  cuda_check(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+  c.finalized = true;
+  DEAR_API_END
+}
+
+int dear_grad_ready(dear_ctx* ctx, int32_t layer, void* stream) {
+  DEAR_API_BEGIN
+  need(ctx, true);
+  dear_ctx& c = *ctx;
+  if (layer < 1 || static_cast<size_t>(layer) > c.layers.size())
+    invalid("dear_grad_ready: layer " + std::to_string(layer) + " out of range");
+  LayerReg& R = c.layers[static_cast<size_t>(layer - 1)];
+  if (R.ready) invalid("dear_grad_ready: layer " + std::to_string(layer) + " reported twice in one iteration");
+  if (c.ags_deferred) invalid("dear_grad_ready: backward started before the deferred all-gathers were flushed");
+  R.ready = true;
+  ++c.reported;
+  if (c.reported == 1) c.trace.clear();
+  Bucket& B = c.buckets[static_cast<size_t>(R.bucket)];
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (std::find(B.ready_streams.begin(), B.ready_streams.end(), s) == B.ready_streams.end())
+    B.ready_streams.push_back(s);
+  if (--B.layers_left == 0) {
+    // All of the bucket's gradients are enqueued: fence each producing stream.
+    while (B.ready_events.size() < B.ready_streams.size()) B.ready_events.push_back(new_event(false));
+    for (size_t i = 0; i < B.ready_streams.size(); ++i)
+      cuda_check(cudaEventRecord(B.ready_events[i], B.ready_streams[i]), "cudaEventRecord");
+    B.ready_events.resize(B.ready_streams.size());
+    c.complete_bucket(R.bucket);
+  }
+  DEAR_API_END
+}
+
+int dear_step(dear_ctx* ctx, void* stream) {
+  DEAR_API_BEGIN
+  need(ctx, true);
+  dear_ctx& c = *ctx;
+  if (c.rs_cursor != static_cast<int>(c.buckets.size())) {
+    std::string missing;
+    for (size_t i = 0; i < c.layers.size(); ++i)
+      if (!c.layers[i].ready) missing += (missing.empty() ? "" : ",") + std::to_string(i + 1);
+    invalid("dear_step: gradients not reported for layers [" + missing + "]");
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // Both directions of the barrier: gradients are consumed (packed) before the
+  // caller may overwrite them; parameters are rewritten only after the
+  // caller's backward work.
+  cuda_check(cudaEventRecord(c.step_ev, s), "cudaEventRecord");
+  c.enqueue({OP_CALLER_WAIT_PACKED, -1, s});
+  if (is_dear(c.cfg.policy)) {
+    if (c.cfg.defer_allgather) {
+      c.ags_deferred = true;
+    } else {
+      c.enqueue_feedpipe();
+    }
+  } else if (c.local) {
+    c.group->drain();
+  }
+  for (LayerReg& R : c.layers) R.ready = false;
+  for (Bucket& B : c.buckets) {
+    B.complete = false;
+    B.layers_left = B.high - B.low + 1;
+    B.ready_streams.clear();
+  }
+  c.rs_cursor = 0;
+  c.reported = 0;
+  ++c.iteration;
+  DEAR_API_END
+}
+
+int dear_param_wait(dear_ctx* ctx, int32_t layer, void* stream) {
+  DEAR_API_BEGIN
+  need(ctx, true);
+  dear_ctx& c = *ctx;
+  if (layer < 1 || static_cast<size_t>(layer) > c.layers.size())
+    invalid("dear_param_wait: layer " + std::to_string(layer) + " out of range");
+  if (c.ags_deferred) {
+    if (c.local) {
+      // The group flushes together: a local collective needs every rank.
+      for (dear_ctx* o : c.group->ranks)
+        if (o && o->ags_deferred) o->enqueue_feedpipe();
+    } else {
+      c.enqueue_feedpipe();
+    }
+  }
+  Bucket& B = c.buckets[static_cast<size_t>(c.layers[static_cast<size_t>(layer - 1)].bucket)];
+  if (!B.ag_live) return DEAR_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (B.waited_valid && B.waited == s) return DEAR_OK;
+  if (c.local) {
+    c.group->drain();
+    if (!c.queue.empty()) invalid("dear_param_wait: local group ranks are out of lock-step");
+  }
+  cuda_check(cudaStreamWaitEvent(s, B.ag_done, 0), "cudaStreamWaitEvent");
+  B.waited = s;
+  B.waited_valid = true;
+  DEAR_API_END
+}
+
+int dear_join(dear_ctx* ctx, void* stream) {
+  DEAR_API_BEGIN
+  need(ctx, true);
+  if (ctx->local) ctx->group->drain();
+  cuda_check(cudaEventRecord(ctx->join_ev, ctx->comm_stream), "cudaEventRecord");
+  cuda_check(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), ctx->join_ev, 0), "cudaStreamWaitEvent");
+  DEAR_API_END
+}
+
+int dear_synchronize(dear_ctx* ctx) {
+  DEAR_API_BEGIN
+  need(ctx, true);
+  if (ctx->local) {
+    for (dear_ctx* o : ctx->group->ranks)
+      if (o && o->ags_deferred) o->enqueue_feedpipe();
+    ctx->group->drain();
+    if (!ctx->queue.empty()) invalid("dear_synchronize: other ranks of the local group lag behind");
+  }
+  else if (ctx->ags_deferred) {
+    ctx->enqueue_feedpipe();
+  }
+  cuda_check(cudaStreamSynchronize(ctx->comm_stream), "cudaStreamSynchronize");
+  DEAR_API_END
+}
+
+int dear_destroy(dear_ctx* ctx) {
+  DEAR_API_BEGIN
+  delete ctx;
+  DEAR_API_END
+}
+
+int dear_set_lr(dear_ctx* ctx, double lr) {
+  DEAR_API_BEGIN
+  need(ctx, true);
+  if (!(lr >= 0.0)) invalid("lr must be >= 0");
+  ctx->cfg.lr = lr;
+  ctx->hp_host.lr = static_cast<float>(lr);
+  // Stream-ordered on the comm stream, so updates already enqueued keep the
+  // old value. The source is a field of the context, read at enqueue time by
+  // the copy engine only after prior comm work; keep a per-call copy alive.
+  static thread_local HyperParams staged;
+  staged = ctx->hp_host;
+  cuda_check(cudaMemcpyAsync(ctx->hp_dev, &staged, sizeof(HyperParams), cudaMemcpyHostToDevice,
+                             ctx->comm_stream),
+             "cudaMemcpyAsync(hp)");
+  cuda_check(cudaStreamSynchronize(ctx->comm_stream), "cudaStreamSynchronize");
+  DEAR_API_END
+}
+
+int dear_num_buckets(dear_ctx* ctx, int32_t* n) {
+  DEAR_API_BEGIN
+  need(ctx, true);
+  *n = static_cast<int32_t>(ctx->buckets.size());
+  DEAR_API_END
+}
+
+int dear_bucket_info(dear_ctx* ctx, int32_t g, int32_t* low, int32_t* high, int64_t* elems,
+                     int64_t* stride) {
+  DEAR_API_BEGIN
+  need(ctx, true);
+  if (g < 0 || static_cast<size_t>(g) >= ctx->buckets.size()) invalid("bucket index out of range");
+  const Bucket& B = ctx->buckets[static_cast<size_t>(g)];
+  if (low) *low = B.low;
+  if (high) *high = B.high;
+  if (elems) *elems = B.d;
+  if (stride) *stride = B.stride;
+  DEAR_API_END
+}
+
+int dear_trace(dear_ctx* ctx, char* buf, int64_t cap, int64_t* needed) {
+  DEAR_API_BEGIN
+  if (!ctx) invalid("null context");
+  std::string s;
+  for (const auto& t : ctx->trace) s += t + "\n";
+  if (needed) *needed = static_cast<int64_t>(s.size()) + 1;
+  if (buf && cap > 0) {
+    const size_t n = std::min(static_cast<size_t>(cap - 1), s.size());
+    memcpy(buf, s.data(), n);
+    buf[n] = 0;
+  }
+  DEAR_API_END
+}
+
+int dear_set_timing(dear_ctx* ctx, int32_t enable) {
+  DEAR_API_BEGIN
+  need(ctx, true);
+  ctx->timing = enable != 0;
+  for (Bucket& B : ctx->buckets)
+    for (bool& r : B.t_rec) r = false;
+  DEAR_API_END
+}
+
+int dear_get_timings(dear_ctx* ctx, float* out, int32_t n_buckets) {
+  DEAR_API_BEGIN
+  need(ctx, true);
+  if (n_buckets != static_cast<int32_t>(ctx->buckets.size())) invalid("dear_get_timings: bucket count mismatch");
+  auto span = [&](const Bucket& B, int a, int b) -> float {
+    if (!B.t_rec[a] || !B.t_rec[b]) return -1.f;
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, B.t[a], B.t[b]) != cudaSuccess) return -1.f;
+    return ms;
+  };
+  for (size_t g = 0; g < ctx->buckets.size(); ++g) {
+    const Bucket& B = ctx->buckets[g];
+    float* o = out + g * 5;
+    o[0] = span(B, T_PACK0, T_PACK1);
+    o[1] = span(B, T_PACK1, T_RS1);
+    o[2] = span(B, T_RS1, T_UPD1);
+    o[3] = span(B, T_AG0, T_AG1);
+    o[4] = span(B, T_AG1, T_UNPACK1);
+  }
+  DEAR_API_END
+}
+
+static unsigned long long hash_params(dear_ctx& c) {
+  cuda_check(cudaMemsetAsync(c.hash_dev, 0, sizeof(unsigned long long), c.comm_stream), "cudaMemsetAsync");
+  for (size_t i = 0; i < c.layers.size(); ++i)
+    cuda_check(launch_hash(c.layers[i].param, c.layers[i].numel, 0x9E3779B97F4A7C15ULL * (i + 1),
+                           c.hash_dev, c.comm_stream),
+               "hash kernel");
+  unsigned long long h = 0;
+  cuda_check(cudaMemcpyAsync(&h, c.hash_dev, sizeof h, cudaMemcpyDeviceToHost, c.comm_stream), "cudaMemcpyAsync");
+  cuda_check(cudaStreamSynchronize(c.comm_stream), "cudaStreamSynchronize");
+  return h;
+}
+
+int dear_check_replicas(dear_ctx* ctx, int32_t* identical) {
+  DEAR_API_BEGIN
+  need(ctx, true);
+  dear_ctx& c = *ctx;
+  if (c.ags_deferred) c.enqueue_feedpipe();
+  cuda_check(cudaStreamSynchronize(c.comm_stream), "cudaStreamSynchronize");
+  const unsigned long long h = hash_params(c);
+  if (c.local) {
+    bool same = true;
+    for (dear_ctx* o : c.group->ranks) {
+      if (!o || o == &c) continue;
+      cuda_check(cudaStreamSynchronize(o->comm_stream), "cudaStreamSynchronize");
+      if (hash_params(*o) != h) same = false;
+    }
+    *identical = same ? 1 : 0;
+  } else if (c.P > 1) {
+    unsigned long long hv[2] = {h, ~h};
+    cuda_check(cudaMemcpy(c.hash_dev, hv, sizeof hv, cudaMemcpyHostToDevice), "cudaMemcpy");
+    nccl_check(ncclAllReduce(c.hash_dev, c.hash_dev, 2, ncclUint64, ncclMax, c.comm, c.comm_stream),
+               "ncclAllReduce(replica check)");
+    unsigned long long out[2];
+    cuda_check(cudaMemcpyAsync(out, c.hash_dev, sizeof out, cudaMemcpyDeviceToHost, c.comm_stream), "cudaMemcpyAsync");
+    cuda_check(cudaStreamSynchronize(c.comm_stream), "cudaStreamSynchronize");
+    *identical = (out[0] == h && out[1] == ~h) ? 1 : 0;
+  } else {
+    *identical = 1;
+  }
+  DEAR_API_END
+}
+
+}  // extern "C"

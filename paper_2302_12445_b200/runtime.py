@@ -1,0 +1,212 @@
+"""Python face of the native DeAR runtime (one context per GPU / rank).
+
+This is a thin object wrapper over the C ABI in ``include/dear.h``; every
+call goes to ``libdear.so`` and errors surface as :class:`DearError`
+(``ValueError`` subclass for invalid arguments). Reference counterparts:
+
+==========================  ===============================================
+``Runtime.register``        LayerSpec / ModelSpec (model.hpp:26-45)
+``Runtime.finalize``        build_fusion_plan / per_layer_plan (fusion.cpp)
+``Runtime.grad_ready``      RS_g <- BP of g's layers (task_graph.cpp:148-194)
+``Runtime.step``            BARRIER + AG issue (task_graph.cpp:195-206)
+``Runtime.param_wait``      FF_l <- AG_g(l) (task_graph.cpp:207)
+``Runtime.check_replicas``  "replica divergence" check (collective.cpp:172)
+==========================  ===============================================
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional
+
+import torch
+
+from ._lib import POLICIES, DearCfg, check, lib
+
+
+def _stream_ptr(stream: Optional[torch.cuda.Stream]) -> int:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream
+
+
+class Communicator:
+    """An NCCL communicator (one rank per process / GPU) over NVLink/NVSwitch."""
+
+    def __init__(self, rank: int, world_size: int, unique_id: bytes):
+        if len(unique_id) != 128:
+            raise ValueError("NCCL unique id must be 128 bytes")
+        self.rank, self.world_size = rank, world_size
+        self._comm = C.c_void_p()
+        check(lib().dear_comm_init(C.byref(self._comm), world_size, unique_id, rank))
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        check(lib().dear_comm_unique_id(buf))
+        return buf.raw
+
+    @classmethod
+    def from_torch_distributed(cls, group=None) -> "Communicator":
+        """Bootstrap over an initialised torch.distributed group (any backend):
+        rank 0 creates the NCCL id, every rank receives it via broadcast."""
+        import torch.distributed as dist
+
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        obj = [cls.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group else 0,
+                                   group=group)
+        return cls(rank, world, obj[0])
+
+    @property
+    def handle(self) -> int:
+        return self._comm.value or 0
+
+    def close(self) -> None:
+        if self._comm.value:
+            check(lib().dear_comm_destroy(self._comm))
+            self._comm = C.c_void_p()
+
+
+class LocalGroup:
+    """P ranks emulated in one process on one device (ring-order collectives).
+
+    Drive the P contexts in lock-step: every rank makes the same sequence of
+    calls, and all ranks finish an iteration's ``step`` before any rank starts
+    the next forward."""
+
+    def __init__(self, P: int):
+        self.P = P
+        self._g = C.c_void_p()
+        check(lib().dear_local_group_create(P, C.byref(self._g)))
+
+    @property
+    def handle(self) -> int:
+        return self._g.value
+
+    def close(self) -> None:
+        if self._g.value:
+            check(lib().dear_local_group_destroy(self._g))
+            self._g = C.c_void_p()
+
+
+class Runtime:
+    """One DeAR context: registered tensors, fusion buckets, comm stream."""
+
+    def __init__(self, comm=None, rank: int = 0, world_size: int = 1, *,
+                 policy: str = "DEAR_FUSED", fusion_buffer_bytes: int = 25_000_000,
+                 lr: float = 0.05, momentum: float = 0.0, dampening: float = 0.0,
+                 weight_decay: float = 0.0, nesterov: bool = False,
+                 dear_group_dependency: bool = False, defer_allgather: bool = False,
+                 stream: Optional[torch.cuda.Stream] = None):
+        if policy not in POLICIES:
+            raise ValueError(f"unknown policy kind {policy!r}; expected one of "
+                             f"{', '.join(POLICIES)}")
+        self.policy = policy
+        cfg = DearCfg(POLICIES[policy], int(fusion_buffer_bytes) if "FUSED" in policy else 0,
+                      int(dear_group_dependency), float(lr),
+                      float(momentum), float(dampening), float(weight_decay), int(nesterov),
+                      int(defer_allgather))
+        self._ctx = C.c_void_p()
+        sp = _stream_ptr(stream)
+        if isinstance(comm, LocalGroup):
+            self.rank, self.world_size = rank, comm.P
+            check(lib().dear_create_local(comm.handle, rank, sp, C.byref(cfg),
+                                          C.byref(self._ctx)))
+        else:
+            if isinstance(comm, Communicator):
+                rank, world_size, handle = comm.rank, comm.world_size, comm.handle
+            else:
+                handle = 0
+            self.rank, self.world_size = rank, world_size
+            check(lib().dear_create(handle or None, rank, world_size, sp, C.byref(cfg),
+                                    C.byref(self._ctx)))
+        self._keep = []  # tensors whose storage the runtime points at
+
+    # -- registration ----------------------------------------------------
+    def register(self, layer: int, param: torch.Tensor, grad: torch.Tensor,
+                 shadow: Optional[torch.Tensor] = None) -> None:
+        for name, t in (("param", param), ("grad", grad)):
+            if t.dtype != torch.float32 or not t.is_cuda or not t.is_contiguous():
+                raise ValueError(f"{name} of layer {layer} must be a contiguous CUDA fp32 tensor")
+        if param.numel() != grad.numel():
+            raise ValueError(f"param/grad size mismatch for layer {layer}")
+        check(lib().dear_register_tensor(self._ctx, layer, param.data_ptr(), grad.data_ptr(),
+                                         param.numel()))
+        self._keep += [param, grad]
+        if shadow is not None:
+            if shadow.dtype != torch.bfloat16 or shadow.numel() < param.numel():
+                raise ValueError(f"shadow of layer {layer} must be bf16 with >= numel elements")
+            check(lib().dear_register_shadow(self._ctx, layer, shadow.data_ptr()))
+            self._keep.append(shadow)
+
+    def finalize(self) -> None:
+        check(lib().dear_finalize(self._ctx))
+
+    # -- schedule hooks ----------------------------------------------------
+    def grad_ready(self, layer: int, stream=None) -> None:
+        check(lib().dear_grad_ready(self._ctx, layer, _stream_ptr(stream)))
+
+    def param_wait(self, layer: int, stream=None) -> None:
+        check(lib().dear_param_wait(self._ctx, layer, _stream_ptr(stream)))
+
+    def step(self, stream=None) -> None:
+        check(lib().dear_step(self._ctx, _stream_ptr(stream)))
+
+    def join(self, stream=None) -> None:
+        check(lib().dear_join(self._ctx, _stream_ptr(stream)))
+
+    def synchronize(self) -> None:
+        check(lib().dear_synchronize(self._ctx))
+
+    def set_lr(self, lr: float) -> None:
+        check(lib().dear_set_lr(self._ctx, float(lr)))
+
+    # -- introspection -------------------------------------------------------
+    def buckets(self) -> list[dict]:
+        n = C.c_int32(0)
+        check(lib().dear_num_buckets(self._ctx, C.byref(n)))
+        out = []
+        for g in range(n.value):
+            lo, hi, d, s = C.c_int32(), C.c_int32(), C.c_int64(), C.c_int64()
+            check(lib().dear_bucket_info(self._ctx, g, C.byref(lo), C.byref(hi), C.byref(d),
+                                         C.byref(s)))
+            out.append({"low": lo.value, "high": hi.value, "elems": d.value,
+                        "slot_stride": s.value})
+        return out
+
+    def trace(self) -> list[str]:
+        need = C.c_int64(0)
+        check(lib().dear_trace(self._ctx, None, 0, C.byref(need)))
+        buf = C.create_string_buffer(int(need.value))
+        check(lib().dear_trace(self._ctx, buf, need.value, C.byref(need)))
+        return [x for x in buf.value.decode().split("\n") if x]
+
+    def set_timing(self, enable: bool) -> None:
+        check(lib().dear_set_timing(self._ctx, int(enable)))
+
+    def timings(self) -> list[dict]:
+        """Per bucket (plan order) milliseconds of pack/rs/update/ag/unpack; None
+        where the stage did not run in the last timed iteration."""
+        n = len(self.buckets())
+        arr = (C.c_float * (5 * n))()
+        check(lib().dear_get_timings(self._ctx, arr, n))
+        keys = ("pack", "rs", "update", "ag", "unpack")
+        return [{k: (arr[5 * g + i] if arr[5 * g + i] >= 0 else None)
+                 for i, k in enumerate(keys)} for g in range(n)]
+
+    def check_replicas(self) -> bool:
+        ok = C.c_int32(0)
+        check(lib().dear_check_replicas(self._ctx, C.byref(ok)))
+        return bool(ok.value)
+
+    def close(self) -> None:
+        if self._ctx.value:
+            check(lib().dear_destroy(self._ctx))
+            self._ctx = C.c_void_p()
+            self._keep = []
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,46 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
+    config.addinivalue_line("markers", "multigpu: needs >= 2 CUDA devices (NCCL)")
+
+
+def pytest_collection_modifyitems(config, items):
+    try:
+        import torch
+
+        have_gpu = torch.cuda.is_available()
+        n_gpu = torch.cuda.device_count() if have_gpu else 0
+    except Exception:
+        have_gpu, n_gpu = False, 0
+    skip_gpu = pytest.mark.skip(reason="no CUDA device")
+    skip_multi = pytest.mark.skip(reason="needs >= 2 CUDA devices")
+    for item in items:
+        if "gpu" in item.keywords and not have_gpu:
+            item.add_marker(skip_gpu)
+        if "multigpu" in item.keywords and n_gpu < 2:
+            item.add_marker(skip_multi)
+
+
+@pytest.fixture(scope="session")
+def restated():
+    from oracle.lib import Restated
+
+    return Restated()
+
+
+@pytest.fixture(scope="session")
+def reference():
+    from oracle.lib import REF_SO, REF_SRC, Reference
+
+    if not os.path.exists(REF_SO) and not os.path.exists(REF_SRC):
+        pytest.skip("oracle/_ref not built and /root/reference absent")
+    return Reference()

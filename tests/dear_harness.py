@@ -1,0 +1,132 @@
+"""Shared test harness: drive the DeAR runtime on seeded inputs and compute the
+oracle's expectation for the same inputs (tests only)."""
+from __future__ import annotations
+
+import numpy as np
+
+from oracle.lib import Restated
+from oracle.schedule import fusion_plan
+
+
+def bucket_plan(numels, policy: str, buffer_bytes: int):
+    fused = "FUSED" in policy
+    return fusion_plan([4 * n for n in numels], buffer_bytes if fused else 0)
+
+
+def seeded_grads(o: Restated, P: int, numels, step: int, seed0: int = 1000) -> np.ndarray:
+    """Rank-major [P, D] fp32 gradients, U(-1,1) from the reference tests'
+    generator (mt19937_64 + uniform_real_distribution), one seed per step."""
+    D = int(sum(numels))
+    return o.random_vectors(P, D, seed0 + step).astype(np.float32)
+
+
+def initial_weights(o: Restated, numels, seed: int = 77) -> np.ndarray:
+    D = int(sum(numels))
+    return o.random_vectors(1, D, seed)[0].astype(np.float32)
+
+
+def oracle_run(o: Restated, numels, P: int, steps: int, policy: str, buffer_bytes: int,
+               lr: float, momentum=0.0, dampening=0.0, weight_decay=0.0, nesterov=False,
+               f32: bool = True, seed0: int = 1000, wseed: int = 77):
+    """Apply the oracle's S-SGD step per fusion bucket (chunk layout is per
+    bucket), for `steps` steps. f32=True uses the fp32 ring-order
+    restatement (bit-exact target for the local group); f32=False the fp64
+    restatement of collective.cpp (tolerance target)."""
+    offs = np.concatenate([[0], np.cumsum(numels)]).astype(np.int64)
+    w = initial_weights(o, numels, wseed)
+    w = w.astype(np.float32 if f32 else np.float64)
+    bufs = {}
+    plan = bucket_plan(numels, policy, buffer_bytes)
+    prescale = (P & (P - 1)) == 0
+    for s in range(steps):
+        g = seeded_grads(o, P, numels, s, seed0)
+        for lo, hi in plan:
+            a, b = offs[lo - 1], offs[hi]
+            if b == a:
+                continue
+            gb = g[:, a:b]
+            key = (lo, hi)
+            if f32:
+                buf, has = bufs.get(key, (np.zeros(b - a, np.float32), False))
+                nw, nbuf, nhas = o.sgd_step_f32(w[a:b], buf, has, gb, lr, momentum, dampening,
+                                                weight_decay, nesterov, prescale)
+            else:
+                buf, has = bufs.get(key, (np.zeros(b - a, np.float64), False))
+                if momentum == 0.0 and weight_decay == 0.0:
+                    nw = o.sgd_step(w[a:b], gb.astype(np.float64), lr)
+                    nbuf, nhas = buf, has
+                else:
+                    nw, nbuf, nhas = o.sgd_step_momentum(w[a:b], buf, has, gb.astype(np.float64),
+                                                         lr, momentum, dampening, weight_decay,
+                                                         nesterov)
+            w[a:b] = nw
+            bufs[key] = (nbuf, nhas)
+    return w
+
+
+def run_local(numels, P: int, steps: int, policy: str, buffer_bytes: int, lr: float,
+              momentum=0.0, dampening=0.0, weight_decay=0.0, nesterov=False,
+              defer_allgather=False, seed0: int = 1000, wseed: int = 77, shadow: bool = False):
+    """Drive P local-group ranks in lock-step through `steps` iterations of
+    backward (layers L..1) + step + forward waits. Returns (params [P, D],
+    shadows or None, traces, runtimes-closed)."""
+    import torch
+
+    from paper_2302_12445_b200 import LocalGroup, Runtime
+
+    o = Restated()
+    dev = torch.device("cuda")
+    L = len(numels)
+    offs = np.concatenate([[0], np.cumsum(numels)]).astype(np.int64)
+    w0 = initial_weights(o, numels, wseed)
+    group = LocalGroup(P)
+    rts, params, grads, shadows = [], [], [], []
+    for r in range(P):
+        rt = Runtime(group, r, P, policy=policy, fusion_buffer_bytes=buffer_bytes, lr=lr,
+                     momentum=momentum, dampening=dampening, weight_decay=weight_decay,
+                     nesterov=nesterov, defer_allgather=defer_allgather)
+        ps, gs, ss = [], [], []
+        for l in range(1, L + 1):
+            a, b = offs[l - 1], offs[l]
+            p = torch.from_numpy(w0[a:b].copy()).to(dev)
+            g = torch.zeros_like(p)
+            sh = torch.zeros(max(b - a, 1), dtype=torch.bfloat16, device=dev) if shadow else None
+            rt.register(l, p, g, sh)
+            ps.append(p)
+            gs.append(g)
+            ss.append(sh)
+        rts.append(rt)
+        params.append(ps)
+        grads.append(gs)
+        shadows.append(ss)
+    for rt in rts:
+        rt.finalize()
+    traces = []
+    for s in range(steps):
+        G = seeded_grads(o, P, numels, s, seed0)
+        # forward of iteration s: wait for each layer's bucket (flushes AGs)
+        for l in range(1, L + 1):
+            for r in range(P):
+                rts[r].param_wait(l)
+        for l in range(L, 0, -1):
+            a, b = offs[l - 1], offs[l]
+            for r in range(P):
+                grads[r][l - 1].copy_(torch.from_numpy(G[r, a:b].copy()).to(dev))
+                rts[r].grad_ready(l)
+        for r in range(P):
+            rts[r].step()
+        traces.append([rt.trace() for rt in rts])
+    for rt in rts:
+        rt.synchronize()
+    torch.cuda.synchronize()
+    out = np.stack([np.concatenate([p.cpu().numpy() for p in params[r]]) if L else np.zeros(0)
+                    for r in range(P)])
+    sh_out = None
+    if shadow:
+        sh_out = np.stack([np.concatenate([s[: numels[i]].float().cpu().numpy()
+                                           for i, s in enumerate(shadows[r])]) for r in range(P)])
+    same = [rt.check_replicas() for rt in rts]
+    for rt in rts:
+        rt.close()
+    group.close()
+    return out, sh_out, traces, same
