@@ -1,0 +1,48 @@
+/*
+ * dear_gemm.h — hand-written sm_100a tcgen05/TMA GEMM for the synthetic
+ * per-layer compute that DeAR's collectives overlap with.
+ *
+ * The reference has no layer math (LayerSpec carries only t_ff / t_bp
+ * durations, model.hpp:30-31); BASELINE.json asks for "synthetic layer
+ * compute" with a tcgen05 GEMM so feed-forward / backprop are real dense
+ * contractions on the tensor cores.
+ *
+ *   D[m, n] (+)= sum_k A[m, k] * B[n, k]        bf16 x bf16 -> fp32 accumulate
+ *
+ *   A : K-major, element (m, k) at A[m * lda + k]
+ *   B : K-major (b_mn_major = 0): (n, k) at B[n * ldb + k]
+ *       MN-major (b_mn_major = 1): (n, k) at B[k * ldb + n]
+ *   D : row-major, (m, n) at D[m * ldd + n], fp32 (d_fp32 = 1) or bf16.
+ *       Elements with m * ldd + n >= d_limit are not written (d_limit < 0:
+ *       no flat bound) — lets a weight gradient land in a flat parameter
+ *       tensor whose last row is partial.
+ *   accumulate = 1: D += result with fp32 reductions (requires fp32 D; the
+ *       K dimension may then be split across CTAs, split_k = 0 picks it).
+ *   Leading dimensions must be multiples of 8 elements, bases 16 B aligned.
+ */
+#ifndef DEAR_GEMM_H_
+#define DEAR_GEMM_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct dear_gemm_plan dear_gemm_plan;
+
+int dear_gemm_plan_create(const void* A, int64_t lda, const void* B, int64_t ldb,
+                          int32_t b_mn_major, void* D, int64_t ldd, int32_t d_fp32, int64_t M,
+                          int64_t N, int64_t K, int64_t d_limit, int32_t accumulate,
+                          int32_t split_k, dear_gemm_plan** out);
+/* Enqueue on `stream` (cudaStream_t as void*). */
+int dear_gemm_run(dear_gemm_plan* plan, void* stream);
+/* Tile geometry actually used: BN, grid.x (N tiles), grid.y (M tiles), splits. */
+int dear_gemm_plan_info(dear_gemm_plan* plan, int32_t* bn, int32_t* n_tiles, int32_t* m_tiles,
+                        int32_t* splits);
+int dear_gemm_plan_destroy(dear_gemm_plan* plan);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DEAR_GEMM_H_ */

@@ -1,0 +1,88 @@
+"""Python binding of the sm_100a tcgen05/TMA GEMM (include/dear_gemm.h).
+
+Used for the synthetic per-layer compute (feed-forward, data-gradient and
+weight-gradient contractions) that the DeAR collectives overlap with. No
+fallback: the plan calls the native kernel or raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from ._lib import check, lib
+
+_bound = False
+
+
+def _bind():
+    global _bound
+    if _bound:
+        return lib()
+    L = lib()
+    P = C.c_void_p
+    L.dear_gemm_plan_create.argtypes = [P, C.c_int64, P, C.c_int64, C.c_int32, P, C.c_int64,
+                                        C.c_int32, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
+                                        C.c_int32, C.c_int32, C.POINTER(P)]
+    L.dear_gemm_run.argtypes = [P, P]
+    L.dear_gemm_plan_info.argtypes = [P] + [C.POINTER(C.c_int32)] * 4
+    L.dear_gemm_plan_destroy.argtypes = [P]
+    for f in ("dear_gemm_plan_create", "dear_gemm_run", "dear_gemm_plan_info",
+              "dear_gemm_plan_destroy"):
+        getattr(L, f).restype = C.c_int
+    _bound = True
+    return L
+
+
+class GemmPlan:
+    """D[M,N] (+)= A[M,K] @ B^T, bf16 inputs, fp32 accumulation.
+
+    a: [M, K] bf16 (K contiguous). b: [N, K] bf16 (``b_mn_major=False``) or
+    [K, N] bf16 (``b_mn_major=True``). d: [M, ldd] fp32 / bf16 view or a flat
+    tensor (``d_limit`` = number of valid flat elements, for partial rows).
+    """
+
+    def __init__(self, a: torch.Tensor, b: torch.Tensor, d: torch.Tensor, M: int, N: int,
+                 K: int, *, b_mn_major: bool = False, lda: int | None = None,
+                 ldb: int | None = None, ldd: int | None = None, d_limit: int = -1,
+                 accumulate: bool = False, split_k: int = 0):
+        L = _bind()
+        for t in (a, b):
+            if t.dtype != torch.bfloat16 or not t.is_cuda:
+                raise ValueError("GEMM operands must be CUDA bf16 tensors")
+        if d.dtype not in (torch.float32, torch.bfloat16):
+            raise ValueError("D must be fp32 or bf16")
+        lda = lda if lda is not None else a.stride(0)
+        ldb = ldb if ldb is not None else b.stride(0)
+        ldd = ldd if ldd is not None else (d.stride(0) if d.dim() == 2 else N)
+        self._keep = (a, b, d)
+        self._plan = C.c_void_p()
+        check(L.dear_gemm_plan_create(a.data_ptr(), lda, b.data_ptr(), ldb, int(b_mn_major),
+                                      d.data_ptr(), ldd, int(d.dtype == torch.float32), M, N,
+                                      K, d_limit, int(accumulate), split_k,
+                                      C.byref(self._plan)))
+        self.M, self.N, self.K = M, N, K
+
+    def run(self, stream: torch.cuda.Stream | None = None) -> None:
+        s = (stream or torch.cuda.current_stream()).cuda_stream
+        check(_bind().dear_gemm_run(self._plan, s))
+
+    def info(self) -> dict:
+        v = [C.c_int32() for _ in range(4)]
+        check(_bind().dear_gemm_plan_info(self._plan, *[C.byref(x) for x in v]))
+        return dict(zip(("bn", "n_tiles", "m_tiles", "splits"), (x.value for x in v)))
+
+    @property
+    def flops(self) -> int:
+        return 2 * self.M * self.N * self.K
+
+    def close(self) -> None:
+        if self._plan.value:
+            check(_bind().dear_gemm_plan_destroy(self._plan))
+            self._plan = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

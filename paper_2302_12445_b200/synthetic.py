@@ -1,0 +1,124 @@
+"""Synthetic per-layer compute for the DeAR benchmarks (BASELINE configs 2-4).
+
+The reference models a layer only by its parameter count and compute
+durations (LayerSpec, model.hpp:26-34); BASELINE.json asks for "synthetic
+layer compute" that the collectives overlap with. Here every learnable tensor
+of a preset (proj/src/model.cpp:111-168 sizes, layer 1 = input side) is a
+linear map on `tokens` rows of width `hidden`:
+
+    its n_l fp32 parameters, viewed row-major as W_l[R_l, hidden] with
+    R_l = ceil(n_l / hidden) (the last row partial, zero-padded in the bf16
+    compute copy), so
+    FF_l     Y_l  = X  W_l^T          [T, R_l]    2 T R_l H flops
+    BP_l     dX   = dY W_l            [T, H]      2 T R_l H flops  (dgrad)
+             G_l += dY^T X            [R_l, H]    2 T R_l H flops  (wgrad, fp32,
+                                                  written into the flat grad)
+All three are the hand-written tcgen05 GEMM (gemm.py). Per layer FF costs
+2 n_l T flops and BP twice that, i.e. the 6 * params * tokens of a dense
+network and the paper's t_bp = 2 t_ff (§VI-H).
+
+What is synthetic: the input X and the upstream gradient dY are fixed seeded
+tensors shared by all layers (layers are not chained numerically), so there
+is no loss function. Parameters and gradients are real: W_l is the bf16 copy
+of the parameters that DeAR's unpack kernel refreshes after every update, and
+G_l is the true weight gradient of Y_l = X W_l^T for upstream dY.
+"""
+from __future__ import annotations
+
+import math
+
+import torch
+
+from .gemm import GemmPlan
+
+
+def _round_up(x: int, m: int) -> int:
+    return (x + m - 1) // m * m
+
+
+class SyntheticModel:
+    def __init__(self, numels: list[int], hidden: int, tokens: int, device="cuda", seed: int = 0):
+        self.numels = [int(n) for n in numels]
+        self.L = len(self.numels)
+        self.H = int(hidden)
+        self.T = int(tokens)
+        if self.H % 64 or self.T % 64:
+            raise ValueError("hidden and tokens must be multiples of 64")
+        dev = torch.device(device)
+        H, T = self.H, self.T
+        self.rows = [max(1, math.ceil(n / H)) for n in self.numels]
+        # Flat fp32 parameter / gradient storage, each layer 256-byte aligned.
+        self.offsets, off = [], 0
+        for n in self.numels:
+            self.offsets.append(off)
+            off += _round_up(max(n, 1), 64)
+        self.flat_elems = off
+        g = torch.Generator(device="cpu").manual_seed(seed)
+        self.params_flat = (torch.rand(off, generator=g) * 2 - 1).mul_(0.02).to(dev)
+        self.grads_flat = torch.zeros(off, device=dev)
+        self.params = [self.params_flat[o:o + n] for o, n in zip(self.offsets, self.numels)]
+        self.grads = [self.grads_flat[o:o + n] for o, n in zip(self.offsets, self.numels)]
+        # bf16 compute copies, full rows (zero pad past n_l).
+        self.w_offsets, woff = [], 0
+        for r in self.rows:
+            self.w_offsets.append(woff)
+            woff += r * H
+        self.shadow_flat = torch.zeros(woff, dtype=torch.bfloat16, device=dev)
+        self.shadows = [self.shadow_flat[o:o + r * H] for o, r in zip(self.w_offsets, self.rows)]
+        for p, s in zip(self.params, self.shadows):
+            s[: p.numel()].copy_(p.to(torch.bfloat16))
+        rmax = max(self.rows)
+        self.rpad = _round_up(rmax, 64)
+        # Activations / upstream gradient (synthetic, seeded).
+        self.x = (torch.rand(T, H, generator=g) * 2 - 1).to(torch.bfloat16).to(dev)
+        self.xt = self.x.t().contiguous()
+        self.dy = (torch.rand(T, self.rpad, generator=g) * 2 - 1).mul_(1e-3).to(torch.bfloat16).to(dev)
+        self.dyt = self.dy.t().contiguous()
+        self.y = torch.empty(T, self.rpad, dtype=torch.bfloat16, device=dev)
+        self.dx = torch.empty(T, H, dtype=torch.bfloat16, device=dev)
+        self._build_plans()
+
+    def _build_plans(self):
+        H, T = self.H, self.T
+        self.ff, self.dgrad, self.wgrad = [], [], []
+        for l in range(self.L):
+            R, n = self.rows[l], self.numels[l]
+            W = self.shadows[l]
+            self.ff.append(GemmPlan(self.x, W, self.y, T, R, H, lda=H, ldb=H, ldd=self.rpad))
+            self.dgrad.append(GemmPlan(self.dy, W, self.dx, T, H, R, b_mn_major=True,
+                                       lda=self.rpad, ldb=H, ldd=H))
+            self.wgrad.append(GemmPlan(self.dyt, self.xt, self.grads[l] if n > 0 else self.grads_flat,
+                                       R, H, T, lda=T, ldb=T, ldd=H, d_limit=n,
+                                       accumulate=True))
+
+    # -- flops ---------------------------------------------------------------
+    def ff_flops(self) -> int:
+        return sum(2 * self.T * r * self.H for r in self.rows)
+
+    def bp_flops(self) -> int:
+        return 2 * self.ff_flops()
+
+    # -- one iteration's compute, stream-ordered ----------------------------
+    def set_input(self, x_host: torch.Tensor | None, stream=None) -> None:
+        """Copy this step's input batch (pinned host -> device) and derive X^T."""
+        if x_host is not None:
+            self.x.copy_(x_host, non_blocking=True)
+        self.xt.copy_(self.x.t())
+
+    def forward_layer(self, l: int, stream=None) -> None:
+        self.ff[l - 1].run(stream)
+
+    def backward_layer(self, l: int, stream=None) -> None:
+        self.wgrad[l - 1].run(stream)
+        self.dgrad[l - 1].run(stream)
+
+    def zero_grad(self) -> None:
+        self.grads_flat.zero_()
+
+    def result_scalar(self) -> torch.Tensor:
+        """A device scalar standing for the step's loss (read back by e2e)."""
+        return self.y[0, 0]
+
+    def close(self):
+        for p in self.ff + self.dgrad + self.wgrad:
+            p.close()

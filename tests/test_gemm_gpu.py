@@ -1,0 +1,86 @@
+"""Numerics of the hand-written tcgen05 GEMM against a plain PyTorch fp32
+reference of the same op (bf16 inputs, fp32 accumulate)."""
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _ref(a, b, mn_major):
+    bb = b.float().t() if mn_major else b.float()
+    return a.float() @ bb.t()
+
+
+def _check(out, ref, K):
+    # fp32 accumulation of bf16 products; different summation order than the
+    # reference matmul: tolerance scales with sqrt(K).
+    err = (out.float() - ref).abs().max().item()
+    scale = ref.abs().max().item() + 1e-6
+    assert err <= 2e-3 * scale * max(1.0, (K / 256) ** 0.5), (err, scale)
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 128, 64), (256, 256, 1024), (4096, 825, 1024),
+                                   (300, 100, 70), (1000, 520, 513), (129, 17, 8)])
+@pytest.mark.parametrize("mn_major", [False, True])
+def test_gemm_fp32_out(M, N, K, mn_major):
+    from paper_2302_12445_b200.gemm import GemmPlan
+
+    torch.manual_seed(M * 7 + N)
+    a = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+    if mn_major:
+        ldb = (N + 7) // 8 * 8
+        bstore = torch.randn(K, ldb, device="cuda").to(torch.bfloat16)
+        b = bstore[:, :N]
+    else:
+        ldk = (K + 7) // 8 * 8
+        bstore = torch.randn(N, ldk, device="cuda").to(torch.bfloat16)
+        b = bstore[:, :K]
+    lda = (K + 7) // 8 * 8
+    astore = torch.zeros(M, lda, device="cuda", dtype=torch.bfloat16)
+    astore[:, :K] = a
+    d = torch.full((M, N), float("nan"), device="cuda")
+    plan = GemmPlan(astore, bstore, d, M, N, K, b_mn_major=mn_major, lda=lda,
+                    ldb=bstore.stride(0), ldd=N)
+    plan.run()
+    torch.cuda.synchronize()
+    _check(d, _ref(astore[:, :K], b, mn_major), K)
+
+
+@pytest.mark.parametrize("M,N,K", [(825, 1024, 4096), (311, 512, 10240), (96, 64, 256)])
+def test_gemm_splitk_accumulate_flat_limit(M, N, K):
+    """Weight-gradient shape: D (flat, partial last row) += A @ B^T, split-K."""
+    from paper_2302_12445_b200.gemm import GemmPlan
+
+    torch.manual_seed(1)
+    a = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+    b = torch.randn(N, K, device="cuda").to(torch.bfloat16)
+    limit = M * N - N // 3
+    flat = torch.zeros(limit + 64, device="cuda")
+    flat[limit:] = 12345.0  # sentinel past the bound must survive
+    base = torch.randn(limit, device="cuda")
+    flat[:limit] = base
+    plan = GemmPlan(a, b, flat, M, N, K, ldd=N, d_limit=limit, accumulate=True)
+    assert plan.info()["splits"] >= 1
+    plan.run()
+    torch.cuda.synchronize()
+    ref = (a.float() @ b.float().t()).reshape(-1)[:limit] + base
+    _check(flat[:limit], ref, K)
+    assert torch.all(flat[limit:] == 12345.0)
+
+
+@pytest.mark.parametrize("M,N,K", [(4096, 825, 1024), (200, 72, 128)])
+def test_gemm_bf16_out(M, N, K):
+    from paper_2302_12445_b200.gemm import GemmPlan
+
+    torch.manual_seed(2)
+    a = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+    b = torch.randn(N, K, device="cuda").to(torch.bfloat16)
+    ldd = (N + 7) // 8 * 8
+    d = torch.zeros(M, ldd, device="cuda", dtype=torch.bfloat16)
+    plan = GemmPlan(a, b, d, M, N, K, ldd=ldd)
+    plan.run()
+    torch.cuda.synchronize()
+    ref = a.float() @ b.float().t()
+    # bf16 output: one bf16 rounding (2^-8 relative) on top of the fp32 tolerance
+    err = (d[:, :N].float() - ref).abs()
+    assert torch.all(err <= ref.abs() * 2.0**-8 + 2e-3 * ref.abs().max()), err.max()
