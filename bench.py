@@ -1,0 +1,477 @@
+#!/usr/bin/env python
+"""DeAR on B200 — training-step throughput on synthetic preset-shaped layers.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload resnet50]
+    torchrun --nproc-per-node N bench.py --gpus N ...     (driver launch, N > 1)
+    python bench.py --impl reference ...                  (the reference's CPU path)
+
+One step = one DeAR iteration: feed-forward of every layer (each gated on its
+own bucket's all-gather + unpack), backprop (wgrad + dgrad tcgen05 GEMMs per
+layer) with pack -> reduce-scatter -> shard SGD update per fusion bucket on
+the comm stream, and the all-gathers of the updated shards that the next
+forward waits on. The whole iteration is captured once as a CUDA graph
+(`--no-graph` runs it eagerly). Per-GPU work is fixed as N grows (weak
+scaling). Printed: ONE JSON line (rank 0).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# BASELINE.json configs 1-4. tokens_per_sample turns a layer's parameters into
+# dense-layer flops: 2 * params * tokens for FF. ResNet-50: 4.1 GMAC / 25.6M
+# params ~= 160 MACs per parameter per image; BERT: 64-token sentences
+# (PAPER.md:195); batch sizes per GPU from PAPER.md Table I.
+WORKLOADS = {
+    "mlp4x1024": dict(preset="mlp4x1024", hidden=1024, tokens_per_sample=1, batch=64,
+                      config="BASELINE config 1: synthetic 4-layer fp32 MLP (1024-wide)"),
+    "resnet50": dict(preset="resnet50", hidden=512, tokens_per_sample=160, batch=64,
+                     config="BASELINE config 2: ResNet-50-shaped gradient set "
+                            "(25.6M params, 161 tensors)"),
+    "bert_base": dict(preset="bert_base", hidden=768, tokens_per_sample=64, batch=64,
+                      config="BASELINE config 3: BERT-Base-shaped (110.1M params, 206 tensors)"),
+    "bert_large": dict(preset="bert_large", hidden=1024, tokens_per_sample=64, batch=32,
+                       config="BASELINE config 4: BERT-Large-shaped (336.2M params, 398 tensors)"),
+}
+METRIC = "samples/s at 1/2/4/8 B200 (DeAR vs WFBP)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="resnet50", choices=list(WORKLOADS))
+    ap.add_argument("--batch", type=int, default=0, help="samples per GPU (0 = workload default)")
+    ap.add_argument("--policy", default="DEAR_FUSED")
+    ap.add_argument("--baseline-policy", default="WFBP_FUSED")
+    ap.add_argument("--buffer", type=int, default=25_000_000, help="fusion buffer bytes")
+    ap.add_argument("--lr", type=float, default=0.05)
+    ap.add_argument("--momentum", type=float, default=0.0)
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-ablation", action="store_true", help="skip WFBP / compute-only runs")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--profile-steps", type=int, default=0,
+                    help="only run this many graph replays (for ncu launch lists)")
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------- helpers ----
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.proc, self.rows = index, None, []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self) -> dict:
+        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 7
+                          for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d["hbm_gbs"], d["bf16_tflops"], d["bf16_tflops_sustained"], "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+# ------------------------------------------------------------ reference arm --
+def reference_arm(a, wl, world: int, rank: int, emit: bool = True):
+    """The reference's own CPU path (oracle/_ref: proj/src/collective.cpp
+    sgd_step per fusion bucket, fp64, P = N virtual workers), all host cores."""
+    if rank != 0:
+        return None
+    import numpy as np
+
+    from oracle.lib import Reference
+    from paper_2302_12445_b200.presets import preset_param_counts
+    from oracle.schedule import fusion_plan
+
+    counts = preset_param_counts(wl["preset"])
+    P = max(1, world)
+    plan = fusion_plan([4 * c for c in counts], a.buffer if "FUSED" in a.policy else 0)
+    buckets = [sum(counts[lo - 1:hi]) for lo, hi in plan]
+    D = sum(buckets)
+    cores = os.cpu_count() or 1
+    # Bound memory (P replicas + P grads in fp64, ~3x transient) to ~12 GB and
+    # the sample to the requested seconds: take whole buckets in plan order.
+    cap = int(12e9 / (8 * P * 5))
+    sample, tot = [], 0
+    for b in buckets:
+        if tot + b > cap and sample:
+            break
+        sample.append(b)
+        tot += b
+    ref = Reference()
+    t1 = ref.time_sgd_steps(sample, P, cores, 1, seed=7)[0]  # warm-up
+    if emit:  # the reference arm proper: exactly K timed steps after W warm-ups
+        for _ in range(max(0, a.warmup - 1)):
+            ref.time_sgd_steps(sample, P, cores, 1, seed=7)
+        steps = a.steps
+    else:     # cpu_baseline leg of our line: bounded to ~cpu_seconds
+        steps = max(1, min(50, int(a.cpu_seconds / max(t1, 1e-6))))
+    ts = ref.time_sgd_steps(sample, P, cores, steps, seed=8)
+    t_sample = float(np.median(ts))
+    t_full = t_sample * D / tot
+    batch = a.batch or wl["batch"]
+    value = batch * P / t_full
+    cpu = {"value": value, "unit": "samples/s", "cores": cores, "kind": "reference",
+           "sample": f"oracle/_ref sgd_step (reference collective.cpp, fp64) over "
+                     f"{len(sample)}/{len(buckets)} fusion buckets ({tot}/{D} elements) x P={P} "
+                     f"virtual workers, {steps} steps, {cores} threads; per-step time scaled "
+                     f"to the full model; samples/s = batch {batch} x P / step time",
+           "step_seconds_full_model": t_full}
+    if emit:
+        line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
+                "steps": steps, "warmup": a.warmup, "ms_per_step": t_full * 1e3,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic",
+                "config": {"workload": wl["config"], "policy": a.policy,
+                           "fusion_buffer_bytes": a.buffer, "global_batch": batch * P},
+                "impl": "reference", "cpu_baseline": cpu,
+                "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+    return cpu
+
+
+# ----------------------------------------------------------------- GPU arm --
+class Step:
+    """One DeAR iteration over the synthetic model through the public API."""
+
+    def __init__(self, model, rt, stream, x_host=None, out_host=None):
+        self.m, self.rt, self.s = model, rt, stream
+        self.x_host, self.out_host = x_host, out_host
+
+    def __call__(self):
+        import torch
+
+        m, rt, s = self.m, self.rt, self.s
+        with torch.cuda.stream(s):
+            m.set_input(self.x_host)
+            for l in range(1, m.L + 1):
+                if rt is not None:
+                    rt.param_wait(l, s)
+                m.forward_layer(l, s)
+            m.zero_grad()
+            for l in range(m.L, 0, -1):
+                m.backward_layer(l, s)
+                if rt is not None:
+                    rt.grad_ready(l, s)
+            if rt is not None:
+                rt.step(s)
+                rt.join(s)
+            if self.out_host is not None:
+                self.out_host.copy_(m.result_scalar(), non_blocking=True)
+
+
+def time_loop(fn, steps, warmup, stream, dist_on):
+    import torch
+
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    if dist_on:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if dist_on:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = t.item()
+        torch.distributed.barrier()
+    return ms / steps
+
+
+def make_runner(step, use_graph, stream):
+    """Eager step, or a CUDA graph of it (captured after one eager step)."""
+    import torch
+
+    if not use_graph:
+        return step
+    step()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream, capture_error_mode="thread_local"):
+        step()
+    torch.cuda.synchronize()
+
+    def replay():
+        with torch.cuda.stream(stream):  # replay on the timed stream
+            g.replay()
+    return replay
+
+
+def gpu_arm(a, wl, world, rank, local_rank):
+    import torch
+
+    import paper_2302_12445_b200 as dear
+    from paper_2302_12445_b200.presets import preset_param_counts
+    from paper_2302_12445_b200.synthetic import SyntheticModel
+
+    dist_on = world > 1
+    torch.cuda.set_device(local_rank)
+    comm = None
+    if dist_on:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+        comm = dear.init()
+    batch = a.batch or wl["batch"]
+    tokens = batch * wl["tokens_per_sample"]
+    counts = preset_param_counts(wl["preset"])
+    model = SyntheticModel(counts, wl["hidden"], tokens, seed=1234)
+    stream = torch.cuda.Stream()
+    use_graph = not a.no_graph
+    hbm, tf_burst, tf_sus, peak_kind = peaks()
+
+    def runtime(policy):
+        rt = dear.Runtime(comm, rank, world, policy=policy, fusion_buffer_bytes=a.buffer,
+                          lr=a.lr, momentum=a.momentum, defer_allgather=use_graph,
+                          stream=stream)
+        for l in range(1, model.L + 1):
+            rt.register(l, model.params[l - 1], model.grads[l - 1], model.shadows[l - 1])
+        rt.finalize()
+        return rt
+
+    res = {}
+    # --- headline: DeAR, inputs resident ---------------------------------
+    rt = runtime(a.policy)
+    buckets = rt.buckets()
+    run = make_runner(Step(model, rt, stream), use_graph, stream)
+    if a.profile_steps:
+        for _ in range(a.profile_steps):
+            run()
+        torch.cuda.synchronize()
+        rt.synchronize()
+        if rank == 0:
+            print(json.dumps({"profile_steps": a.profile_steps}), flush=True)
+        return None
+    with ClockSampler(local_rank) as clk:
+        ms = time_loop(run, a.steps, a.warmup, stream, dist_on)
+    res["dear_ms"] = ms
+    clocks = clk.summary()
+
+    # --- e2e through the public API: pinned host input in, scalar out -------
+    x_host = torch.empty(model.x.shape, dtype=model.x.dtype, pin_memory=True)
+    x_host.copy_(model.x.cpu())
+    out_host = torch.empty((), dtype=model.y.dtype, pin_memory=True)
+    rt.synchronize()
+    run_e2e = make_runner(Step(model, rt, stream, x_host, out_host), use_graph, stream)
+    res["e2e_ms"] = time_loop(run_e2e, a.steps, a.warmup, stream, dist_on)
+    h2d = x_host.numel() * x_host.element_size()
+    d2h = out_host.element_size()
+
+    # --- per-stage timings (one instrumented eager step) ---------------------
+    rt.synchronize()
+    rt.set_timing(True)
+    Step(model, rt, stream)()
+    rt.synchronize()
+    torch.cuda.synchronize()
+    stage = rt.timings()
+    rt.set_timing(False)
+    # GEMM launch durations inside one eager step (compute stream events).
+    gemm_ms, gemm_flops = _time_gemms(model, rt, stream)
+    rt.synchronize()
+    ok_replicas = rt.check_replicas()
+    rt.close()
+
+    # --- HBM kernels in isolation: comm-only iterations (no GEMMs) -----------
+    iso = _isolated_stage_times(model, runtime, stream, a.policy)
+
+    # --- ablation: same kernels, WFBP schedule; compute-only ------------------
+    if not a.no_ablation:
+        rtw = runtime(a.baseline_policy)
+        runw = make_runner(Step(model, rtw, stream), use_graph, stream)
+        res["wfbp_ms"] = time_loop(runw, a.steps, a.warmup, stream, dist_on)
+        rtw.synchronize()
+        rtw.close()
+        runc = make_runner(Step(model, None, stream), use_graph, stream)
+        res["compute_ms"] = time_loop(runc, a.steps, a.warmup, stream, dist_on)
+
+    if rank != 0:
+        return None
+    samples = batch * world
+    value = samples / (res["dear_ms"] / 1e3)
+    e2e = samples / (res["e2e_ms"] / 1e3)
+    # Bucket-stage rooflines (isolated): algorithmic bytes per element.
+    D = sum(counts)
+    shard = sum(b["slot_stride"] for b in buckets)
+    elem_bytes = {"pack": 8 * D, "update": (20 if a.momentum else 12) * shard,
+                  "unpack": 10 * D}
+    roof = {}
+    for k, nbytes in elem_bytes.items():
+        t = iso.get(k)
+        if t:
+            roof[k] = {"bound": "hbm", "achieved": nbytes / (t / 1e3) / 1e9, "peak": hbm,
+                       "unit": "GB/s", "frac": nbytes / (t / 1e3) / 1e9 / hbm,
+                       "bytes_per_step": nbytes, "ms_per_step": t}
+    busbw = {}
+    if world > 1:
+        for k in ("rs", "ag"):
+            ts = [(b["slot_stride"], st[k]) for b, st in zip(buckets, stage) if st[k]]
+            tot_t = sum(t for _, t in ts)
+            tot_b = sum((world - 1) * s * 4 for s, _ in ts)
+            busbw[k] = tot_b / (tot_t / 1e3) / 1e9 if tot_t else None
+    gemm_achieved = gemm_flops / (gemm_ms / 1e3) / 1e12
+    line = {
+        "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": res["dear_ms"],
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic",
+        "config": {"workload": wl["config"], "policy": a.policy,
+                   "fusion_buffer_bytes": a.buffer, "buckets": len(buckets),
+                   "batch_per_gpu": batch, "global_batch": samples, "tokens_per_gpu": tokens,
+                   "hidden": wl["hidden"], "params": D, "cuda_graph": use_graph,
+                   "l2": "working set (params+grads+buckets) > 126 MB L2; no flush"},
+        "e2e": {"value": e2e, "unit": "samples/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "clocks": clocks,
+        "gpu_launches": a.steps * (3 * model.L + 3 * len(buckets)),
+        "roofline": {"bound": "tensor", "kernel": "tcgen05 GEMM (FF+dgrad+wgrad)",
+                     "achieved": gemm_achieved, "peak": tf_sus, "unit": "TFLOP/s",
+                     "frac": gemm_achieved / tf_sus, "traffic": None,
+                     "peak_kind": f"{peak_kind} sustained"},
+        "hbm_kernels": roof,
+        "replicas_identical": ok_replicas,
+    }
+    if "wfbp_ms" in res:
+        line["wfbp"] = {"policy": a.baseline_policy, "value": samples / (res["wfbp_ms"] / 1e3),
+                        "ms_per_step": res["wfbp_ms"]}
+        line["dear_over_wfbp"] = res["wfbp_ms"] / res["dear_ms"]
+        line["compute_only_ms"] = res["compute_ms"]
+        line["exposed_comm_pct"] = max(0.0, 100 * (res["dear_ms"] - res["compute_ms"]) /
+                                       res["dear_ms"])
+        line["wfbp_exposed_comm_pct"] = max(0.0, 100 * (res["wfbp_ms"] - res["compute_ms"]) /
+                                            res["wfbp_ms"])
+    if busbw:
+        line["busbw_gbs"] = busbw
+    if world == 1 and not a.no_cpu:
+        line["cpu_baseline"] = reference_arm(a, wl, world, rank, emit=False)
+    return line
+
+
+def _time_gemms(model, rt, stream):
+    """Average GEMM launch time inside one eager DeAR step (events between the
+    layer GEMMs on the compute stream)."""
+    import torch
+
+    evs = []
+    with torch.cuda.stream(stream):
+        for l in range(1, model.L + 1):
+            rt.param_wait(l, stream)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            model.forward_layer(l, stream)
+            e1.record(stream)
+            evs.append((e0, e1, model.ff[l - 1].flops))
+        model.zero_grad()
+        for l in range(model.L, 0, -1):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            model.backward_layer(l, stream)
+            e1.record(stream)
+            evs.append((e0, e1, model.wgrad[l - 1].flops + model.dgrad[l - 1].flops))
+            rt.grad_ready(l, stream)
+        rt.step(stream)
+    torch.cuda.synchronize()
+    ms = sum(e0.elapsed_time(e1) for e0, e1, _ in evs)
+    return ms, sum(f for _, _, f in evs)
+
+
+def _isolated_stage_times(model, runtime, stream, policy):
+    """pack / update / unpack per step with no GEMMs running: grads reported
+    back to back, so the comm stream runs the bucket kernels alone."""
+    import torch
+
+    rt = runtime(policy)
+    rt.set_timing(True)
+    for it in range(3):
+        with torch.cuda.stream(stream):
+            for l in range(1, model.L + 1):
+                rt.param_wait(l, stream)
+            for l in range(model.L, 0, -1):
+                rt.grad_ready(l, stream)
+            rt.step(stream)
+        rt.synchronize()
+    torch.cuda.synchronize()
+    st = rt.timings()
+    rt.close()
+    out = {}
+    for k in ("pack", "update", "unpack"):
+        v = [s[k] for s in st if s[k] is not None]
+        out[k] = sum(v) if v else None
+    return out
+
+
+def main():
+    a = parse()
+    wl = WORKLOADS[a.workload]
+    world = int(os.environ.get("WORLD_SIZE", a.gpus))
+    rank = int(os.environ.get("RANK", 0))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if a.impl == "reference":
+        reference_arm(a, wl, world, rank)
+        return 0
+    line = gpu_arm(a, wl, world, rank, local_rank)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -109,5 +109,9 @@ def check(rc: int) -> None:
         raise DearError(rc, msg)
 
 
+GEMM_SYMBOLS = ["dear_gemm_plan_create", "dear_gemm_run", "dear_gemm_plan_info",
+                "dear_gemm_plan_destroy"]  # bound in gemm.py
+
+
 def exported_symbols() -> list[str]:
-    return sorted(_SIGNATURES) + ["dear_last_error", "dear_slot_stride"]
+    return sorted(_SIGNATURES) + ["dear_last_error", "dear_slot_stride"] + GEMM_SYMBOLS

@@ -99,6 +99,7 @@ struct Bucket {
   bool any_shadow = false;
   bool mom_init = false;
   cudaEvent_t ag_done = nullptr;
+  unsigned long long ag_capture = 0;  // capture id ag_done was recorded in (0: eager)
   bool ag_live = false;          // an AG for this bucket is enqueued
   cudaStream_t waited = nullptr; // last stream that waited on ag_done
   bool waited_valid = false;
@@ -156,7 +157,7 @@ struct dear_ctx {
   void exec(const Op& op);
   void complete_bucket(int b);
   void enqueue_backpipe(int b);
-  void enqueue_feedpipe();
+  void enqueue_feedpipe(cudaStream_t fence_stream);
   void record_t(int b, int which);
   std::string label(const char* kind, int b) const;
 };
@@ -167,6 +168,14 @@ void free_events(std::vector<cudaEvent_t>& evs) {
   for (cudaEvent_t e : evs)
     if (e) cudaEventDestroy(e);
   evs.clear();
+}
+
+// Id of the CUDA-graph capture `s` is part of, 0 when not capturing.
+unsigned long long capture_id(cudaStream_t s) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  unsigned long long id = 0;
+  cuda_check(cudaStreamGetCaptureInfo(s, &st, &id), "cudaStreamGetCaptureInfo");
+  return st == cudaStreamCaptureStatusActive ? id : 0;
 }
 
 cudaEvent_t new_event(bool timing) {
@@ -368,6 +377,7 @@ void dear_ctx::exec(const Op& op) {
       break;
     case OP_AG_DONE:
       cuda_check(cudaEventRecord(B->ag_done, comm_stream), "cudaEventRecord");
+      B->ag_capture = capture_id(comm_stream);
       break;
     case OP_CALLER_WAIT_PACKED:
       cuda_check(cudaStreamWaitEvent(op.stream, packed_ev, 0), "cudaStreamWaitEvent");
@@ -402,7 +412,12 @@ void dear_ctx::enqueue_backpipe(int b) {
   if (local) group->drain();
 }
 
-void dear_ctx::enqueue_feedpipe() {
+void dear_ctx::enqueue_feedpipe(cudaStream_t fence_stream) {
+  // BARRIER: the all-gathers (which rewrite parameters) start after the work
+  // already enqueued on `fence_stream` (the end of backprop, or — when
+  // deferred — the start of the next forward, which keeps the comm stream
+  // inside a CUDA-graph capture of that stream).
+  cuda_check(cudaEventRecord(step_ev, fence_stream), "cudaEventRecord");
   // Reverse plan order = feed-forward order (task_graph.cpp:199-206).
   enqueue({OP_FENCE_STEP, -1, nullptr});
   for (int g = static_cast<int>(buckets.size()) - 1; g >= 0; --g) {
@@ -803,13 +818,12 @@ int dear_step(dear_ctx* ctx, void* stream) {
   // Both directions of the barrier: gradients are consumed (packed) before the
   // caller may overwrite them; parameters are rewritten only after the
   // caller's backward work.
-  cuda_check(cudaEventRecord(c.step_ev, s), "cudaEventRecord");
   c.enqueue({OP_CALLER_WAIT_PACKED, -1, s});
   if (is_dear(c.cfg.policy)) {
     if (c.cfg.defer_allgather) {
       c.ags_deferred = true;
     } else {
-      c.enqueue_feedpipe();
+      c.enqueue_feedpipe(s);
     }
   } else if (c.local) {
     c.group->drain();
@@ -836,15 +850,21 @@ int dear_param_wait(dear_ctx* ctx, int32_t layer, void* stream) {
     if (c.local) {
       // The group flushes together: a local collective needs every rank.
       for (dear_ctx* o : c.group->ranks)
-        if (o && o->ags_deferred) o->enqueue_feedpipe();
+        if (o && o->ags_deferred) o->enqueue_feedpipe(o == &c ? static_cast<cudaStream_t>(stream) : o->compute);
     } else {
-      c.enqueue_feedpipe();
+      c.enqueue_feedpipe(static_cast<cudaStream_t>(stream));
     }
   }
   Bucket& B = c.buckets[static_cast<size_t>(c.layers[static_cast<size_t>(layer - 1)].bucket)];
   if (!B.ag_live) return DEAR_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (B.waited_valid && B.waited == s) return DEAR_OK;
+  // Inside a CUDA-graph capture, an all-gather recorded outside this capture
+  // (the previous iteration of a WFBP schedule) is ordered before the graph
+  // launch by the capture's trailing dear_join; a cross-capture wait is
+  // illegal, so it is dropped.
+  const unsigned long long cap = capture_id(s);
+  if (cap != 0 && B.ag_capture != cap) return DEAR_OK;
   if (c.local) {
     c.group->drain();
     if (!c.queue.empty()) invalid("dear_param_wait: local group ranks are out of lock-step");
@@ -869,12 +889,12 @@ int dear_synchronize(dear_ctx* ctx) {
   need(ctx, true);
   if (ctx->local) {
     for (dear_ctx* o : ctx->group->ranks)
-      if (o && o->ags_deferred) o->enqueue_feedpipe();
+      if (o && o->ags_deferred) o->enqueue_feedpipe(o->compute);
     ctx->group->drain();
     if (!ctx->queue.empty()) invalid("dear_synchronize: other ranks of the local group lag behind");
   }
   else if (ctx->ags_deferred) {
-    ctx->enqueue_feedpipe();
+    ctx->enqueue_feedpipe(ctx->compute);
   }
   cuda_check(cudaStreamSynchronize(ctx->comm_stream), "cudaStreamSynchronize");
   DEAR_API_END
@@ -985,7 +1005,7 @@ int dear_check_replicas(dear_ctx* ctx, int32_t* identical) {
   DEAR_API_BEGIN
   need(ctx, true);
   dear_ctx& c = *ctx;
-  if (c.ags_deferred) c.enqueue_feedpipe();
+  if (c.ags_deferred) c.enqueue_feedpipe(c.compute);
   cuda_check(cudaStreamSynchronize(c.comm_stream), "cudaStreamSynchronize");
   const unsigned long long h = hash_params(c);
   if (c.local) {

@@ -28,7 +28,7 @@ def test_library_exports_every_declared_symbol():
     missing = [n for n in sorted(declared) if not hasattr(L, n)]
     assert not missing, missing
     # and the Python binding knows the signature of each of them
-    assert set(_lib.exported_symbols()) | {"dear_gemm_bf16"} >= declared - {"dear_gemm_bf16"}
+    assert set(_lib.exported_symbols()) == declared
 
 
 def test_dynamic_symbol_table():
