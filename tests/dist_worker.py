@@ -1,0 +1,148 @@
+"""torchrun worker for the multi-GPU (NCCL over NVLink) parity tests.
+
+    torchrun --nproc-per-node N tests/dist_worker.py <case>
+
+case "runtime": the C-ABI runtime through NCCL on seeded gradients (the
+reference tests' generator), every policy, 3 steps; parameters must be
+bit-identical across ranks and within 1e-5 of the oracle's fp64 sgd_step
+(per fusion bucket), momentum variant against the fp64 momentum restatement.
+case "distoptim": DistOptim on a torch MLP, each rank its own micro-batch;
+parameters must match single-process torch.optim.SGD on the averaged
+gradient within 1e-5.
+Exit code 0 = pass.
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+import paper_2302_12445_b200 as dear  # noqa: E402
+from dear_harness import initial_weights, oracle_run, seeded_grads  # noqa: E402
+from oracle.lib import Restated  # noqa: E402
+
+RAGGED = [1000, 4097, 3, 0, 2049, 1, 70001, 513, 12345, 7, 262144, 100003]
+
+
+def close(a, b, tol=1e-5):
+    return bool(np.all(np.abs(a - b) <= tol * np.maximum(1.0, np.abs(b))))
+
+
+def run_runtime(comm, rank, P, policy, buf, steps, lr, **kw):
+    o = Restated()
+    numels = RAGGED
+    offs = np.concatenate([[0], np.cumsum(numels)]).astype(np.int64)
+    w0 = initial_weights(o, numels)
+    s = torch.cuda.Stream()
+    rt = dear.Runtime(comm, rank, P, policy=policy, fusion_buffer_bytes=buf, lr=lr, stream=s, **kw)
+    params, grads = [], []
+    for l in range(1, len(numels) + 1):
+        p = torch.from_numpy(w0[offs[l - 1]:offs[l]].copy()).cuda()
+        g = torch.zeros_like(p)
+        rt.register(l, p, g)
+        params.append(p)
+        grads.append(g)
+    rt.finalize()
+    with torch.cuda.stream(s):
+        for step in range(steps):
+            G = seeded_grads(o, P, numels, step)
+            for l in range(1, len(numels) + 1):
+                rt.param_wait(l, s)
+            for l in range(len(numels), 0, -1):
+                grads[l - 1].copy_(torch.from_numpy(G[rank, offs[l - 1]:offs[l]].copy()))
+                rt.grad_ready(l, s)
+            rt.step(s)
+    rt.synchronize()
+    torch.cuda.synchronize()
+    same = rt.check_replicas()
+    trace = rt.trace()
+    w = torch.cat([p for p in params]).cpu().numpy()
+    rt.close()
+    return w, same, trace
+
+
+def case_runtime(rank, P):
+    comm = dear.init()
+    o = Restated()
+    ok = True
+    for policy, buf in (("DEAR_FUSED", 100_000), ("DEAR", 0), ("WFBP_FUSED", 400_000),
+                        ("WFBP", 0), ("DEAR_FUSED", 25_000_000)):
+        w, same, trace = run_runtime(comm, rank, P, policy, buf, 3, 0.05)
+        exp = oracle_run(o, RAGGED, P, 3, policy, buf, 0.05, f32=False)
+        allw = [torch.zeros_like(torch.from_numpy(w)).cuda() for _ in range(P)]
+        dist.all_gather(allw, torch.from_numpy(w).cuda())
+        bit_same = all(torch.equal(allw[0], x) for x in allw)
+        good = same and bit_same and close(w.astype(np.float64), exp)
+        if rank == 0:
+            print(f"[runtime P={P}] {policy:11s} buf={buf:>9} replicas={same and bit_same} "
+                  f"oracle_1e-5={close(w.astype(np.float64), exp)} trace0={trace[:2]}", flush=True)
+        ok &= good
+    kw = dict(momentum=0.9, weight_decay=1e-3, nesterov=True)
+    w, same, _ = run_runtime(comm, rank, P, "DEAR_FUSED", 200_000, 4, 0.02, **kw)
+    exp = oracle_run(o, RAGGED, P, 4, "DEAR_FUSED", 200_000, 0.02, f32=False, **kw)
+    good = same and close(w.astype(np.float64), exp)
+    if rank == 0:
+        print(f"[runtime P={P}] momentum/wd/nesterov replicas={same} oracle_1e-5={good}",
+              flush=True)
+    ok &= good
+    comm.close()
+    return ok
+
+
+def case_distoptim(rank, P):
+    comm = dear.init()
+    torch.manual_seed(0)
+    layers = [torch.nn.Linear(64, 128), torch.nn.ReLU(), torch.nn.Linear(128, 96),
+              torch.nn.ReLU(), torch.nn.Linear(96, 10)]
+    model = torch.nn.Sequential(*layers).cuda()
+    ref = torch.nn.Sequential(*[type(m)(*([m.in_features, m.out_features]
+                                          if isinstance(m, torch.nn.Linear) else []))
+                                for m in layers]).cuda()
+    ref.load_state_dict(model.state_dict())
+    kw = dict(lr=0.1, momentum=0.9, weight_decay=1e-4)
+    opt = dear.DistOptim(torch.optim.SGD(model.parameters(), **kw), model, comm=comm,
+                         policy="DEAR_FUSED", fusion_buffer_bytes=20_000)
+    ropt = torch.optim.SGD(ref.parameters(), foreach=False, **kw)
+    g = torch.Generator(device="cpu").manual_seed(42)
+    for step in range(5):
+        xs = [torch.randn(16, 64, generator=g) for _ in range(P)]
+        ys = [torch.randint(0, 10, (16,), generator=g) for _ in range(P)]
+        loss = torch.nn.functional.cross_entropy(model(xs[rank].cuda()), ys[rank].cuda())
+        loss.backward()
+        opt.step()
+        opt.zero_grad()
+        # reference: mean of the P micro-batch gradients, one process
+        ropt.zero_grad()
+        for r in range(P):
+            torch.nn.functional.cross_entropy(ref(xs[r].cuda()), ys[r].cuda()).div(P).backward()
+        ropt.step()
+    opt.synchronize()
+    ok = opt.check_replicas()
+    for p, q in zip(model.parameters(), ref.parameters()):
+        ok &= close(p.detach().double().cpu().numpy(), q.detach().double().cpu().numpy(), 1e-5)
+    if rank == 0:
+        print(f"[distoptim P={P}] match single-process SGD on averaged grads: {ok}", flush=True)
+    opt.close()
+    comm.close()
+    return ok
+
+
+def main():
+    case = sys.argv[1]
+    rank, P = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    torch.cuda.set_device(int(os.environ["LOCAL_RANK"]))
+    dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ["LOCAL_RANK"])))
+    ok = {"runtime": case_runtime, "distoptim": case_distoptim}[case](rank, P)
+    t = torch.tensor([0 if ok else 1], device="cuda")
+    dist.all_reduce(t)
+    dist.destroy_process_group()
+    sys.exit(int(t.item() != 0))
+
+
+if __name__ == "__main__":
+    main()
