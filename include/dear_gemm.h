@@ -35,8 +35,12 @@ int dear_gemm_plan_create(const void* A, int64_t lda, const void* B, int64_t ldb
                           int32_t b_mn_major, void* D, int64_t ldd, int32_t d_fp32, int64_t M,
                           int64_t N, int64_t K, int64_t d_limit, int32_t accumulate,
                           int32_t split_k, dear_gemm_plan** out);
-/* Enqueue on `stream` (cudaStream_t as void*). */
+/* Enqueue on `stream` (cudaStream_t as void*). Launches are persistent (one
+ * CTA per SM) and use programmatic dependent launch. */
 int dear_gemm_run(dear_gemm_plan* plan, void* stream);
+/* One launch computing n (1 or 2) independent plans on a shared persistent
+ * grid, e.g. the weight- and data-gradient GEMMs of one layer. */
+int dear_gemm_run_group(dear_gemm_plan* const* plans, int32_t n, void* stream);
 /* Tile geometry actually used: BN, grid.x (N tiles), grid.y (M tiles), splits. */
 int dear_gemm_plan_info(dear_gemm_plan* plan, int32_t* bn, int32_t* n_tiles, int32_t* m_tiles,
                         int32_t* splits);

@@ -109,8 +109,8 @@ def check(rc: int) -> None:
         raise DearError(rc, msg)
 
 
-GEMM_SYMBOLS = ["dear_gemm_plan_create", "dear_gemm_run", "dear_gemm_plan_info",
-                "dear_gemm_plan_destroy"]  # bound in gemm.py
+GEMM_SYMBOLS = ["dear_gemm_plan_create", "dear_gemm_run", "dear_gemm_run_group",
+                "dear_gemm_plan_info", "dear_gemm_plan_destroy"]  # bound in gemm.py
 
 
 def exported_symbols() -> list[str]:

@@ -1,20 +1,30 @@
-// Hand-written sm_100a GEMM: TMA (cp.async.bulk.tensor, 128B swizzle) ->
-// 4-stage smem ring (mbarrier full/empty) -> tcgen05.mma (kind::f16, bf16 in,
-// fp32 accumulate in TMEM, issued by one thread) -> tcgen05.ld epilogue.
+// Hand-written sm_100a GEMM for the synthetic layer compute.
+//
+//   TMA (cp.async.bulk.tensor.2d, 128B swizzle) -> 4-stage smem ring
+//   (mbarrier full/empty) -> tcgen05.mma kind::f16 (bf16 in, fp32 accumulate
+//   in TMEM, issued by one thread) -> tcgen05.ld epilogue -> global.
+//
+// Persistent: one CTA per SM walks a static round-robin list of output tiles
+// (128 x BN, BN <= 256 a multiple of 16 chosen per problem). TMEM holds two
+// 256-column accumulators, so the epilogue of tile i overlaps the mainloop of
+// tile i+1. A launch may carry up to two independent problems (the wgrad and
+// dgrad of one layer's backprop), sharing the persistent grid. Launches use
+// programmatic dependent launch: the next GEMM's CTAs run their prologue
+// (barrier init, TMEM alloc, descriptor prefetch) while this one drains, and
+// block in griddepcontrol.wait before touching memory.
 //
 // Warp roles per CTA (192 threads):
 //   warp 0      TMA producer (one lane)
 //   warp 1      TMEM allocator + MMA issuer (one lane)
-//   warps 2..5  epilogue: warp w reads TMEM lanes 32*(w%4) .. +31
-// One CTA computes one 128 x BN output tile (BN <= 256, a multiple of 16
-// chosen on the host to minimise N padding) over a K range; with
-// `accumulate` the K range may be split across CTAs (grid.z) and partial
-// tiles are reduced into fp32 D with red.global.add.v4.f32.
+//   warps 2..5  epilogue; warp w reads TMEM lanes 32*(w%4) .. +31
+// With `accumulate`, a problem's K range may be split across tiles and the
+// partial tiles are reduced into fp32 D with red.global.add.v4.f32.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <string>
 
 #include "dear_gemm.h"
@@ -30,23 +40,38 @@ constexpr int kStages = 4;
 constexpr int kAStage = kBM * kBK * 2;     // 16 KB
 constexpr int kBStage = kBNMax * kBK * 2;  // 32 KB
 constexpr int kThreads = 192;
-constexpr int kTmemCols = 256;
+constexpr int kAccCols = 256;
+constexpr int kTmemCols = 2 * kAccCols;
 constexpr int kSmemBytes = kStages * (kAStage + kBStage) + 1024 + 256;
+constexpr int kMaxProblems = 2;
+constexpr int kSms = 148;
 
-struct Params {
+struct alignas(64) Problem {
+  CUtensorMap tmA;
+  CUtensorMap tmB;
   void* D;
   int64_t ldd;
   int64_t M, N;
   int64_t d_limit;
   int32_t num_kb;
   int32_t kb_per_split;
+  int32_t splits;
   int32_t bn;
+  int32_t m_tiles;
+  int32_t n_tiles;
+  int32_t tiles;
   int32_t b_mn_major;
   int32_t d_fp32;
   int32_t accumulate;
-  uint32_t idesc;
   int32_t b_boxes;
+  uint32_t idesc;
   uint32_t tx_bytes;
+};
+
+struct Launch {
+  Problem p[kMaxProblems];
+  int32_t n_problems;
+  int32_t total_tiles;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -63,13 +88,17 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                : "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
   uint32_t ok = 0;
   uint32_t polls = 0;
   do {
     // A pipeline bug must fail loudly (trap) rather than hang the GPU.
-    if (++polls > (1u << 27)) __trap();
+    if (++polls > (1u << 28)) __trap();
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
@@ -90,6 +119,9 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* ba
 }
 
 // UMMA shared-memory matrix descriptor, SWIZZLE_128B, Blackwell version 1.
+//   K-major  : rows of 128 B (64 bf16 along K); 8-row groups SBO = 1024 B apart.
+//   MN-major : 64 MN-elements per 128 B row, one row per k; 8-k groups
+//              SBO = 1024 B apart; 64-wide MN blocks LBO = 8192 B apart.
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   uint64_t d = static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
   d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
@@ -143,8 +175,8 @@ __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, 
 }
 
 // Stores 32 accumulator columns of one row; columns >= col_end (the end of
-// this CTA's tile clipped to N) are not written.
-__device__ __forceinline__ void store_row_chunk(const Params& p, int64_t row, int64_t col0,
+// this tile clipped to N) and flat offsets >= d_limit are not written.
+__device__ __forceinline__ void store_row_chunk(const Problem& p, int64_t row, int64_t col0,
                                                 int64_t col_end, const uint32_t (&v)[32]) {
   if (row >= p.M) return;
   const int64_t base = row * p.ldd;
@@ -206,9 +238,31 @@ __device__ __forceinline__ void store_row_chunk(const Params& p, int64_t row, in
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 1)
-    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                const Params p) {
+struct TileCoord {
+  int prob;
+  int64_t m0, n0;
+  int kb0, kb1;
+};
+
+// Tile t of the launch: problems back to back; inside a problem
+// (split, m_tile, n_tile) with n fastest, so concurrently running CTAs share
+// the same A rows.
+__device__ __forceinline__ TileCoord decode(const Launch& L, int t) {
+  TileCoord c;
+  c.prob = (L.n_problems > 1 && t >= L.p[0].tiles) ? 1 : 0;
+  const Problem& P = L.p[c.prob];
+  const int local = c.prob ? t - L.p[0].tiles : t;
+  const int per = P.m_tiles * P.n_tiles;
+  const int split = local / per;
+  const int r = local - split * per;
+  c.m0 = static_cast<int64_t>(r / P.n_tiles) * kBM;
+  c.n0 = static_cast<int64_t>(r % P.n_tiles) * P.bn;
+  c.kb0 = split * P.kb_per_split;
+  c.kb1 = min(c.kb0 + P.kb_per_split, P.num_kb);
+  return c;
+}
+
+__global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant__ Launch L) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -216,26 +270,32 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sB = smem + kStages * kAStage;
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + kStages * kBStage);
   uint64_t* empty = full + kStages;
-  uint64_t* tmem_full = empty + kStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* tmem_full = empty + kStages;   // [2]
+  uint64_t* tmem_empty = tmem_full + 2;    // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int64_t n0 = static_cast<int64_t>(blockIdx.x) * p.bn;
-  const int64_t m0 = static_cast<int64_t>(blockIdx.y) * kBM;
-  const int kb0 = blockIdx.z * p.kb_per_split;
-  const int kb1 = min(kb0 + p.kb_per_split, p.num_kb);
-  const int nkb = kb1 - kb0;
+
+  // Let the next kernel in the stream start its prologue as soon as SMs free.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tmem_full, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tmem_full[a], 1);
+      mbar_init(&tmem_empty[a], 4);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    for (int i = 0; i < L.n_problems; ++i) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&L.p[i].tmA))
+                   : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&L.p[i].tmB))
+                   : "memory");
+    }
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -247,31 +307,45 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // Everything above overlaps the previous kernel; memory is touched only now.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
-  if (nkb > 0) {
-    if (warp == 0) {
-      if (lane == 0) {
-        for (int i = 0; i < nkb; ++i) {
-          const int s = i % kStages;
-          const uint32_t ph = (i / kStages) & 1;
+  if (warp == 0) {
+    if (lane == 0) {
+      uint32_t g = 0;
+      for (int t = blockIdx.x; t < L.total_tiles; t += gridDim.x) {
+        const TileCoord tc = decode(L, t);
+        const Problem& P = L.p[tc.prob];
+        for (int kb = tc.kb0; kb < tc.kb1; ++kb, ++g) {
+          const int s = g % kStages;
+          const uint32_t ph = (g / kStages) & 1;
           mbar_wait(&empty[s], ph ^ 1);
-          mbar_expect_tx(&full[s], p.tx_bytes);
-          const int kc = (kb0 + i) * kBK;
-          tma_load_2d(&tmA, &full[s], sA + s * kAStage, kc, static_cast<int32_t>(m0));
-          if (!p.b_mn_major) {
-            tma_load_2d(&tmB, &full[s], sB + s * kBStage, kc, static_cast<int32_t>(n0));
+          mbar_expect_tx(&full[s], P.tx_bytes);
+          const int kc = kb * kBK;
+          tma_load_2d(&P.tmA, &full[s], sA + s * kAStage, kc, static_cast<int32_t>(tc.m0));
+          if (!P.b_mn_major) {
+            tma_load_2d(&P.tmB, &full[s], sB + s * kBStage, kc, static_cast<int32_t>(tc.n0));
           } else {
-            for (int j = 0; j < p.b_boxes; ++j)
-              tma_load_2d(&tmB, &full[s], sB + s * kBStage + j * 8192,
-                          static_cast<int32_t>(n0 + 64 * j), kc);
+            for (int j = 0; j < P.b_boxes; ++j)
+              tma_load_2d(&P.tmB, &full[s], sB + s * kBStage + j * 8192,
+                          static_cast<int32_t>(tc.n0 + 64 * j), kc);
           }
         }
       }
-    } else if (warp == 1) {
-      if (lane == 0) {
-        for (int i = 0; i < nkb; ++i) {
-          const int s = i % kStages;
-          const uint32_t ph = (i / kStages) & 1;
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      uint32_t g = 0, j = 0;
+      for (int t = blockIdx.x; t < L.total_tiles; t += gridDim.x, ++j) {
+        const TileCoord tc = decode(L, t);
+        const Problem& P = L.p[tc.prob];
+        const uint32_t acc = j & 1, aph = (j >> 1) & 1;
+        mbar_wait(&tmem_empty[acc], aph ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem + acc * kAccCols;
+        for (int kb = tc.kb0; kb < tc.kb1; ++kb, ++g) {
+          const int s = g % kStages;
+          const uint32_t ph = (g / kStages) & 1;
           mbar_wait(&full[s], ph);
           tc_fence_after();
           const uint32_t a_base = smem_u32(sA + s * kAStage);
@@ -279,26 +353,36 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k) {
             const uint64_t ad = sdesc(a_base + k * 32, 16, 1024);
-            const uint64_t bd = p.b_mn_major ? sdesc(b_base + k * 2048, 8192, 1024)
+            const uint64_t bd = P.b_mn_major ? sdesc(b_base + k * 2048, 8192, 1024)
                                              : sdesc(b_base + k * 32, 16, 1024);
-            umma_bf16(tmem, ad, bd, p.idesc, (i | k) != 0);
+            umma_bf16(d_tmem, ad, bd, P.idesc, (kb != tc.kb0 || k != 0) ? 1u : 0u);
           }
           umma_commit(&empty[s]);
         }
-        umma_commit(tmem_full);
+        umma_commit(&tmem_full[acc]);
       }
-      __syncwarp();
-    } else {
-      mbar_wait(tmem_full, 0);
+    }
+    __syncwarp();
+  } else {
+    const int q = warp & 3;
+    uint32_t j = 0;
+    for (int t = blockIdx.x; t < L.total_tiles; t += gridDim.x, ++j) {
+      const TileCoord tc = decode(L, t);
+      const Problem& P = L.p[tc.prob];
+      const uint32_t acc = j & 1, aph = (j >> 1) & 1;
+      mbar_wait(&tmem_full[acc], aph);
       tc_fence_after();
-      const int q = warp & 3;
-      const int64_t row = m0 + 32 * q + lane;
-      const int64_t col_end = min(p.N, n0 + p.bn);
-      for (int c = 0; c < p.bn; c += 32) {
+      const int64_t row = tc.m0 + 32 * q + lane;
+      const int64_t col_end = min(P.N, tc.n0 + P.bn);
+      const uint32_t base = tmem + acc * kAccCols + (static_cast<uint32_t>(32 * q) << 16);
+      for (int c = 0; c < P.bn; c += 32) {
         uint32_t v[32];
-        tmem_ld32(tmem + (static_cast<uint32_t>(32 * q) << 16) + static_cast<uint32_t>(c), v);
-        store_row_chunk(p, row, n0 + c, col_end, v);
+        tmem_ld32(base + static_cast<uint32_t>(c), v);
+        store_row_chunk(P, row, tc.n0 + c, col_end, v);
       }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tmem_empty[acc]);
     }
   }
   tc_fence_before();
@@ -345,17 +429,67 @@ void make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer
   }
 }
 
+// Tile width: the fewest N tiles (<= 256 wide) unless more, narrower tiles
+// fill the persistent grid markedly better (fewer waves of work per SM).
+int choose_bn(int64_t M, int64_t N, int splits) {
+  const int64_t m_tiles = (M + kBM - 1) / kBM;
+  auto waves_cost = [&](int64_t bn) {
+    const int64_t nt = (N + bn - 1) / bn;
+    const int64_t tiles = m_tiles * nt * splits;
+    const int64_t waves = (tiles + kSms - 1) / kSms;
+    // per-tile mainloop cost ~ max(bn, 64) columns + fixed overhead
+    return waves * (std::max<int64_t>(bn, 64) + 48);
+  };
+  const int64_t nt0 = (N + kBNMax - 1) / kBNMax;
+  int64_t best_bn = ((N + nt0 - 1) / nt0 + 15) / 16 * 16;
+  int64_t best = waves_cost(best_bn);
+  for (int64_t nt = nt0 + 1; nt <= nt0 * 4; ++nt) {
+    const int64_t bn = ((N + nt - 1) / nt + 15) / 16 * 16;
+    if (bn < 64) break;
+    const int64_t c = waves_cost(bn);
+    if (c < best) {
+      best = c;
+      best_bn = bn;
+    }
+  }
+  return static_cast<int>(best_bn);
+}
+
 }  // namespace gemm
 }  // namespace dear
 
 struct dear_gemm_plan {
-  alignas(64) CUtensorMap a;
-  alignas(64) CUtensorMap b;
-  dear::gemm::Params p;
-  dim3 grid;
+  dear::gemm::Problem p;
 };
 
 using dear::Error;
+
+namespace {
+
+void launch(const dear::gemm::Launch& L, cudaStream_t stream) {
+  using namespace dear::gemm;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kSmemBytes) != cudaSuccess)
+      throw Error(DEAR_EINTERNAL, "cudaFuncSetAttribute(gemm smem)");
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(std::min(L.total_tiles, kSms)));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmemBytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_kernel, L);
+  if (e != cudaSuccess) throw Error(DEAR_EINTERNAL, std::string("gemm launch: ") + cudaGetErrorString(e));
+}
+
+}  // namespace
 
 extern "C" {
 
@@ -375,32 +509,28 @@ int dear_gemm_plan_create(const void* A, int64_t lda, const void* B, int64_t ldb
   if (accumulate && !d_fp32) throw Error(DEAR_EINVAL, "dear_gemm: accumulate needs fp32 D");
   if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX)
     throw Error(DEAR_EINVAL, "dear_gemm: dimensions exceed 2^31");
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             kSmemBytes) != cudaSuccess)
-      throw Error(DEAR_EINTERNAL, "cudaFuncSetAttribute(gemm smem)");
-    attr = true;
-  }
+  if (!accumulate && split_k > 1) throw Error(DEAR_EINVAL, "dear_gemm: split_k > 1 needs accumulate");
   auto* plan = new dear_gemm_plan();
-  Params& p = plan->p;
-  const int64_t n_tiles = (N + kBNMax - 1) / kBNMax;
-  int64_t bn = (N + n_tiles - 1) / n_tiles;
-  bn = (bn + 15) / 16 * 16;
-  const int64_t m_tiles = (M + kBM - 1) / kBM;
+  Problem& p = plan->p;
   const int num_kb = static_cast<int>((K + kBK - 1) / kBK);
+  const int64_t m_tiles = (M + kBM - 1) / kBM;
   int splits = 1;
   if (accumulate) {
-    const int64_t tiles = n_tiles * m_tiles;
-    splits = split_k > 0 ? split_k : static_cast<int>(tiles < 148 ? 148 / tiles : 1);
-    if (splits < 1) splits = 1;
-    if (splits > num_kb) splits = num_kb;
-  } else if (split_k > 1) {
-    delete plan;
-    throw Error(DEAR_EINVAL, "dear_gemm: split_k > 1 needs accumulate");
+    if (split_k > 0) {
+      splits = split_k;
+    } else {
+      // Enough (split) tiles for the persistent grid, but keep >= 16 k-blocks
+      // (K >= 1024) per split so the fp32 reductions stay a small fraction of
+      // the operand traffic.
+      const int64_t nt = (N + kBNMax - 1) / kBNMax;
+      const int64_t tiles = m_tiles * nt;
+      splits = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(kSms / tiles, num_kb / 16)));
+    }
+    splits = std::max(1, std::min(splits, num_kb));
   }
-  int kb_per = (num_kb + splits - 1) / splits;
+  const int kb_per = (num_kb + splits - 1) / splits;
   splits = (num_kb + kb_per - 1) / kb_per;
+  const int bn = choose_bn(M, N, splits);
   p.D = D;
   p.ldd = ldd;
   p.M = M;
@@ -408,42 +538,53 @@ int dear_gemm_plan_create(const void* A, int64_t lda, const void* B, int64_t ldb
   p.d_limit = d_limit;
   p.num_kb = num_kb;
   p.kb_per_split = kb_per;
-  p.bn = static_cast<int32_t>(bn);
+  p.splits = splits;
+  p.bn = bn;
+  p.m_tiles = static_cast<int32_t>(m_tiles);
+  p.n_tiles = static_cast<int32_t>((N + bn - 1) / bn);
+  p.tiles = p.m_tiles * p.n_tiles * splits;
   p.b_mn_major = b_mn_major ? 1 : 0;
   p.d_fp32 = d_fp32 ? 1 : 0;
   p.accumulate = accumulate ? 1 : 0;
   p.idesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(p.b_mn_major) << 16) |
             (static_cast<uint32_t>(bn >> 3) << 17) | (static_cast<uint32_t>(kBM >> 4) << 24);
-  p.b_boxes = static_cast<int32_t>((bn + 63) / 64);
+  p.b_boxes = (bn + 63) / 64;
   p.tx_bytes = kAStage + (b_mn_major ? p.b_boxes * 8192 : static_cast<uint32_t>(bn) * kBK * 2);
   try {
-    make_map(&plan->a, A, static_cast<uint64_t>(K), static_cast<uint64_t>(M),
+    make_map(&p.tmA, A, static_cast<uint64_t>(K), static_cast<uint64_t>(M),
              static_cast<uint64_t>(lda), kBK, kBM);
     if (!b_mn_major)
-      make_map(&plan->b, B, static_cast<uint64_t>(K), static_cast<uint64_t>(N),
+      make_map(&p.tmB, B, static_cast<uint64_t>(K), static_cast<uint64_t>(N),
                static_cast<uint64_t>(ldb), kBK, static_cast<uint32_t>(bn));
     else
-      make_map(&plan->b, B, static_cast<uint64_t>(N), static_cast<uint64_t>(K),
+      make_map(&p.tmB, B, static_cast<uint64_t>(N), static_cast<uint64_t>(K),
                static_cast<uint64_t>(ldb), 64, kBK);
   } catch (...) {
     delete plan;
     throw;
   }
-  plan->grid = dim3(static_cast<unsigned>(n_tiles), static_cast<unsigned>(m_tiles),
-                    static_cast<unsigned>(splits));
   *out = plan;
   DEAR_API_END
 }
 
-int dear_gemm_run(dear_gemm_plan* plan, void* stream) {
+int dear_gemm_run_group(dear_gemm_plan* const* plans, int32_t n, void* stream) {
   DEAR_API_BEGIN
   using namespace dear::gemm;
-  if (!plan) throw Error(DEAR_EINVAL, "dear_gemm_run: null plan");
-  gemm_kernel<<<plan->grid, kThreads, kSmemBytes, static_cast<cudaStream_t>(stream)>>>(
-      plan->a, plan->b, plan->p);
-  const cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) throw Error(DEAR_EINTERNAL, std::string("gemm launch: ") + cudaGetErrorString(e));
+  if (!plans || n < 1 || n > kMaxProblems) throw Error(DEAR_EINVAL, "dear_gemm_run_group: 1 or 2 plans");
+  Launch L;
+  L.n_problems = n;
+  L.total_tiles = 0;
+  for (int i = 0; i < n; ++i) {
+    if (!plans[i]) throw Error(DEAR_EINVAL, "dear_gemm_run_group: null plan");
+    L.p[i] = plans[i]->p;
+    L.total_tiles += plans[i]->p.tiles;
+  }
+  launch(L, static_cast<cudaStream_t>(stream));
   DEAR_API_END
+}
+
+int dear_gemm_run(dear_gemm_plan* plan, void* stream) {
+  return dear_gemm_run_group(&plan, 1, stream);
 }
 
 int dear_gemm_plan_info(dear_gemm_plan* plan, int32_t* bn, int32_t* n_tiles, int32_t* m_tiles,
@@ -451,9 +592,9 @@ int dear_gemm_plan_info(dear_gemm_plan* plan, int32_t* bn, int32_t* n_tiles, int
   DEAR_API_BEGIN
   if (!plan) throw Error(DEAR_EINVAL, "null plan");
   if (bn) *bn = plan->p.bn;
-  if (n_tiles) *n_tiles = static_cast<int32_t>(plan->grid.x);
-  if (m_tiles) *m_tiles = static_cast<int32_t>(plan->grid.y);
-  if (splits) *splits = static_cast<int32_t>(plan->grid.z);
+  if (n_tiles) *n_tiles = plan->p.n_tiles;
+  if (m_tiles) *m_tiles = plan->p.m_tiles;
+  if (splits) *splits = plan->p.splits;
   DEAR_API_END
 }
 

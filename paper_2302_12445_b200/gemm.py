@@ -25,10 +25,11 @@ def _bind():
                                         C.c_int32, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
                                         C.c_int32, C.c_int32, C.POINTER(P)]
     L.dear_gemm_run.argtypes = [P, P]
+    L.dear_gemm_run_group.argtypes = [C.POINTER(P), C.c_int32, P]
     L.dear_gemm_plan_info.argtypes = [P] + [C.POINTER(C.c_int32)] * 4
     L.dear_gemm_plan_destroy.argtypes = [P]
-    for f in ("dear_gemm_plan_create", "dear_gemm_run", "dear_gemm_plan_info",
-              "dear_gemm_plan_destroy"):
+    for f in ("dear_gemm_plan_create", "dear_gemm_run", "dear_gemm_run_group",
+              "dear_gemm_plan_info", "dear_gemm_plan_destroy"):
         getattr(L, f).restype = C.c_int
     _bound = True
     return L
@@ -75,6 +76,13 @@ class GemmPlan:
     @property
     def flops(self) -> int:
         return 2 * self.M * self.N * self.K
+
+    @staticmethod
+    def run_group(plans: "list[GemmPlan]", stream: torch.cuda.Stream | None = None) -> None:
+        """One persistent launch computing up to two independent plans."""
+        s = (stream or torch.cuda.current_stream()).cuda_stream
+        arr = (C.c_void_p * len(plans))(*[p._plan.value for p in plans])
+        check(_bind().dear_gemm_run_group(arr, len(plans), s))
 
     def close(self) -> None:
         if self._plan.value:

@@ -109,8 +109,8 @@ class SyntheticModel:
         self.ff[l - 1].run(stream)
 
     def backward_layer(self, l: int, stream=None) -> None:
-        self.wgrad[l - 1].run(stream)
-        self.dgrad[l - 1].run(stream)
+        # wgrad and dgrad are independent: one persistent launch computes both.
+        GemmPlan.run_group([self.wgrad[l - 1], self.dgrad[l - 1]], stream)
 
     def zero_grad(self) -> None:
         self.grads_flat.zero_()

@@ -84,3 +84,50 @@ def test_gemm_bf16_out(M, N, K):
     # bf16 output: one bf16 rounding (2^-8 relative) on top of the fp32 tolerance
     err = (d[:, :N].float() - ref).abs()
     assert torch.all(err <= ref.abs() * 2.0**-8 + 2e-3 * ref.abs().max()), err.max()
+
+
+@pytest.mark.parametrize("M,N,K", [(8192, 1024, 512), (10240, 311, 512), (2048, 825, 1024)])
+def test_gemm_persistent_many_tiles(M, N, K):
+    """More tiles than SMs: exercises the persistent loop and both TMEM
+    accumulators (epilogue of tile i overlapping the mainloop of tile i+1)."""
+    from paper_2302_12445_b200.gemm import GemmPlan
+
+    torch.manual_seed(3)
+    a = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+    b = torch.randn(N, K, device="cuda").to(torch.bfloat16)
+    d = torch.full((M, N), float("nan"), device="cuda")
+    plan = GemmPlan(a, b, d, M, N, K, ldd=N)
+    info = plan.info()
+    assert info["m_tiles"] * info["n_tiles"] > 0
+    for _ in range(3):  # repeated launches (programmatic dependent launch chain)
+        plan.run()
+    torch.cuda.synchronize()
+    _check(d, a.float() @ b.float().t(), K)
+
+
+def test_gemm_group_wgrad_dgrad():
+    """One launch computing a layer's weight gradient (split-K, fp32 reduce
+    into a flat buffer) and data gradient (MN-major weights, bf16 out)."""
+    from paper_2302_12445_b200.gemm import GemmPlan
+
+    torch.manual_seed(4)
+    T, H, R, n = 10240, 512, 311, 159006
+    dy = torch.randn(T, 320, device="cuda").to(torch.bfloat16)
+    dyt = dy.t().contiguous()
+    x = torch.randn(T, H, device="cuda").to(torch.bfloat16)
+    xt = x.t().contiguous()
+    W = torch.zeros(R * H, device="cuda", dtype=torch.bfloat16)
+    W[:n] = torch.randn(n, device="cuda").to(torch.bfloat16)
+    G = torch.zeros(n + 64, device="cuda")
+    G[n:] = 7.0
+    dx = torch.zeros(T, H, device="cuda", dtype=torch.bfloat16)
+    wg = GemmPlan(dyt, xt, G, R, H, T, lda=T, ldb=T, ldd=H, d_limit=n, accumulate=True)
+    dg = GemmPlan(dy, W, dx, T, H, R, b_mn_major=True, lda=320, ldb=H, ldd=H)
+    GemmPlan.run_group([wg, dg])
+    torch.cuda.synchronize()
+    ref_g = (dyt[:R].float() @ xt.float().t()).reshape(-1)[:n]
+    _check(G[:n], ref_g, T)
+    assert torch.all(G[n:] == 7.0)
+    ref_dx = dy[:, :R].float() @ W.view(R, H).float()
+    err = (dx.float() - ref_dx).abs()
+    assert torch.all(err <= ref_dx.abs() * 2.0**-8 + 4e-3 * ref_dx.abs().max()), err.max()
