@@ -154,6 +154,10 @@ class Reference:
         lib.ref_free.argtypes = [C.c_void_p]
         lib.ref_time_sgd_steps.argtypes = [_i64p, C.c_int, C.c_int, C.c_int, C.c_int,
                                            C.c_uint64, C.c_double, _f64p]
+        D = C.POINTER(C.c_double)
+        lib.ref_calibrate.argtypes = [_f64p, _f64p, C.c_int, C.c_int, D, D, C.POINTER(C.c_int)]
+        lib.ref_costs.argtypes = [C.c_double, C.c_int, C.c_double, C.c_double, D, D]
+        lib.ref_theory.argtypes = [C.c_double] * 4 + [C.c_int, D, D, D]
         self.lib = lib
 
     def _check(self, rc):
@@ -232,6 +236,25 @@ class Reference:
             return json.loads(C.string_at(p).decode())
         finally:
             self.lib.ref_free(p)
+
+    def calibrate(self, measurements, workers: int) -> dict:
+        b = np.ascontiguousarray([m[0] for m in measurements], np.float64)
+        t = np.ascontiguousarray([m[1] for m in measurements], np.float64)
+        a, be, cl = C.c_double(), C.c_double(), C.c_int()
+        self._check(self.lib.ref_calibrate(b, t, len(b), workers, C.byref(a), C.byref(be),
+                                           C.byref(cl)))
+        return {"alpha": a.value, "beta": be.value, "clamped": bool(cl.value)}
+
+    def costs(self, nbytes: float, workers: int, alpha: float, beta: float):
+        rs, ar = C.c_double(), C.c_double()
+        self._check(self.lib.ref_costs(nbytes, workers, alpha, beta, C.byref(rs), C.byref(ar)))
+        return rs.value, ar.value
+
+    def theory(self, t_ff, t_bp, t_rs, t_ag, workers):
+        d, b, s = C.c_double(), C.c_double(), C.c_double()
+        self._check(self.lib.ref_theory(t_ff, t_bp, t_rs, t_ag, workers, C.byref(d), C.byref(b),
+                                        C.byref(s)))
+        return {"dear": d.value, "baseline": b.value, "smax": s.value}
 
     def time_sgd_steps(self, bucket_elems, P: int, threads: int, steps: int,
                        seed: int = 1, lr: float = 0.05) -> np.ndarray:

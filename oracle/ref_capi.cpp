@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "dearsim/analysis.hpp"
+#include "dearsim/cost_model.hpp"
 #include "dearsim/collective.hpp"
 #include "dearsim/fusion.hpp"
 #include "dearsim/model.hpp"
@@ -263,6 +264,48 @@ char* ref_simulate_json(const int64_t* counts, int L, const double* t_ff, const 
 }
 
 void ref_free(void* p) { std::free(p); }
+
+// calibrate_alpha_beta (cost_model.cpp:79-133) on (bytes, seconds) pairs.
+int ref_calibrate(const double* bytes, const double* seconds, int n, int workers, double* alpha,
+                  double* beta, int* clamped) {
+  try {
+    std::vector<std::pair<double, double>> m;
+    for (int i = 0; i < n; ++i) m.push_back({bytes[i], seconds[i]});
+    const Calibration c = calibrate_alpha_beta(m, workers);
+    *alpha = c.alpha;
+    *beta = c.beta;
+    *clamped = c.clamped ? 1 : 0;
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+// reduce_scatter_time / all_reduce_time (cost_model.cpp:34-48);
+// theoretical_times (analysis.cpp:50-60); max_speedup (:34-48).
+int ref_costs(double bytes, int workers, double alpha, double beta, double* rs, double* ar) {
+  try {
+    const ClusterSpec c{"capi", workers, alpha, beta};
+    *rs = reduce_scatter_time(bytes, c);
+    *ar = all_reduce_time(bytes, c);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+int ref_theory(double t_ff, double t_bp, double t_rs, double t_ag, int workers, double* dear,
+               double* baseline, double* smax) {
+  try {
+    const TheoreticalTimes t = theoretical_times(t_ff, t_bp, t_rs, t_ag);
+    *dear = t.dear;
+    *baseline = t.baseline;
+    *smax = max_speedup(t_ff, t_bp, t_rs, t_ag, workers);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
 
 // CPU baseline: the reference's per-bucket S-SGD step (sgd_step =
 // ring RS + ring AG + 1/P + w -= lr*mean, fp64) over `n_buckets` buckets of

@@ -1,0 +1,171 @@
+"""alpha-beta collective cost model, DeAR/WFBP schedule prediction and the
+paper's analysis bounds — the reference's prediction layer, fed with what the
+B200 runtime measures.
+
+Restates (tested against the reference build in tests/test_costmodel.py):
+  * reduce_scatter_time / all_gather_time / all_reduce_time
+        proj/src/cost_model.cpp:34-48      (P-1)(alpha + (d/P) beta), AR = RS + AG
+  * calibrate_alpha_beta                 proj/src/cost_model.cpp:79-133
+  * theoretical_times (Eq. 7 / Eq. 8), max_speedup (Eq. 6), breakdown
+        proj/src/analysis.cpp:34-101
+  * predict_iteration: build_graph (task_graph.cpp:127-210) + the two-stream
+    list scheduler (simulate.cpp:65-159) on measured per-layer times.
+"""
+from __future__ import annotations
+
+import heapq
+
+import numpy as np
+
+from .plan import build_fusion_plan
+
+
+def reduce_scatter_time(nbytes: float, P: int, alpha: float, beta: float) -> float:
+    if not (nbytes >= 0) or P < 1 or alpha < 0 or beta < 0:
+        raise ValueError("message_bytes must be finite and >= 0; P >= 1; alpha, beta >= 0")
+    return (P - 1.0) * (alpha + (nbytes / P) * beta)
+
+
+def all_gather_time(nbytes: float, P: int, alpha: float, beta: float) -> float:
+    return reduce_scatter_time(nbytes, P, alpha, beta)
+
+
+def all_reduce_time(nbytes: float, P: int, alpha: float, beta: float) -> float:
+    return reduce_scatter_time(nbytes, P, alpha, beta) + all_gather_time(nbytes, P, alpha, beta)
+
+
+def calibrate_alpha_beta(measurements, workers: int) -> dict:
+    """Least-squares fit of t = 2(P-1) alpha + 2(P-1)(d/P) beta to measured
+    all-reduce times [(bytes, seconds)], size column rescaled for conditioning,
+    negative coefficients clamped to 0."""
+    if workers < 2:
+        raise ValueError("calibrate_alpha_beta: workers must be >= 2")
+    if len(measurements) < 2:
+        raise ValueError("calibrate_alpha_beta: need at least 2 measurements")
+    d = np.array([m[0] for m in measurements], np.float64)
+    t = np.array([m[1] for m in measurements], np.float64)
+    if not np.all(np.isfinite(d)) or not np.all(np.isfinite(t)) or np.any(d < 0):
+        raise ValueError("calibrate_alpha_beta: measurements must be finite, sizes >= 0")
+    if np.all(d == d[0]):
+        raise ValueError("rank-deficient calibration: all message sizes are identical")
+    p = float(workers)
+    c = 2.0 * (p - 1.0)
+    scale = d.max() if d.max() > 0 else 1.0
+    A = np.stack([np.full_like(d, c), c * (d / p) / scale], axis=1)
+    x, *_ = np.linalg.lstsq(A, t, rcond=None)
+    alpha, beta = float(x[0]), float(x[1] / scale)
+    clamped = False
+    if alpha < 0:
+        alpha, clamped = 0.0, True
+    if beta < 0:
+        beta, clamped = 0.0, True
+    return {"alpha": alpha, "beta": beta, "clamped": clamped}
+
+
+def theoretical_times(t_ff, t_bp, t_rs, t_ag) -> dict:
+    """Eq. 7 (DeAR) and Eq. 8 (all-reduce baseline) bounds."""
+    for v in (t_ff, t_bp, t_rs, t_ag):
+        if not (v >= 0) or not np.isfinite(v):
+            raise ValueError("times must be finite and >= 0")
+    return {"dear": max(t_ff, t_ag) + max(t_bp, t_rs), "baseline": t_ff + max(t_bp, t_rs + t_ag)}
+
+
+def max_speedup(t_ff, t_bp, t_rs, t_ag, workers: int) -> float:
+    """Eq. 6: S_max = P (t_ff + t_bp) / (max(t_ff, t_ag) + max(t_bp, t_rs))."""
+    den = max(t_ff, t_ag) + max(t_bp, t_rs)
+    if not den > 0:
+        raise ValueError("max_speedup: denominator is zero")
+    return workers * (t_ff + t_bp) / den
+
+
+def exposed_comm(iteration: float, t_ff_total: float, t_bp_total: float) -> float:
+    """breakdown (analysis.cpp:85-101): iteration - sum(t_ff) - sum(t_bp), >= 0."""
+    return max(0.0, iteration - t_ff_total - t_bp_total)
+
+
+def predict_iteration(layer_bytes, t_ff, t_bp, policy: str, buffer_bytes: int, P: int,
+                      alpha: float, beta: float, group_dependency: bool = False) -> dict:
+    """Simulated steady-state iteration (seconds) of one worker: BP_L..BP_1 and
+    FF_1..FF_L on the compute stream, RS/AG/AR on the comm stream, issue order
+    and dependencies of task_graph.cpp:127-210, non-preemptive list
+    scheduling by (issue_order, id) as simulate.cpp:65-159."""
+    L = len(layer_bytes)
+    tasks = []  # (kind, subject, duration, deps, order, resource)
+
+    def add(kind, subj, dur, deps, order):
+        tasks.append([kind, subj, dur, list(deps), order, 0 if kind in ("FF", "BP") else 1])
+        return len(tasks) - 1
+
+    bp, ff, order = [0] * (L + 2), [0] * (L + 2), 0
+    for l in range(L, 0, -1):
+        bp[l] = add("BP", l, t_bp[l - 1], [bp[l + 1]] if l < L else [], order)
+        order += 1
+    for l in range(1, L + 1):
+        ff[l] = add("FF", l, t_ff[l - 1], [ff[l - 1]] if l > 1 else [], order)
+        order += 1
+    fused = policy.endswith("_FUSED")
+    plan = build_fusion_plan(list(layer_bytes), buffer_bytes if fused else 0)
+    gbytes = [sum(layer_bytes[lo - 1:hi]) for lo, hi in plan]
+    deps_bp = [[bp[l] for l in range(hi, lo - 1, -1)] for lo, hi in plan]
+    order = 0
+    if policy.startswith("WFBP"):
+        for gi, (lo, hi) in enumerate(plan):
+            t = add("AR", gi + 1, all_reduce_time(gbytes[gi], P, alpha, beta), deps_bp[gi], order)
+            order += 1
+            for l in range(lo, hi + 1):
+                tasks[ff[l]][3].append(t)
+    elif policy.startswith("DEAR"):
+        rs = []
+        for gi in range(len(plan)):
+            rs.append(add("RS", gi + 1, reduce_scatter_time(gbytes[gi], P, alpha, beta),
+                          deps_bp[gi], order))
+            order += 1
+        bar = -1
+        if not group_dependency:
+            bar = add("BARRIER", 0, 0.0, rs, order)
+            order += 1
+        for gi in range(len(plan) - 1, -1, -1):
+            lo, hi = plan[gi]
+            t = add("AG", gi + 1, all_gather_time(gbytes[gi], P, alpha, beta),
+                    [bar] if bar >= 0 else [rs[gi]], order)
+            order += 1
+            for l in range(lo, hi + 1):
+                tasks[ff[l]][3].append(t)
+    else:
+        raise ValueError(f"unknown policy {policy!r}")
+    n = len(tasks)
+    remaining = [len(t[3]) for t in tasks]
+    finish = [0.0] * n
+    dependents = [[] for _ in range(n)]
+    for i, t in enumerate(tasks):
+        for d in t[3]:
+            dependents[d].append(i)
+    ev = [(0.0, 1, i) for i in range(n) if not tasks[i][3]]
+    heapq.heapify(ev)
+    ready, running, end_at = [[], []], [-1, -1], [0.0] * n
+    done = 0
+    while ev:
+        now = ev[0][0]
+        while ev and ev[0][0] == now:
+            _, typ, i = heapq.heappop(ev)
+            if typ == 0:
+                running[tasks[i][5]] = -1
+                done += 1
+                for j in dependents[i]:
+                    finish[j] = max(finish[j], now)
+                    remaining[j] -= 1
+                    if remaining[j] == 0:
+                        heapq.heappush(ev, (finish[j], 1, j))
+            else:
+                heapq.heappush(ready[tasks[i][5]], (tasks[i][4], i))
+        for r in (0, 1):
+            if running[r] == -1 and ready[r]:
+                _, i = heapq.heappop(ready[r])
+                running[r] = i
+                end_at[i] = now + tasks[i][2]
+                heapq.heappush(ev, (end_at[i], 0, i))
+    if done != n:
+        raise RuntimeError("simulate: cycle detected")
+    it = max(end_at)
+    return {"iteration_seconds": it, "buckets": len(plan),
+            "exposed_comm_seconds": exposed_comm(it, float(sum(t_ff)), float(sum(t_bp)))}

@@ -20,9 +20,25 @@ struct Unit {
   float* b;
   void* c;
   int64_t len;
+  int64_t start;  // prefix sum of len over the op's unit list
 };
 
-constexpr int64_t kUnitElems = 8192;
+// Units are cut at this length only to bound the per-unit index arithmetic;
+// load balance comes from giving every CTA an equal slice of the op's total
+// elements: the host precomputes, per CTA, the unit and offset its slice
+// starts at (a Slice table next to the units).
+constexpr int64_t kUnitElems = 1 << 20;
+
+// Grid of every bucket-op launch: 4 resident 256-thread CTAs on each of the
+// 148 SMs, one wave, equal element slices.
+constexpr int kSlices = 148 * 4;
+
+struct Slice {
+  int32_t unit;   // first unit of this CTA's slice
+  int32_t pad;
+  int64_t off;    // offset inside that unit
+  int64_t count;  // elements in the slice (multiple of 4 except the last)
+};
 
 // Device-resident optimizer hyper-parameters (graph-safe lr changes).
 struct HyperParams {
@@ -36,11 +52,17 @@ struct HyperParams {
   int32_t pad;
 };
 
-// Launchers (stream-ordered, no host sync). n_units may be 0.
-cudaError_t launch_pack(const Unit* units, int n_units, float scale, cudaStream_t s);
-cudaError_t launch_update(const Unit* units, int n_units, const HyperParams* hp,
-                          int has_momentum_buf, int use_momentum, int use_wd, cudaStream_t s);
-cudaError_t launch_unpack(const Unit* units, int n_units, int with_shadow, cudaStream_t s);
+// Launchers (stream-ordered, no host sync). n_units may be 0; total is the
+// sum of the units' lengths.
+cudaError_t launch_pack(const Unit* units, const Slice* slices, int64_t total, float scale,
+                        cudaStream_t s);
+cudaError_t launch_update(const Unit* units, const Slice* slices, int64_t total,
+                          const HyperParams* hp, int has_momentum_buf, int use_momentum,
+                          int use_wd, cudaStream_t s);
+cudaError_t launch_unpack(const Unit* units, const Slice* slices, int64_t total, int with_shadow,
+                          cudaStream_t s);
+// Host: the Slice table (kSlices entries) for a unit list with prefix starts.
+void make_slices(const Unit* units, int n_units, int64_t total, Slice* out);
 
 // Local-group collectives over P same-device buffers (ring order, in place):
 // rs: bufs[r][r*stride + i] = fold_k bufs[(r+1+k)%P][r*stride + i], k = 0..P-1

@@ -1,6 +1,6 @@
 // Hand-written sm_100a GEMM for the synthetic layer compute.
 //
-//   TMA (cp.async.bulk.tensor.2d, 128B swizzle) -> 4-stage smem ring
+//   TMA (cp.async.bulk.tensor.2d, 128B swizzle) -> 4..8-stage smem ring
 //   (mbarrier full/empty) -> tcgen05.mma kind::f16 (bf16 in, fp32 accumulate
 //   in TMEM, issued by one thread) -> tcgen05.ld epilogue -> global.
 //
@@ -36,13 +36,14 @@ namespace gemm {
 constexpr int kBM = 128;
 constexpr int kBK = 64;  // one 128-byte swizzle atom of bf16 along K
 constexpr int kBNMax = 256;
-constexpr int kStages = 4;
+constexpr int kMaxStages = 8;
 constexpr int kAStage = kBM * kBK * 2;     // 16 KB
-constexpr int kBStage = kBNMax * kBK * 2;  // 32 KB
+constexpr int kBStage = kBNMax * kBK * 2;  // 32 KB (widest B stage)
+constexpr int kRingBytes = 4 * (kAStage + kBStage);  // 192 KB: 4..8 stages by BN
 constexpr int kThreads = 192;
 constexpr int kAccCols = 256;
 constexpr int kTmemCols = 2 * kAccCols;
-constexpr int kSmemBytes = kStages * (kAStage + kBStage) + 1024 + 256;
+constexpr int kSmemBytes = kRingBytes + 1024 + 256;
 constexpr int kMaxProblems = 2;
 constexpr int kSms = 148;
 
@@ -72,6 +73,8 @@ struct Launch {
   Problem p[kMaxProblems];
   int32_t n_problems;
   int32_t total_tiles;
+  int32_t stages;       // smem ring depth (narrow B tiles -> deeper ring)
+  int32_t stage_bytes;  // A (16 KB) + widest B of the problems, 1 KB aligned
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -266,11 +269,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + kStages * kAStage;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + kStages * kBStage);
-  uint64_t* empty = full + kStages;
-  uint64_t* tmem_full = empty + kStages;   // [2]
+  const int stages = L.stages;
+  const int stage_bytes = L.stage_bytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRingBytes);
+  uint64_t* empty = full + kMaxStages;
+  uint64_t* tmem_full = empty + kMaxStages;  // [2]
   uint64_t* tmem_empty = tmem_full + 2;    // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
 
@@ -281,7 +284,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   if (warp == 0 && lane == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -317,18 +320,20 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         const TileCoord tc = decode(L, t);
         const Problem& P = L.p[tc.prob];
         for (int kb = tc.kb0; kb < tc.kb1; ++kb, ++g) {
-          const int s = g % kStages;
-          const uint32_t ph = (g / kStages) & 1;
+          const int s = g % stages;
+          const uint32_t ph = (g / stages) & 1;
           mbar_wait(&empty[s], ph ^ 1);
           mbar_expect_tx(&full[s], P.tx_bytes);
           const int kc = kb * kBK;
-          tma_load_2d(&P.tmA, &full[s], sA + s * kAStage, kc, static_cast<int32_t>(tc.m0));
+          uint8_t* sA = smem + s * stage_bytes;
+          uint8_t* sB = sA + kAStage;
+          tma_load_2d(&P.tmA, &full[s], sA, kc, static_cast<int32_t>(tc.m0));
           if (!P.b_mn_major) {
-            tma_load_2d(&P.tmB, &full[s], sB + s * kBStage, kc, static_cast<int32_t>(tc.n0));
+            tma_load_2d(&P.tmB, &full[s], sB, kc, static_cast<int32_t>(tc.n0));
           } else {
             for (int j = 0; j < P.b_boxes; ++j)
-              tma_load_2d(&P.tmB, &full[s], sB + s * kBStage + j * 8192,
-                          static_cast<int32_t>(tc.n0 + 64 * j), kc);
+              tma_load_2d(&P.tmB, &full[s], sB + j * 8192, static_cast<int32_t>(tc.n0 + 64 * j),
+                          kc);
           }
         }
       }
@@ -344,12 +349,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         tc_fence_after();
         const uint32_t d_tmem = tmem + acc * kAccCols;
         for (int kb = tc.kb0; kb < tc.kb1; ++kb, ++g) {
-          const int s = g % kStages;
-          const uint32_t ph = (g / kStages) & 1;
+          const int s = g % stages;
+          const uint32_t ph = (g / stages) & 1;
           mbar_wait(&full[s], ph);
           tc_fence_after();
-          const uint32_t a_base = smem_u32(sA + s * kAStage);
-          const uint32_t b_base = smem_u32(sB + s * kBStage);
+          const uint32_t a_base = smem_u32(smem + s * stage_bytes);
+          const uint32_t b_base = a_base + kAStage;
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k) {
             const uint64_t ad = sdesc(a_base + k * 32, 16, 1024);
@@ -574,11 +579,17 @@ int dear_gemm_run_group(dear_gemm_plan* const* plans, int32_t n, void* stream) {
   Launch L;
   L.n_problems = n;
   L.total_tiles = 0;
+  int b_stage = 0;
   for (int i = 0; i < n; ++i) {
     if (!plans[i]) throw Error(DEAR_EINVAL, "dear_gemm_run_group: null plan");
     L.p[i] = plans[i]->p;
     L.total_tiles += plans[i]->p.tiles;
+    const Problem& P = plans[i]->p;
+    const int bs = P.b_mn_major ? P.b_boxes * 8192 : (P.bn * kBK * 2 + 1023) / 1024 * 1024;
+    b_stage = std::max(b_stage, bs);
   }
+  L.stage_bytes = kAStage + b_stage;
+  L.stages = std::min(kMaxStages, kRingBytes / L.stage_bytes);
   launch(L, static_cast<cudaStream_t>(stream));
   DEAR_API_END
 }

@@ -4,9 +4,10 @@
 //
 // All three are HBM-streaming kernels: pack and unpack move
 // 8 B/elem (+2 B/elem for the bf16 copy), update 12 B/shard-elem (20 with a
-// momentum buffer). Work is pre-cut on the host into Units of <= 8192
-// elements (one layer x chunk intersection each), one CTA per unit in a
-// grid-stride loop. Inside a unit the destination is peeled to 16 B alignment
+// momentum buffer). The host cuts every bucket op into Units (one layer x
+// chunk intersection each) and gives each of the kSlices CTAs (4 per SM, one
+// wave) an equal contiguous slice of the op's elements, which it walks across
+// units. Inside a unit the destination is peeled to 16 B alignment
 // and every access is a 128-bit vector; when the source is misaligned
 // relative to the destination (layer boundaries fall anywhere inside a
 // bucket), each lane loads its aligned float4 and takes the next lane's via
@@ -21,7 +22,6 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kUnroll = 4;
-constexpr int kMaxCtasPerSm = 8;
 constexpr int kSms = 148;
 
 __device__ __forceinline__ float4 shfl_down4(float4 v) {
@@ -59,7 +59,9 @@ __device__ __forceinline__ float4 ld4(const float4* p) {
 // Warp-cooperative walk over destination vectors q in [0, n4). The source
 // element for destination element 4q+e is src_floor[M + 4q + e]; src_floor is
 // 16 B aligned and vectors up to index qmax hold at least one valid element.
-// body(q, v) runs on every lane whose q < n4.
+// body(q, v) runs on every lane whose q < n4. All loads of one round (kUnroll
+// vectors per lane, plus the one vector past the round that lane 31 needs
+// when M != 0) are issued before any is consumed: no dependent second trip.
 template <int M, Hint H, typename Body>
 __device__ __forceinline__ void warp_stream(const float* src_floor, int64_t n4, int64_t qmax,
                                             Body&& body) {
@@ -67,26 +69,36 @@ __device__ __forceinline__ void warp_stream(const float* src_floor, int64_t n4, 
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   constexpr int kWarps = kThreads / 32;
+  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int64_t base = static_cast<int64_t>(warp) * 32 * kUnroll; base < n4;
        base += static_cast<int64_t>(kWarps) * 32 * kUnroll) {
-    float4 a[kUnroll], b[kUnroll];
+    float4 a[kUnroll];
 #pragma unroll
     for (int k = 0; k < kUnroll; ++k) {
       const int64_t q = base + k * 32 + lane;
-      a[k] = q <= qmax ? ld4<H>(s4 + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+      a[k] = q <= qmax ? ld4<H>(s4 + q) : zero;
     }
+    float4 extra = zero;
     if constexpr (M != 0) {
-#pragma unroll
-      for (int k = 0; k < kUnroll; ++k) {
-        b[k] = shfl_down4(a[k]);
-        const int64_t q = base + k * 32 + lane;
-        if (lane == 31 && q + 1 <= qmax) b[k] = ld4<H>(s4 + q + 1);
-      }
+      const int64_t qx = base + kUnroll * 32;
+      if (lane == 31 && qx <= qmax) extra = ld4<H>(s4 + qx);
     }
 #pragma unroll
     for (int k = 0; k < kUnroll; ++k) {
       const int64_t q = base + k * 32 + lane;
-      if (q < n4) body(q, realign<M>(a[k], M != 0 ? b[k] : a[k]));
+      float4 b = a[k];
+      if constexpr (M != 0) {
+        b = shfl_down4(a[k]);
+        float4 nxt = extra;
+        if (k + 1 < kUnroll) {
+          nxt.x = __shfl_sync(0xffffffffu, a[k + 1 < kUnroll ? k + 1 : k].x, 0);
+          nxt.y = __shfl_sync(0xffffffffu, a[k + 1 < kUnroll ? k + 1 : k].y, 0);
+          nxt.z = __shfl_sync(0xffffffffu, a[k + 1 < kUnroll ? k + 1 : k].z, 0);
+          nxt.w = __shfl_sync(0xffffffffu, a[k + 1 < kUnroll ? k + 1 : k].w, 0);
+        }
+        if (lane == 31) b = nxt;
+      }
+      if (q < n4) body(q, realign<M>(a[k], b));
     }
   }
 }
@@ -124,15 +136,31 @@ __device__ __forceinline__ void run_unit(const float* src, const float* dst, int
   for (int64_t i = head + n4 * 4 + threadIdx.x; i < len; i += kThreads) scalar_fn(i);
 }
 
-// ---------------------------------------------------------------- pack ----
-__global__ void __launch_bounds__(kThreads) pack_kernel(const Unit* __restrict__ units,
-                                                        int n_units, float scale) {
-  for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+// Every CTA walks its equal slice of the op's elements across units.
+template <typename F>
+__device__ __forceinline__ void walk_slice(const Unit* __restrict__ units,
+                                           const Slice* __restrict__ slices, F&& f) {
+  const Slice sl = slices[blockIdx.x];
+  int64_t left = sl.count;
+  int64_t off = sl.off;
+  for (int u = sl.unit; left > 0; ++u) {
     const Unit U = units[u];
-    const float* src = U.a;
-    float* dst = U.b;
+    const int64_t n = min(U.len - off, left);
+    if (n > 0) f(U, off, n);
+    left -= n;
+    off = 0;
+  }
+}
+
+// ---------------------------------------------------------------- pack ----
+__global__ void __launch_bounds__(kThreads, 4) pack_kernel(const Unit* __restrict__ units,
+                                                           const Slice* __restrict__ slices,
+                                                           float scale) {
+  walk_slice(units, slices, [&](const Unit& U, int64_t off, int64_t n) {
+    const float* src = U.a + off;
+    float* dst = U.b + off;
     run_unit<Hint::kStream>(
-        src, dst, U.len, [&](int64_t i) { dst[i] = __fmul_rn(src[i], scale); },
+        src, dst, n, [&](int64_t i) { dst[i] = __fmul_rn(src[i], scale); },
         [&](int64_t head, int64_t q, float4 v) {
           v.x = __fmul_rn(v.x, scale);
           v.y = __fmul_rn(v.y, scale);
@@ -140,7 +168,7 @@ __global__ void __launch_bounds__(kThreads) pack_kernel(const Unit* __restrict__
           v.w = __fmul_rn(v.w, scale);
           reinterpret_cast<float4*>(dst + head)[q] = v;
         });
-  }
+  });
 }
 
 // -------------------------------------------------------------- update ----
@@ -162,18 +190,17 @@ __device__ __forceinline__ float sgd_elem(float g, float w, float& m, const Hype
 }
 
 template <bool kMom, bool kWd>
-__global__ void __launch_bounds__(kThreads) update_kernel(const Unit* __restrict__ units,
-                                                          int n_units,
-                                                          const HyperParams* __restrict__ hpp,
-                                                          int has_buf) {
+__global__ void __launch_bounds__(kThreads, 4) update_kernel(const Unit* __restrict__ units,
+                                                             const Slice* __restrict__ slices,
+                                                             const HyperParams* __restrict__ hpp,
+                                                             int has_buf) {
   const HyperParams hp = *hpp;
-  for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-    const Unit U = units[u];
-    const float* w = U.a;
-    float* g = U.b;
-    float* mom = static_cast<float*>(U.c);
+  walk_slice(units, slices, [&](const Unit& U, int64_t off, int64_t n) {
+    const float* w = U.a + off;
+    float* g = U.b + off;
+    float* mom = kMom ? static_cast<float*>(U.c) + off : nullptr;
     run_unit<Hint::kKeep>(
-        w, g, U.len,
+        w, g, n,
         [&](int64_t i) {
           float m = kMom ? mom[i] : 0.f;
           g[i] = sgd_elem<kMom, kWd>(g[i], w[i], m, hp, has_buf);
@@ -181,38 +208,37 @@ __global__ void __launch_bounds__(kThreads) update_kernel(const Unit* __restrict
         },
         [&](int64_t head, int64_t q, float4 wv) {
           float4* g4 = reinterpret_cast<float4*>(g + head);
-          float4* m4 = reinterpret_cast<float4*>(mom + head);
           float4 gv = __ldcs(g4 + q);
-          float4 mv = kMom && has_buf ? m4[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+          float4 mv = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (kMom && has_buf) mv = reinterpret_cast<float4*>(mom + head)[q];
           gv.x = sgd_elem<kMom, kWd>(gv.x, wv.x, mv.x, hp, has_buf);
           gv.y = sgd_elem<kMom, kWd>(gv.y, wv.y, mv.y, hp, has_buf);
           gv.z = sgd_elem<kMom, kWd>(gv.z, wv.z, mv.z, hp, has_buf);
           gv.w = sgd_elem<kMom, kWd>(gv.w, wv.w, mv.w, hp, has_buf);
           g4[q] = gv;
-          if (kMom) m4[q] = mv;
+          if (kMom) reinterpret_cast<float4*>(mom + head)[q] = mv;
         });
-  }
+  });
 }
 
 // -------------------------------------------------------------- unpack ----
 template <bool kShadow>
-__global__ void __launch_bounds__(kThreads) unpack_kernel(const Unit* __restrict__ units,
-                                                          int n_units) {
-  for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-    const Unit U = units[u];
-    const float* src = U.a;
-    float* dst = U.b;
-    __nv_bfloat16* sh = static_cast<__nv_bfloat16*>(U.c);
+__global__ void __launch_bounds__(kThreads, 4) unpack_kernel(const Unit* __restrict__ units,
+                                                             const Slice* __restrict__ slices) {
+  walk_slice(units, slices, [&](const Unit& U, int64_t off, int64_t n) {
+    const float* src = U.a + off;
+    float* dst = U.b + off;
+    __nv_bfloat16* sh = (kShadow && U.c) ? static_cast<__nv_bfloat16*>(U.c) + off : nullptr;
     run_unit<Hint::kStream>(
-        src, dst, U.len,
+        src, dst, n,
         [&](int64_t i) {
           const float v = src[i];
           dst[i] = v;
-          if (kShadow) sh[i] = __float2bfloat16_rn(v);
+          if (kShadow && sh) sh[i] = __float2bfloat16_rn(v);
         },
         [&](int64_t head, int64_t q, float4 v) {
           reinterpret_cast<float4*>(dst + head)[q] = v;
-          if (kShadow) {
+          if (kShadow && sh) {
             __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y);
             __nv_bfloat162 hi = __floats2bfloat162_rn(v.z, v.w);
             uint2 packed;
@@ -221,7 +247,7 @@ __global__ void __launch_bounds__(kThreads) unpack_kernel(const Unit* __restrict
             reinterpret_cast<uint2*>(sh + head)[q] = packed;
           }
         });
-  }
+  });
 }
 
 // ---------------------------------------------------- local collectives ----
@@ -274,41 +300,57 @@ __global__ void hash_kernel(const float* __restrict__ x, int64_t n, uint64_t sal
   if ((threadIdx.x & 31) == 0) atomicAdd(acc, static_cast<unsigned long long>(h));
 }
 
-int grid_for(int n_units) {
-  const int cap = kSms * kMaxCtasPerSm;
-  return n_units < cap ? n_units : cap;
-}
-
 }  // namespace
 
-cudaError_t launch_pack(const Unit* units, int n_units, float scale, cudaStream_t s) {
-  if (n_units <= 0) return cudaSuccess;
-  pack_kernel<<<grid_for(n_units), kThreads, 0, s>>>(units, n_units, scale);
+cudaError_t launch_pack(const Unit* units, const Slice* slices, int64_t total, float scale,
+                        cudaStream_t s) {
+  if (total <= 0) return cudaSuccess;
+  pack_kernel<<<kSlices, kThreads, 0, s>>>(units, slices, scale);
   return cudaGetLastError();
 }
 
-cudaError_t launch_update(const Unit* units, int n_units, const HyperParams* hp,
-                          int has_momentum_buf, int use_momentum, int use_wd, cudaStream_t s) {
-  if (n_units <= 0) return cudaSuccess;
-  const int g = grid_for(n_units);
+cudaError_t launch_update(const Unit* units, const Slice* slices, int64_t total,
+                          const HyperParams* hp, int has_momentum_buf, int use_momentum,
+                          int use_wd, cudaStream_t s) {
+  if (total <= 0) return cudaSuccess;
   if (use_momentum && use_wd)
-    update_kernel<true, true><<<g, kThreads, 0, s>>>(units, n_units, hp, has_momentum_buf);
+    update_kernel<true, true><<<kSlices, kThreads, 0, s>>>(units, slices, hp, has_momentum_buf);
   else if (use_momentum)
-    update_kernel<true, false><<<g, kThreads, 0, s>>>(units, n_units, hp, has_momentum_buf);
+    update_kernel<true, false><<<kSlices, kThreads, 0, s>>>(units, slices, hp, has_momentum_buf);
   else if (use_wd)
-    update_kernel<false, true><<<g, kThreads, 0, s>>>(units, n_units, hp, has_momentum_buf);
+    update_kernel<false, true><<<kSlices, kThreads, 0, s>>>(units, slices, hp, has_momentum_buf);
   else
-    update_kernel<false, false><<<g, kThreads, 0, s>>>(units, n_units, hp, has_momentum_buf);
+    update_kernel<false, false><<<kSlices, kThreads, 0, s>>>(units, slices, hp, has_momentum_buf);
   return cudaGetLastError();
 }
 
-cudaError_t launch_unpack(const Unit* units, int n_units, int with_shadow, cudaStream_t s) {
-  if (n_units <= 0) return cudaSuccess;
+cudaError_t launch_unpack(const Unit* units, const Slice* slices, int64_t total, int with_shadow,
+                          cudaStream_t s) {
+  if (total <= 0) return cudaSuccess;
   if (with_shadow)
-    unpack_kernel<true><<<grid_for(n_units), kThreads, 0, s>>>(units, n_units);
+    unpack_kernel<true><<<kSlices, kThreads, 0, s>>>(units, slices);
   else
-    unpack_kernel<false><<<grid_for(n_units), kThreads, 0, s>>>(units, n_units);
+    unpack_kernel<false><<<kSlices, kThreads, 0, s>>>(units, slices);
   return cudaGetLastError();
+}
+
+void make_slices(const Unit* units, int n_units, int64_t total, Slice* out) {
+  int64_t per = (total + kSlices - 1) / kSlices;
+  per = (per + 3) / 4 * 4;
+  int u = 0;
+  int64_t base = 0;  // start of unit u
+  for (int c = 0; c < kSlices; ++c) {
+    const int64_t lo = static_cast<int64_t>(c) * per;
+    const int64_t cnt = lo >= total ? 0 : (total - lo < per ? total - lo : per);
+    while (u < n_units && base + units[u].len <= lo && cnt > 0) {
+      base += units[u].len;
+      ++u;
+    }
+    out[c].unit = cnt > 0 ? u : 0;
+    out[c].pad = 0;
+    out[c].off = cnt > 0 ? lo - base : 0;
+    out[c].count = cnt;
+  }
 }
 
 cudaError_t launch_local_reduce_scatter(float* const* bufs_dev, int P, int64_t stride,

@@ -96,6 +96,8 @@ struct Bucket {
   std::vector<cudaEvent_t> ready_events;
   Unit *pack_u = nullptr, *upd_u = nullptr, *unpack_u = nullptr;
   int n_pack = 0, n_upd = 0, n_unpack = 0;
+  int64_t e_pack = 0, e_upd = 0, e_unpack = 0;  // elements per op
+  Slice *pack_s = nullptr, *upd_s = nullptr, *unpack_s = nullptr;  // kSlices each
   bool any_shadow = false;
   bool mom_init = false;
   cudaEvent_t ag_done = nullptr;
@@ -200,6 +202,16 @@ void for_each_piece(const dear_ctx& ctx, const Bucket& B, int64_t cb, int64_t ce
       emit(l, p - lb, len, p - cb);
     }
   }
+}
+
+// Prefix offsets of the units from `first` to the end; returns the total.
+int64_t set_starts(std::vector<Unit>& u, size_t first) {
+  int64_t at = 0;
+  for (size_t i = first; i < u.size(); ++i) {
+    u[i].start = at;
+    at += u[i].len;
+  }
+  return at;
 }
 
 }  // namespace
@@ -341,7 +353,7 @@ void dear_ctx::exec(const Op& op) {
       break;
     case OP_PACK:
       record_t(op.bucket, T_PACK0);
-      cuda_check(launch_pack(B->pack_u, B->n_pack, pack_scale, comm_stream), "pack kernel");
+      cuda_check(launch_pack(B->pack_u, B->pack_s, B->e_pack, pack_scale, comm_stream), "pack kernel");
       cuda_check(cudaEventRecord(packed_ev, comm_stream), "cudaEventRecord");
       record_t(op.bucket, T_PACK1);
       break;
@@ -355,7 +367,7 @@ void dear_ctx::exec(const Op& op) {
       record_t(op.bucket, T_RS1);
       break;
     case OP_UPDATE:
-      cuda_check(launch_update(B->upd_u, B->n_upd, hp_dev, B->mom_init ? 1 : 0,
+      cuda_check(launch_update(B->upd_u, B->upd_s, B->e_upd, hp_dev, B->mom_init ? 1 : 0,
                                cfg.momentum != 0.0, cfg.weight_decay != 0.0, comm_stream),
                  "update kernel");
       if (cfg.momentum != 0.0) B->mom_init = true;
@@ -371,7 +383,8 @@ void dear_ctx::exec(const Op& op) {
       record_t(op.bucket, T_AG1);
       break;
     case OP_UNPACK:
-      cuda_check(launch_unpack(B->unpack_u, B->n_unpack, B->any_shadow ? 1 : 0, comm_stream),
+      cuda_check(launch_unpack(B->unpack_u, B->unpack_s, B->e_unpack, B->any_shadow ? 1 : 0,
+                               comm_stream),
                  "unpack kernel");
       record_t(op.bucket, T_UNPACK1);
       break;
@@ -670,13 +683,18 @@ int dear_finalize(dear_ctx* ctx) {
   }
   const size_t float_bytes = (floats * sizeof(float) + 255) / 256 * 256;
   const size_t unit_bytes = (units * sizeof(Unit) + 255) / 256 * 256;
-  const size_t total = float_bytes + unit_bytes + 256 + 256;
+  const size_t n_slices = plan.size() * 3 * static_cast<size_t>(kSlices);
+  const size_t slice_bytes = (n_slices * sizeof(Slice) + 255) / 256 * 256;
+  const size_t total = float_bytes + unit_bytes + slice_bytes + 256 + 256;
   cuda_check(cudaMalloc(&c.arena, total), "cudaMalloc(bucket arena)");
   cuda_check(cudaMemset(c.arena, 0, float_bytes), "cudaMemset");
   float* fp = reinterpret_cast<float*>(c.arena);
   Unit* up = reinterpret_cast<Unit*>(c.arena + float_bytes);
-  c.hp_dev = reinterpret_cast<HyperParams*>(c.arena + float_bytes + unit_bytes);
-  c.hash_dev = reinterpret_cast<unsigned long long*>(c.arena + float_bytes + unit_bytes + 256);
+  Slice* sp = reinterpret_cast<Slice*>(c.arena + float_bytes + unit_bytes);
+  c.hp_dev = reinterpret_cast<HyperParams*>(c.arena + float_bytes + unit_bytes + slice_bytes);
+  c.hash_dev = reinterpret_cast<unsigned long long*>(c.arena + float_bytes + unit_bytes +
+                                                      slice_bytes + 256);
+  std::vector<Slice> host_slices(n_slices);
   for (size_t g = 0; g < plan.size(); ++g) {
     Bucket& B = c.buckets[g];
     B.buf = fp;
@@ -697,10 +715,11 @@ int dear_finalize(dear_ctx* ctx) {
       for_each_piece(c, B, bg[static_cast<size_t>(ch)], bg[static_cast<size_t>(ch) + 1],
                      [&](int l, int64_t j, int64_t len, int64_t pos) {
                        const LayerReg& R = c.layers[static_cast<size_t>(l - 1)];
-                       host_units.push_back({R.grad + j, B.buf + slot * B.stride + pos, nullptr, len});
+                       host_units.push_back({R.grad + j, B.buf + slot * B.stride + pos, nullptr, len, 0});
                      });
     }
     B.n_pack = static_cast<int>(host_units.size() - static_cast<size_t>(B.pack_u - up));
+    B.e_pack = set_starts(host_units, static_cast<size_t>(B.pack_u - up));
     // update: own chunk (rank+1) mod P, in slot `rank`.
     B.upd_u = up + host_units.size();
     const int own = (c.rank + 1) % c.P;
@@ -708,9 +727,10 @@ int dear_finalize(dear_ctx* ctx) {
                    [&](int l, int64_t j, int64_t len, int64_t pos) {
                      const LayerReg& R = c.layers[static_cast<size_t>(l - 1)];
                      host_units.push_back({R.param + j, B.buf + c.rank * B.stride + pos,
-                                           B.mom ? static_cast<void*>(B.mom + pos) : nullptr, len});
+                                           B.mom ? static_cast<void*>(B.mom + pos) : nullptr, len, 0});
                    });
     B.n_upd = static_cast<int>(host_units.size() - static_cast<size_t>(B.upd_u - up));
+    B.e_upd = set_starts(host_units, static_cast<size_t>(B.upd_u - up));
     // unpack: every slot back to the layers (and their bf16 copies).
     B.unpack_u = up + host_units.size();
     for (int ch = 0; ch < c.P; ++ch) {
@@ -719,10 +739,19 @@ int dear_finalize(dear_ctx* ctx) {
                      [&](int l, int64_t j, int64_t len, int64_t pos) {
                        const LayerReg& R = c.layers[static_cast<size_t>(l - 1)];
                        void* sh = R.shadow ? static_cast<void*>(static_cast<uint16_t*>(R.shadow) + j) : nullptr;
-                       host_units.push_back({B.buf + slot * B.stride + pos, R.param + j, sh, len});
+                       host_units.push_back({B.buf + slot * B.stride + pos, R.param + j, sh, len, 0});
                      });
     }
     B.n_unpack = static_cast<int>(host_units.size() - static_cast<size_t>(B.unpack_u - up));
+    B.e_unpack = set_starts(host_units, static_cast<size_t>(B.unpack_u - up));
+    // Equal element slices per CTA for each op (one wave of kSlices CTAs).
+    Slice* hs = host_slices.data() + g * 3 * kSlices;
+    make_slices(host_units.data() + (B.pack_u - up), B.n_pack, B.e_pack, hs);
+    make_slices(host_units.data() + (B.upd_u - up), B.n_upd, B.e_upd, hs + kSlices);
+    make_slices(host_units.data() + (B.unpack_u - up), B.n_unpack, B.e_unpack, hs + 2 * kSlices);
+    B.pack_s = sp + g * 3 * kSlices;
+    B.upd_s = B.pack_s + kSlices;
+    B.unpack_s = B.upd_s + kSlices;
     B.ag_done = new_event(false);
     for (int k = 0; k < T_COUNT; ++k) B.t[k] = new_event(true);
     B.layers_left = B.high - B.low + 1;
@@ -731,6 +760,8 @@ int dear_finalize(dear_ctx* ctx) {
     cuda_check(cudaMemcpy(up, host_units.data(), host_units.size() * sizeof(Unit), cudaMemcpyHostToDevice),
                "cudaMemcpy(units)");
   }
+  cuda_check(cudaMemcpy(sp, host_slices.data(), n_slices * sizeof(Slice), cudaMemcpyHostToDevice),
+             "cudaMemcpy(slices)");
   // Hyper-parameters; 1/P folded into pack when it is exact (P = 2^k).
   const bool pow2 = (c.P & (c.P - 1)) == 0;
   c.pack_scale = pow2 ? 1.0f / static_cast<float>(c.P) : 1.0f;

@@ -1,0 +1,64 @@
+"""The product's prediction layer (paper_2302_12445_b200.costmodel) against the
+reference build: alpha-beta costs, calibration, Eq. 6-8, and the simulated
+DeAR / WFBP iteration times of the golden scenarios."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from paper_2302_12445_b200 import costmodel as cm
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def test_costs_match_reference(reference):
+    rng = np.random.default_rng(5)
+    for _ in range(200):
+        d, P = float(rng.uniform(0, 1e9)), int(rng.integers(1, 65))
+        a, b = float(rng.uniform(0, 1e-4)), float(rng.uniform(0, 2e-9))
+        rs, ar = reference.costs(d, P, a, b)
+        assert cm.reduce_scatter_time(d, P, a, b) == rs
+        assert cm.all_reduce_time(d, P, a, b) == ar
+        assert cm.reduce_scatter_time(d, P, a, b) + cm.all_gather_time(d, P, a, b) == ar
+
+
+def test_calibration_matches_reference(reference):
+    # the paper's two points (test_cost_model.cpp:33-34)
+    pts = [(1e6, 4.5e-3), (5e5, 3.9e-3)]
+    got, ref = cm.calibrate_alpha_beta(pts, 64), reference.calibrate(pts, 64)
+    assert got["alpha"] == pytest.approx(ref["alpha"], rel=1e-9)
+    assert got["beta"] == pytest.approx(ref["beta"], rel=1e-9)
+    assert got["alpha"] == pytest.approx(2.6190476e-5, rel=1e-6)
+    rng = np.random.default_rng(9)
+    for _ in range(50):
+        P = int(rng.integers(2, 9))
+        a, b = float(rng.uniform(1e-6, 1e-4)), float(rng.uniform(1e-12, 1e-9))
+        sizes = np.exp(rng.uniform(np.log(6.4e4), np.log(2.6e8), 8))
+        pts = [(s, cm.all_reduce_time(s, P, a, b) * float(rng.uniform(0.95, 1.05))) for s in sizes]
+        got, ref = cm.calibrate_alpha_beta(pts, P), reference.calibrate(pts, P)
+        assert got["alpha"] == pytest.approx(ref["alpha"], rel=1e-6, abs=1e-15)
+        assert got["beta"] == pytest.approx(ref["beta"], rel=1e-6, abs=1e-21)
+    with pytest.raises(ValueError):
+        cm.calibrate_alpha_beta([(1e6, 1e-3), (1e6, 2e-3)], 4)
+
+
+def test_theory_matches_reference(reference):
+    rng = np.random.default_rng(3)
+    for _ in range(100):
+        v = [float(x) for x in rng.uniform(0, 1e-2, 4)]
+        P = int(rng.integers(1, 65))
+        ref = reference.theory(*v, P)
+        t = cm.theoretical_times(*v)
+        assert t["dear"] == ref["dear"] and t["baseline"] == ref["baseline"]
+        assert cm.max_speedup(*v, P) == pytest.approx(ref["smax"], rel=1e-15)
+
+
+def test_predicted_iterations_match_reference_simulator():
+    with open(os.path.join(GOLD, "schedules.json")) as f:
+        scen = json.load(f)["scenarios"]
+    for s in scen:
+        got = cm.predict_iteration([4 * c for c in s["counts"]], s["t_ff"], s["t_bp"],
+                                   s["policy"], s["buffer"], s["P"], s["alpha"], s["beta"])
+        assert got["iteration_seconds"] == pytest.approx(s["result"]["iteration_seconds"],
+                                                         rel=1e-12), s["name"]
