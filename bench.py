@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--lr", type=float, default=0.05)
     ap.add_argument("--momentum", type=float, default=0.0)
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "peer"],
+                    help="bucket collectives: NCCL RS/AG, or fused NVLink peer kernels")
     ap.add_argument("--no-ablation", action="store_true", help="skip WFBP / compute-only runs")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -278,7 +280,7 @@ def gpu_arm(a, wl, world, rank, local_rank):
     def runtime(policy):
         rt = dear.Runtime(comm, rank, world, policy=policy, fusion_buffer_bytes=a.buffer,
                           lr=a.lr, momentum=a.momentum, defer_allgather=use_graph,
-                          stream=stream)
+                          backend=a.backend, stream=stream)
         for l in range(1, model.L + 1):
             rt.register(l, model.params[l - 1], model.grads[l - 1], model.shadows[l - 1])
         rt.finalize()
@@ -369,7 +371,7 @@ def gpu_arm(a, wl, world, rank, local_rank):
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": res["dear_ms"],
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic",
-        "config": {"workload": wl["config"], "policy": a.policy,
+        "config": {"workload": wl["config"], "policy": a.policy, "collectives": a.backend,
                    "fusion_buffer_bytes": a.buffer, "buckets": len(buckets),
                    "batch_per_gpu": batch, "global_batch": samples, "tokens_per_gpu": tokens,
                    "hidden": wl["hidden"], "params": D, "cuda_graph": use_graph,

@@ -153,6 +153,23 @@ int dear_destroy(dear_ctx* ctx);
 int dear_set_lr(dear_ctx* ctx, double lr);
 
 /* ---------------------------------------------------------------------------
+ * NVLink peer backend (one process per GPU, after dear_finalize on every rank).
+ * Each rank exports an IPC handle of its bucket arena; once every rank has
+ * connected to all handles, each bucket's reduce-scatter runs as ONE kernel
+ * that reads every rank's slot over NVLink, sums in the reference's ring
+ * order (collective.cpp:70-90, bit-exact with the fp32 restatement) and
+ * applies the SGD update; the all-gather runs as ONE kernel that reads each
+ * owner's updated slot over NVLink straight into the parameters (+ bf16 copy).
+ * Cross-GPU ordering uses per-bucket completion counters in each arena
+ * (graph-safe). The NCCL communicator is still used for dear_finalize's and
+ * dear_check_replicas' cross-rank checks.
+ * ------------------------------------------------------------------------ */
+#define DEAR_PEER_HANDLE_BYTES 128
+int dear_peer_handle(dear_ctx* ctx, uint8_t out[DEAR_PEER_HANDLE_BYTES]);
+/* handles: n = P records of DEAR_PEER_HANDLE_BYTES, in rank order. */
+int dear_peer_connect(dear_ctx* ctx, const uint8_t* handles, int32_t n);
+
+/* ---------------------------------------------------------------------------
  * Introspection, timing and checks.
  * ------------------------------------------------------------------------ */
 int dear_num_buckets(dear_ctx* ctx, int32_t* n);

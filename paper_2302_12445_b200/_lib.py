@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libdear.so")
+# DEAR_LIB selects an alternative in-tree build (kernel-variant experiments).
+LIB_PATH = os.path.join(PKG, os.environ.get("DEAR_LIB", "libdear.so"))
 
 DEAR_OK, DEAR_EINVAL, DEAR_EINTERNAL = 0, 1, 2
 POLICIES = {"WFBP": 0, "WFBP_FUSED": 1, "DEAR": 3, "DEAR_FUSED": 4}
@@ -71,6 +72,8 @@ _SIGNATURES = {
     "dear_set_timing": [_P, C.c_int32],
     "dear_get_timings": [_P, C.POINTER(C.c_float), C.c_int32],
     "dear_check_replicas": [_P, C.POINTER(C.c_int32)],
+    "dear_peer_handle": [_P, C.c_char_p],
+    "dear_peer_connect": [_P, C.c_char_p, C.c_int32],
 }
 
 _lib = None

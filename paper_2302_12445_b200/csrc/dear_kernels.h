@@ -21,6 +21,8 @@ struct Unit {
   void* c;
   int64_t len;
   int64_t start;  // prefix sum of len over the op's unit list
+  int32_t peer;   // unpack units: rank whose slot `a` points into (peer backend)
+  int32_t pad;
 };
 
 // Units are cut at this length only to bound the per-unit index arithmetic;
@@ -73,6 +75,47 @@ cudaError_t launch_local_reduce_scatter(float* const* bufs_dev, int P, int64_t s
                                         int64_t count, cudaStream_t s);
 cudaError_t launch_local_all_gather(float* const* bufs_dev, int P, int64_t stride,
                                     int64_t count, cudaStream_t s);
+
+// ---- Peer (NVLink P2P) backend -------------------------------------------
+// Every rank's arena is IPC-mapped by every other rank; the same object lives
+// at address p + delta[k] in rank k's arena. Per bucket, each rank keeps three
+// monotonically increasing completion counters in its arena (packs, updates,
+// gathers done); ordering across GPUs is "wait until every peer's counter
+// reaches mine", so no host-side epoch is baked into CUDA graphs.
+constexpr int kMaxPeers = 16;
+struct PeerArgs {
+  int64_t delta[kMaxPeers];  // peer arena base - own arena base (bytes)
+  int32_t P;
+  int32_t rank;
+};
+struct BucketFlags {
+  uint32_t packed;
+  uint32_t updated;
+  uint32_t gathered;
+  uint32_t pad;
+  uint32_t done[4];  // per-op CTA completion counters (last CTA signals)
+};
+
+// One-warp kernel: waits until, for every peer k, the counter at
+// watch + delta[k] >= *mine (acquire, system scope).
+cudaError_t launch_wait_peers(const uint32_t* mine, const uint32_t* watch, const PeerArgs& pa,
+                              cudaStream_t s);
+// pack with a completion signal (flags->packed += 1 after all CTAs finish).
+cudaError_t launch_pack_signal(const Unit* units, const Slice* slices, int64_t total, float scale,
+                               BucketFlags* flags, cudaStream_t s);
+// Fused reduce-scatter + shard SGD update: for each own-shard element, sum the
+// peers' slot-`rank` values in ring order (rank+1, ..., rank), update, write
+// w' into the own slot; then flags->updated += 1.
+cudaError_t launch_rs_update_peer(const Unit* units, const Slice* slices, int64_t total,
+                                  const HyperParams* hp, int has_momentum_buf, int use_momentum,
+                                  int use_wd, const PeerArgs& pa, BucketFlags* flags,
+                                  cudaStream_t s);
+// Fused all-gather + unpack: every element read from its owner's slot (remote
+// over NVLink unless owned), written to the params (+ bf16 copy); then
+// flags->gathered += 1.
+cudaError_t launch_ag_unpack_peer(const Unit* units, const Slice* slices, int64_t total,
+                                  int with_shadow, const PeerArgs& pa, BucketFlags* flags,
+                                  cudaStream_t s);
 
 // Order-independent 64-bit hash of float bit patterns (sum of mixed words),
 // accumulated into *acc with atomics. Used by dear_check_replicas.

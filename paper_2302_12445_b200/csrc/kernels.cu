@@ -22,6 +22,7 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kUnroll = 4;
+constexpr int kCtasPerSm = kSlices / 148;
 constexpr int kSms = 148;
 
 __device__ __forceinline__ float4 shfl_down4(float4 v) {
@@ -152,10 +153,52 @@ __device__ __forceinline__ void walk_slice(const Unit* __restrict__ units,
   }
 }
 
+// ------------------------------------------------------ peer signalling ----
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <typename T>
+__device__ __forceinline__ const T* at_peer(const T* p, int64_t delta) {
+  return reinterpret_cast<const T*>(reinterpret_cast<const char*>(p) + delta);
+}
+
+// Last CTA of the launch bumps `counter` (release, system scope) once every
+// CTA's writes are globally visible.
+__device__ __forceinline__ void signal_done(uint32_t* done, uint32_t* counter) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    const uint32_t prev = atomicAdd(done, 1u);
+    if (prev == gridDim.x - 1) {
+      *done = 0;
+      __threadfence_system();
+      atomicAdd_system(counter, 1u);
+    }
+  }
+}
+
+__global__ void wait_peers_kernel(const uint32_t* mine, const uint32_t* watch, PeerArgs pa) {
+  const uint32_t target = ld_acquire_sys(mine);
+  const int k = threadIdx.x;
+  if (k < pa.P && k != pa.rank) {
+    const uint32_t* f = at_peer(watch, pa.delta[k]);
+    const long long t0 = clock64();
+    while (static_cast<int32_t>(ld_acquire_sys(f) - target) < 0) {
+      __nanosleep(256);
+      // A peer that never arrives must fail loudly, not hang the GPU.
+      if (clock64() - t0 > 60ll * 2000000000ll) __trap();
+    }
+  }
+}
+
 // ---------------------------------------------------------------- pack ----
-__global__ void __launch_bounds__(kThreads, 4) pack_kernel(const Unit* __restrict__ units,
+template <bool kSignal>
+__global__ void __launch_bounds__(kThreads, kCtasPerSm) pack_kernel(const Unit* __restrict__ units,
                                                            const Slice* __restrict__ slices,
-                                                           float scale) {
+                                                           float scale, BucketFlags* flags) {
   walk_slice(units, slices, [&](const Unit& U, int64_t off, int64_t n) {
     const float* src = U.a + off;
     float* dst = U.b + off;
@@ -169,6 +212,7 @@ __global__ void __launch_bounds__(kThreads, 4) pack_kernel(const Unit* __restric
           reinterpret_cast<float4*>(dst + head)[q] = v;
         });
   });
+  if (kSignal) signal_done(&flags->done[0], &flags->packed);
 }
 
 // -------------------------------------------------------------- update ----
@@ -190,7 +234,7 @@ __device__ __forceinline__ float sgd_elem(float g, float w, float& m, const Hype
 }
 
 template <bool kMom, bool kWd>
-__global__ void __launch_bounds__(kThreads, 4) update_kernel(const Unit* __restrict__ units,
+__global__ void __launch_bounds__(kThreads, kCtasPerSm) update_kernel(const Unit* __restrict__ units,
                                                              const Slice* __restrict__ slices,
                                                              const HyperParams* __restrict__ hpp,
                                                              int has_buf) {
@@ -223,7 +267,7 @@ __global__ void __launch_bounds__(kThreads, 4) update_kernel(const Unit* __restr
 
 // -------------------------------------------------------------- unpack ----
 template <bool kShadow>
-__global__ void __launch_bounds__(kThreads, 4) unpack_kernel(const Unit* __restrict__ units,
+__global__ void __launch_bounds__(kThreads, kCtasPerSm) unpack_kernel(const Unit* __restrict__ units,
                                                              const Slice* __restrict__ slices) {
   walk_slice(units, slices, [&](const Unit& U, int64_t off, int64_t n) {
     const float* src = U.a + off;
@@ -248,6 +292,93 @@ __global__ void __launch_bounds__(kThreads, 4) unpack_kernel(const Unit* __restr
           }
         });
   });
+}
+
+// ------------------------------------------- fused peer RS+update --------
+// Ring-order sum (collective.cpp:70-90): chunk (rank+1)%P starts on rank
+// rank+1 and picks up rank+2, ..., rank — the same fold as the local-group
+// kernel, so the result is bit-exact with the fp32 restatement.
+template <bool kMom, bool kWd>
+__global__ void __launch_bounds__(kThreads, kCtasPerSm)
+    rs_update_peer_kernel(const Unit* __restrict__ units, const Slice* __restrict__ slices,
+                          const HyperParams* __restrict__ hpp, int has_buf, PeerArgs pa,
+                          BucketFlags* flags) {
+  const HyperParams hp = *hpp;
+  const int k0 = (pa.rank + 1) % pa.P;
+  walk_slice(units, slices, [&](const Unit& U, int64_t off, int64_t n) {
+    const float* w = U.a + off;
+    float* g = U.b + off;
+    float* mom = kMom ? static_cast<float*>(U.c) + off : nullptr;
+    auto sum1 = [&](const float* p) {
+      int k = k0;
+      float acc = __ldcg(at_peer(p, pa.delta[k]));
+      for (int j = 1; j < pa.P; ++j) {
+        k = k + 1 == pa.P ? 0 : k + 1;
+        acc = __fadd_rn(acc, __ldcg(at_peer(p, pa.delta[k])));
+      }
+      return acc;
+    };
+    run_unit<Hint::kKeep>(
+        w, g, n,
+        [&](int64_t i) {
+          float m = kMom ? mom[i] : 0.f;
+          g[i] = sgd_elem<kMom, kWd>(sum1(g + i), w[i], m, hp, has_buf);
+          if (kMom) mom[i] = m;
+        },
+        [&](int64_t head, int64_t q, float4 wv) {
+          const float4* g4 = reinterpret_cast<const float4*>(g + head) + q;
+          int k = k0;
+          float4 acc = __ldcg(at_peer(g4, pa.delta[k]));
+          for (int j = 1; j < pa.P; ++j) {
+            k = k + 1 == pa.P ? 0 : k + 1;
+            const float4 v = __ldcg(at_peer(g4, pa.delta[k]));
+            acc.x = __fadd_rn(acc.x, v.x);
+            acc.y = __fadd_rn(acc.y, v.y);
+            acc.z = __fadd_rn(acc.z, v.z);
+            acc.w = __fadd_rn(acc.w, v.w);
+          }
+          float4 mv = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (kMom && has_buf) mv = reinterpret_cast<float4*>(mom + head)[q];
+          acc.x = sgd_elem<kMom, kWd>(acc.x, wv.x, mv.x, hp, has_buf);
+          acc.y = sgd_elem<kMom, kWd>(acc.y, wv.y, mv.y, hp, has_buf);
+          acc.z = sgd_elem<kMom, kWd>(acc.z, wv.z, mv.z, hp, has_buf);
+          acc.w = sgd_elem<kMom, kWd>(acc.w, wv.w, mv.w, hp, has_buf);
+          reinterpret_cast<float4*>(g + head)[q] = acc;
+          if (kMom) reinterpret_cast<float4*>(mom + head)[q] = mv;
+        });
+  });
+  signal_done(&flags->done[1], &flags->updated);
+}
+
+// ------------------------------------------- fused peer AG+unpack ---------
+template <bool kShadow>
+__global__ void __launch_bounds__(kThreads, kCtasPerSm)
+    ag_unpack_peer_kernel(const Unit* __restrict__ units, const Slice* __restrict__ slices,
+                          PeerArgs pa, BucketFlags* flags) {
+  walk_slice(units, slices, [&](const Unit& U, int64_t off, int64_t n) {
+    const float* src = at_peer(U.a + off, pa.delta[U.peer]);
+    float* dst = U.b + off;
+    __nv_bfloat16* sh = (kShadow && U.c) ? static_cast<__nv_bfloat16*>(U.c) + off : nullptr;
+    run_unit<Hint::kStream>(
+        src, dst, n,
+        [&](int64_t i) {
+          const float v = src[i];
+          dst[i] = v;
+          if (kShadow && sh) sh[i] = __float2bfloat16_rn(v);
+        },
+        [&](int64_t head, int64_t q, float4 v) {
+          reinterpret_cast<float4*>(dst + head)[q] = v;
+          if (kShadow && sh) {
+            __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y);
+            __nv_bfloat162 hi = __floats2bfloat162_rn(v.z, v.w);
+            uint2 packed;
+            packed.x = *reinterpret_cast<uint32_t*>(&lo);
+            packed.y = *reinterpret_cast<uint32_t*>(&hi);
+            reinterpret_cast<uint2*>(sh + head)[q] = packed;
+          }
+        });
+  });
+  signal_done(&flags->done[2], &flags->gathered);
 }
 
 // ---------------------------------------------------- local collectives ----
@@ -305,7 +436,47 @@ __global__ void hash_kernel(const float* __restrict__ x, int64_t n, uint64_t sal
 cudaError_t launch_pack(const Unit* units, const Slice* slices, int64_t total, float scale,
                         cudaStream_t s) {
   if (total <= 0) return cudaSuccess;
-  pack_kernel<<<kSlices, kThreads, 0, s>>>(units, slices, scale);
+  pack_kernel<false><<<kSlices, kThreads, 0, s>>>(units, slices, scale, nullptr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_signal(const Unit* units, const Slice* slices, int64_t total, float scale,
+                               BucketFlags* flags, cudaStream_t s) {
+  (void)total;  // the signal must fire even for an empty bucket
+  pack_kernel<true><<<kSlices, kThreads, 0, s>>>(units, slices, scale, flags);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_wait_peers(const uint32_t* mine, const uint32_t* watch, const PeerArgs& pa,
+                              cudaStream_t s) {
+  wait_peers_kernel<<<1, 32, 0, s>>>(mine, watch, pa);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rs_update_peer(const Unit* units, const Slice* slices, int64_t total,
+                                  const HyperParams* hp, int has_momentum_buf, int use_momentum,
+                                  int use_wd, const PeerArgs& pa, BucketFlags* flags,
+                                  cudaStream_t s) {
+  (void)total;
+  if (use_momentum && use_wd)
+    rs_update_peer_kernel<true, true><<<kSlices, kThreads, 0, s>>>(units, slices, hp, has_momentum_buf, pa, flags);
+  else if (use_momentum)
+    rs_update_peer_kernel<true, false><<<kSlices, kThreads, 0, s>>>(units, slices, hp, has_momentum_buf, pa, flags);
+  else if (use_wd)
+    rs_update_peer_kernel<false, true><<<kSlices, kThreads, 0, s>>>(units, slices, hp, has_momentum_buf, pa, flags);
+  else
+    rs_update_peer_kernel<false, false><<<kSlices, kThreads, 0, s>>>(units, slices, hp, has_momentum_buf, pa, flags);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ag_unpack_peer(const Unit* units, const Slice* slices, int64_t total,
+                                  int with_shadow, const PeerArgs& pa, BucketFlags* flags,
+                                  cudaStream_t s) {
+  (void)total;
+  if (with_shadow)
+    ag_unpack_peer_kernel<true><<<kSlices, kThreads, 0, s>>>(units, slices, pa, flags);
+  else
+    ag_unpack_peer_kernel<false><<<kSlices, kThreads, 0, s>>>(units, slices, pa, flags);
   return cudaGetLastError();
 }
 

@@ -98,6 +98,7 @@ struct Bucket {
   int n_pack = 0, n_upd = 0, n_unpack = 0;
   int64_t e_pack = 0, e_upd = 0, e_unpack = 0;  // elements per op
   Slice *pack_s = nullptr, *upd_s = nullptr, *unpack_s = nullptr;  // kSlices each
+  BucketFlags* flags = nullptr;  // peer backend completion counters (in the arena)
   bool any_shadow = false;
   bool mom_init = false;
   cudaEvent_t ag_done = nullptr;
@@ -150,6 +151,10 @@ struct dear_ctx {
   cudaEvent_t step_ev = nullptr;
   cudaEvent_t join_ev = nullptr;
   unsigned long long* hash_dev = nullptr;
+  size_t arena_bytes = 0;
+  bool peer = false;             // NVLink peer backend (fused RS+update, AG+unpack)
+  PeerArgs pa{};
+  std::vector<void*> peer_maps;  // cudaIpcOpenMemHandle mappings to close
   bool timing = false;
   std::vector<std::string> trace;
   std::deque<Op> queue;  // local mode: ops not yet executed
@@ -316,6 +321,7 @@ dear_ctx::~dear_ctx() {
   if (packed_ev) cudaEventDestroy(packed_ev);
   if (step_ev) cudaEventDestroy(step_ev);
   if (join_ev) cudaEventDestroy(join_ev);
+  for (void* m : peer_maps) cudaIpcCloseMemHandle(m);
   if (arena) cudaFree(arena);
   if (comm_stream) cudaStreamDestroy(comm_stream);
   if (group) {
@@ -353,12 +359,31 @@ void dear_ctx::exec(const Op& op) {
       break;
     case OP_PACK:
       record_t(op.bucket, T_PACK0);
-      cuda_check(launch_pack(B->pack_u, B->pack_s, B->e_pack, pack_scale, comm_stream), "pack kernel");
+      if (peer) {
+        // Our buffer may be rewritten only once every peer gathered from it.
+        cuda_check(launch_wait_peers(&B->flags->packed, &B->flags->gathered, pa, comm_stream),
+                   "wait kernel");
+        cuda_check(launch_pack_signal(B->pack_u, B->pack_s, B->e_pack, pack_scale, B->flags,
+                                      comm_stream),
+                   "pack kernel");
+      } else {
+        cuda_check(launch_pack(B->pack_u, B->pack_s, B->e_pack, pack_scale, comm_stream),
+                   "pack kernel");
+      }
       cuda_check(cudaEventRecord(packed_ev, comm_stream), "cudaEventRecord");
       record_t(op.bucket, T_PACK1);
       break;
     case OP_RS:
-      if (!local && P > 1 && B->stride > 0) {
+      if (peer) {
+        // Fused reduce-scatter + update over NVLink (OP_UPDATE becomes a no-op).
+        cuda_check(launch_wait_peers(&B->flags->packed, &B->flags->packed, pa, comm_stream),
+                   "wait kernel");
+        cuda_check(launch_rs_update_peer(B->upd_u, B->upd_s, B->e_upd, hp_dev, B->mom_init ? 1 : 0,
+                                         cfg.momentum != 0.0, cfg.weight_decay != 0.0, pa,
+                                         B->flags, comm_stream),
+                   "rs+update kernel");
+        if (cfg.momentum != 0.0) B->mom_init = true;
+      } else if (!local && P > 1 && B->stride > 0) {
         nccl_check(ncclReduceScatter(B->buf, B->buf + static_cast<int64_t>(rank) * B->stride,
                                      static_cast<size_t>(B->stride), ncclFloat32, ncclSum, comm,
                                      comm_stream),
@@ -367,6 +392,7 @@ void dear_ctx::exec(const Op& op) {
       record_t(op.bucket, T_RS1);
       break;
     case OP_UPDATE:
+      if (peer) break;
       cuda_check(launch_update(B->upd_u, B->upd_s, B->e_upd, hp_dev, B->mom_init ? 1 : 0,
                                cfg.momentum != 0.0, cfg.weight_decay != 0.0, comm_stream),
                  "update kernel");
@@ -375,7 +401,14 @@ void dear_ctx::exec(const Op& op) {
       break;
     case OP_AG:
       if (!local) record_t(op.bucket, T_AG0);
-      if (!local && P > 1 && B->stride > 0) {
+      if (peer) {
+        // Fused all-gather + unpack over NVLink (OP_UNPACK becomes a no-op).
+        cuda_check(launch_wait_peers(&B->flags->updated, &B->flags->updated, pa, comm_stream),
+                   "wait kernel");
+        cuda_check(launch_ag_unpack_peer(B->unpack_u, B->unpack_s, B->e_unpack,
+                                         B->any_shadow ? 1 : 0, pa, B->flags, comm_stream),
+                   "ag+unpack kernel");
+      } else if (!local && P > 1 && B->stride > 0) {
         nccl_check(ncclAllGather(B->buf + static_cast<int64_t>(rank) * B->stride, B->buf,
                                  static_cast<size_t>(B->stride), ncclFloat32, comm, comm_stream),
                    "ncclAllGather");
@@ -383,6 +416,7 @@ void dear_ctx::exec(const Op& op) {
       record_t(op.bucket, T_AG1);
       break;
     case OP_UNPACK:
+      if (peer) break;
       cuda_check(launch_unpack(B->unpack_u, B->unpack_s, B->e_unpack, B->any_shadow ? 1 : 0,
                                comm_stream),
                  "unpack kernel");
@@ -685,15 +719,24 @@ int dear_finalize(dear_ctx* ctx) {
   const size_t unit_bytes = (units * sizeof(Unit) + 255) / 256 * 256;
   const size_t n_slices = plan.size() * 3 * static_cast<size_t>(kSlices);
   const size_t slice_bytes = (n_slices * sizeof(Slice) + 255) / 256 * 256;
-  const size_t total = float_bytes + unit_bytes + slice_bytes + 256 + 256;
+  // Layout: [bucket buffers + momentum][flags] is identical on every rank (the
+  // region peers address through IPC); unit/slice tables (rank-specific)
+  // follow.
+  const size_t flag_bytes = (plan.size() * sizeof(BucketFlags) + 255) / 256 * 256;
+  const size_t total = float_bytes + flag_bytes + unit_bytes + slice_bytes + 256 + 256;
   cuda_check(cudaMalloc(&c.arena, total), "cudaMalloc(bucket arena)");
   cuda_check(cudaMemset(c.arena, 0, float_bytes), "cudaMemset");
   float* fp = reinterpret_cast<float*>(c.arena);
-  Unit* up = reinterpret_cast<Unit*>(c.arena + float_bytes);
-  Slice* sp = reinterpret_cast<Slice*>(c.arena + float_bytes + unit_bytes);
-  c.hp_dev = reinterpret_cast<HyperParams*>(c.arena + float_bytes + unit_bytes + slice_bytes);
-  c.hash_dev = reinterpret_cast<unsigned long long*>(c.arena + float_bytes + unit_bytes +
-                                                      slice_bytes + 256);
+  Unit* up = reinterpret_cast<Unit*>(c.arena + float_bytes + flag_bytes);
+  BucketFlags* fl = reinterpret_cast<BucketFlags*>(c.arena + float_bytes);
+  Slice* sp = reinterpret_cast<Slice*>(c.arena + float_bytes + flag_bytes + unit_bytes);
+  c.hp_dev = reinterpret_cast<HyperParams*>(c.arena + float_bytes + flag_bytes + unit_bytes +
+                                            slice_bytes);
+  c.hash_dev = reinterpret_cast<unsigned long long*>(c.arena + float_bytes + flag_bytes +
+                                                      unit_bytes + slice_bytes + 256);
+  c.arena_bytes = float_bytes + flag_bytes;  // the rank-independent (peer-shared) prefix
+  cuda_check(cudaMemset(fl, 0, flag_bytes), "cudaMemset(flags)");
+  for (size_t g = 0; g < plan.size(); ++g) c.buckets[g].flags = fl + g;
   std::vector<Slice> host_slices(n_slices);
   for (size_t g = 0; g < plan.size(); ++g) {
     Bucket& B = c.buckets[g];
@@ -715,7 +758,7 @@ int dear_finalize(dear_ctx* ctx) {
       for_each_piece(c, B, bg[static_cast<size_t>(ch)], bg[static_cast<size_t>(ch) + 1],
                      [&](int l, int64_t j, int64_t len, int64_t pos) {
                        const LayerReg& R = c.layers[static_cast<size_t>(l - 1)];
-                       host_units.push_back({R.grad + j, B.buf + slot * B.stride + pos, nullptr, len, 0});
+                       host_units.push_back({R.grad + j, B.buf + slot * B.stride + pos, nullptr, len, 0, 0, 0});
                      });
     }
     B.n_pack = static_cast<int>(host_units.size() - static_cast<size_t>(B.pack_u - up));
@@ -727,7 +770,7 @@ int dear_finalize(dear_ctx* ctx) {
                    [&](int l, int64_t j, int64_t len, int64_t pos) {
                      const LayerReg& R = c.layers[static_cast<size_t>(l - 1)];
                      host_units.push_back({R.param + j, B.buf + c.rank * B.stride + pos,
-                                           B.mom ? static_cast<void*>(B.mom + pos) : nullptr, len, 0});
+                                           B.mom ? static_cast<void*>(B.mom + pos) : nullptr, len, 0, 0, 0});
                    });
     B.n_upd = static_cast<int>(host_units.size() - static_cast<size_t>(B.upd_u - up));
     B.e_upd = set_starts(host_units, static_cast<size_t>(B.upd_u - up));
@@ -739,7 +782,7 @@ int dear_finalize(dear_ctx* ctx) {
                      [&](int l, int64_t j, int64_t len, int64_t pos) {
                        const LayerReg& R = c.layers[static_cast<size_t>(l - 1)];
                        void* sh = R.shadow ? static_cast<void*>(static_cast<uint16_t*>(R.shadow) + j) : nullptr;
-                       host_units.push_back({B.buf + slot * B.stride + pos, R.param + j, sh, len, 0});
+                       host_units.push_back({B.buf + slot * B.stride + pos, R.param + j, sh, len, 0, slot, 0});
                      });
     }
     B.n_unpack = static_cast<int>(host_units.size() - static_cast<size_t>(B.unpack_u - up));
@@ -952,6 +995,65 @@ int dear_set_lr(dear_ctx* ctx, double lr) {
                              ctx->comm_stream),
              "cudaMemcpyAsync(hp)");
   cuda_check(cudaStreamSynchronize(ctx->comm_stream), "cudaStreamSynchronize");
+  DEAR_API_END
+}
+
+int dear_peer_handle(dear_ctx* ctx, uint8_t out[DEAR_PEER_HANDLE_BYTES]) {
+  DEAR_API_BEGIN
+  need(ctx, true);
+  if (ctx->local) invalid("dear_peer_handle: local-group contexts have no peer backend");
+  if (!out) invalid("dear_peer_handle: null output");
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "ipc handle size");
+  cudaIpcMemHandle_t h;
+  cuda_check(cudaIpcGetMemHandle(&h, ctx->arena), "cudaIpcGetMemHandle");
+  memset(out, 0, DEAR_PEER_HANDLE_BYTES);
+  memcpy(out, &h, 64);
+  const uint64_t sz = ctx->arena_bytes;
+  memcpy(out + 64, &sz, 8);
+  const int32_t r = ctx->rank;
+  memcpy(out + 72, &r, 4);
+  DEAR_API_END
+}
+
+int dear_peer_connect(dear_ctx* ctx, const uint8_t* handles, int32_t n) {
+  DEAR_API_BEGIN
+  need(ctx, true);
+  dear_ctx& c = *ctx;
+  if (c.local) invalid("dear_peer_connect: local-group contexts have no peer backend");
+  if (c.peer) invalid("dear_peer_connect: already connected");
+  if (!handles || n != c.P) invalid("dear_peer_connect: need one handle per rank");
+  if (c.P > kMaxPeers) invalid("dear_peer_connect: at most 16 ranks");
+  PeerArgs pa{};
+  pa.P = c.P;
+  pa.rank = c.rank;
+  std::vector<void*> maps;
+  try {
+    for (int k = 0; k < c.P; ++k) {
+      const uint8_t* h = handles + static_cast<size_t>(k) * DEAR_PEER_HANDLE_BYTES;
+      uint64_t sz = 0;
+      int32_t r = -1;
+      memcpy(&sz, h + 64, 8);
+      memcpy(&r, h + 72, 4);
+      if (r != k) invalid("dear_peer_connect: handles must be in rank order");
+      if (sz != c.arena_bytes) invalid("dear_peer_connect: ranks registered different models");
+      if (k == c.rank) {
+        pa.delta[k] = 0;
+        continue;
+      }
+      cudaIpcMemHandle_t ih;
+      memcpy(&ih, h, 64);
+      void* p = nullptr;
+      cuda_check(cudaIpcOpenMemHandle(&p, ih, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+      maps.push_back(p);
+      pa.delta[k] = static_cast<int64_t>(static_cast<char*>(p) - c.arena);
+    }
+  } catch (...) {
+    for (void* m : maps) cudaIpcCloseMemHandle(m);
+    throw;
+  }
+  c.pa = pa;
+  c.peer_maps = std::move(maps);
+  c.peer = true;
   DEAR_API_END
 }
 

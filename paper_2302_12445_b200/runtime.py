@@ -97,11 +97,16 @@ class Runtime:
                  lr: float = 0.05, momentum: float = 0.0, dampening: float = 0.0,
                  weight_decay: float = 0.0, nesterov: bool = False,
                  dear_group_dependency: bool = False, defer_allgather: bool = False,
-                 stream: Optional[torch.cuda.Stream] = None):
+                 backend: str = "nccl", stream: Optional[torch.cuda.Stream] = None):
         if policy not in POLICIES:
             raise ValueError(f"unknown policy kind {policy!r}; expected one of "
                              f"{', '.join(POLICIES)}")
+        if backend not in ("nccl", "peer"):
+            raise ValueError("backend must be 'nccl' or 'peer'")
+        if backend == "peer" and isinstance(comm, LocalGroup):
+            raise ValueError("the peer backend needs one process per GPU (not a LocalGroup)")
         self.policy = policy
+        self.backend = backend
         cfg = DearCfg(POLICIES[policy], int(fusion_buffer_bytes) if "FUSED" in policy else 0,
                       int(dear_group_dependency), float(lr),
                       float(momentum), float(dampening), float(weight_decay), int(nesterov),
@@ -141,6 +146,19 @@ class Runtime:
 
     def finalize(self) -> None:
         check(lib().dear_finalize(self._ctx))
+        if self.backend == "peer" and self.world_size > 1:
+            self._connect_peers()
+
+    def _connect_peers(self) -> None:
+        """Exchange arena IPC handles over torch.distributed and map the peers."""
+        import torch.distributed as dist
+
+        buf = C.create_string_buffer(128)
+        check(lib().dear_peer_handle(self._ctx, buf))
+        handles = [None] * self.world_size
+        dist.all_gather_object(handles, buf.raw)
+        check(lib().dear_peer_connect(self._ctx, b"".join(handles), self.world_size))
+        dist.barrier()
 
     # -- schedule hooks ----------------------------------------------------
     def grad_ready(self, layer: int, stream=None) -> None:

@@ -33,13 +33,14 @@ def close(a, b, tol=1e-5):
     return bool(np.all(np.abs(a - b) <= tol * np.maximum(1.0, np.abs(b))))
 
 
-def run_runtime(comm, rank, P, policy, buf, steps, lr, **kw):
+def run_runtime(comm, rank, P, policy, buf, steps, lr, backend="nccl", **kw):
     o = Restated()
     numels = RAGGED
     offs = np.concatenate([[0], np.cumsum(numels)]).astype(np.int64)
     w0 = initial_weights(o, numels)
     s = torch.cuda.Stream()
-    rt = dear.Runtime(comm, rank, P, policy=policy, fusion_buffer_bytes=buf, lr=lr, stream=s, **kw)
+    rt = dear.Runtime(comm, rank, P, policy=policy, fusion_buffer_bytes=buf, lr=lr, stream=s,
+                      backend=backend, **kw)
     params, grads = [], []
     for l in range(1, len(numels) + 1):
         p = torch.from_numpy(w0[offs[l - 1]:offs[l]].copy()).cuda()
@@ -94,6 +95,35 @@ def case_runtime(rank, P):
     return ok
 
 
+def case_peer(rank, P):
+    """NVLink peer backend: fused RS+update / AG+unpack kernels sum in the
+    reference's ring order, so parameters are BIT-EXACT with the fp32
+    ring-order restatement (and within 1e-5 of the fp64 oracle)."""
+    comm = dear.init()
+    o = Restated()
+    ok = True
+    for policy, buf in (("DEAR_FUSED", 100_000), ("DEAR", 0), ("WFBP_FUSED", 400_000),
+                        ("WFBP", 0), ("DEAR_FUSED", 25_000_000)):
+        w, same, _ = run_runtime(comm, rank, P, policy, buf, 3, 0.05, backend="peer")
+        exp32 = oracle_run(o, RAGGED, P, 3, policy, buf, 0.05, f32=True)
+        exp64 = oracle_run(o, RAGGED, P, 3, policy, buf, 0.05, f32=False)
+        good = same and np.array_equal(w, exp32) and close(w.astype(np.float64), exp64)
+        if rank == 0:
+            print(f"[peer P={P}] {policy:11s} buf={buf:>9} replicas={same} "
+                  f"bit_exact_fp32_ring={np.array_equal(w, exp32)} "
+                  f"oracle_1e-5={close(w.astype(np.float64), exp64)}", flush=True)
+        ok &= good
+    kw = dict(momentum=0.9, weight_decay=1e-3, nesterov=True)
+    w, same, _ = run_runtime(comm, rank, P, "DEAR_FUSED", 200_000, 4, 0.02, backend="peer", **kw)
+    exp32 = oracle_run(o, RAGGED, P, 4, "DEAR_FUSED", 200_000, 0.02, f32=True, **kw)
+    good = same and np.array_equal(w, exp32)
+    if rank == 0:
+        print(f"[peer P={P}] momentum/wd/nesterov bit_exact={good}", flush=True)
+    ok &= good
+    comm.close()
+    return ok
+
+
 def case_distoptim(rank, P):
     comm = dear.init()
     torch.manual_seed(0)
@@ -137,7 +167,7 @@ def main():
     rank, P = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     torch.cuda.set_device(int(os.environ["LOCAL_RANK"]))
     dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ["LOCAL_RANK"])))
-    ok = {"runtime": case_runtime, "distoptim": case_distoptim}[case](rank, P)
+    ok = {"runtime": case_runtime, "distoptim": case_distoptim, "peer": case_peer}[case](rank, P)
     t = torch.tensor([0 if ok else 1], device="cuda")
     dist.all_reduce(t)
     dist.destroy_process_group()
