@@ -44,6 +44,14 @@ int dear_gemm_run_group(dear_gemm_plan* const* plans, int32_t n, void* stream);
 /* Tile geometry actually used: BN, grid.x (N tiles), grid.y (M tiles), splits. */
 int dear_gemm_plan_info(dear_gemm_plan* plan, int32_t* bn, int32_t* n_tiles, int32_t* m_tiles,
                         int32_t* splits);
+/* Cluster shape (cm x cn CTAs sharing operands by TMA multicast) and how
+ * many such clusters are resident at once. */
+int dear_gemm_plan_cluster(dear_gemm_plan* plan, int32_t* cm, int32_t* cn, int32_t* resident);
+/* Profiling: when set, every subsequent launch writes 8 %globaltimer stamps
+ * per CTA into this device buffer (CTA start, prologue done, dependency
+ * released, first stage landed, last MMA issued, epilogue done, CTA end);
+ * NULL turns it off (the default). */
+int dear_gemm_set_trace(void* device_buffer);
 int dear_gemm_plan_destroy(dear_gemm_plan* plan);
 
 #ifdef __cplusplus

@@ -20,8 +20,12 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-BUILD = os.path.join(ROOT, "build", "dear")
-LIB = os.path.join(PKG, "libdear.so")
+# DEAR_VARIANT="NAME:-DFOO=1,-DBAR=2" builds an experiment variant into
+# libdear_NAME.so (selected at run time with DEAR_LIB=libdear_NAME.so).
+_VARIANT = os.environ.get("DEAR_VARIANT", "")
+_VNAME, _VDEFS = (_VARIANT.split(":", 1) + [""])[:2] if _VARIANT else ("", "")
+BUILD = os.path.join(ROOT, "build", "dear" + (f"_{_VNAME}" if _VNAME else ""))
+LIB = os.path.join(PKG, f"libdear_{_VNAME}.so" if _VNAME else "libdear.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CUTLASS_INC = None  # CuTe headers are not needed by the current kernels
 
@@ -36,7 +40,8 @@ def nvcc() -> str:
 def _flags() -> list[str]:
     return [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-Wall",
             "-I" + os.path.join(ROOT, "include"), "-I" + CSRC,
-            "--expt-relaxed-constexpr", "-Xptxas", "-v" if os.environ.get("DEAR_PTXAS_V") else "-O3"]
+            "--expt-relaxed-constexpr", "-Xptxas", "-v" if os.environ.get("DEAR_PTXAS_V") else "-O3",
+            *[d for d in _VDEFS.split(",") if d]]
 
 
 def _stale(obj: str, deps: list[str]) -> bool:

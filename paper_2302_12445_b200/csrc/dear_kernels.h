@@ -33,7 +33,13 @@ constexpr int64_t kUnitElems = 1 << 20;
 
 // Grid of every bucket-op launch: 4 resident 256-thread CTAs on each of the
 // 148 SMs, one wave, equal element slices.
-constexpr int kSlices = 148 * 4;
+#ifndef DEAR_SLICES_PER_SM
+#define DEAR_SLICES_PER_SM 4
+#endif
+constexpr int kSlices = 148 * DEAR_SLICES_PER_SM;
+// NVLink-bound peer kernels need far fewer CTAs to saturate the links
+// (~1.2 MB in flight); a small grid leaves the SMs to the concurrent GEMMs.
+constexpr int kPeerSlices = 64;
 
 struct Slice {
   int32_t unit;   // first unit of this CTA's slice
@@ -63,8 +69,10 @@ cudaError_t launch_update(const Unit* units, const Slice* slices, int64_t total,
                           int use_wd, cudaStream_t s);
 cudaError_t launch_unpack(const Unit* units, const Slice* slices, int64_t total, int with_shadow,
                           cudaStream_t s);
-// Host: the Slice table (kSlices entries) for a unit list with prefix starts.
-void make_slices(const Unit* units, int n_units, int64_t total, Slice* out);
+// Host: the Slice table (n_slices entries, one per CTA) for a unit list with
+// prefix starts.
+void make_slices(const Unit* units, int n_units, int64_t total, Slice* out,
+                 int n_slices = kSlices);
 
 // Local-group collectives over P same-device buffers (ring order, in place):
 // rs: bufs[r][r*stride + i] = fold_k bufs[(r+1+k)%P][r*stride + i], k = 0..P-1

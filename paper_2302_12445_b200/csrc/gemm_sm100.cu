@@ -25,6 +25,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <string>
 
 #include "dear_gemm.h"
@@ -67,6 +68,14 @@ struct alignas(64) Problem {
   int32_t b_boxes;
   uint32_t idesc;
   uint32_t tx_bytes;
+  // Thread-block cluster of cm x cn CTAs sharing operands through TMA
+  // multicast: CTA (i, j) computes tile (mg*cm + i, ng*cn + j); the A tile
+  // of row i is fetched once, in cn pieces of a_rows rows, and multicast to
+  // the cn CTAs of that row; B likewise to the cm CTAs of column j.
+  int32_t cm, cn;
+  int32_t mg_tiles, ng_tiles;  // cluster tiles along M / N
+  int32_t a_rows;              // 128 / cn
+  int32_t b_rows;              // K-major: bn / cm rows; MN-major: 64 / cm k-rows per box
 };
 
 struct Launch {
@@ -75,6 +84,8 @@ struct Launch {
   int32_t total_tiles;
   int32_t stages;       // smem ring depth (narrow B tiles -> deeper ring)
   int32_t stage_bytes;  // A (16 KB) + widest B of the problems, 1 KB aligned
+  int32_t cm, cn;       // cluster shape shared by the problems of the launch
+  uint64_t* trace;      // optional per-CTA phase timestamps (profiling), or null
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -121,6 +132,41 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* ba
       : "memory");
 }
 
+__device__ __forceinline__ void tma_load_2d_mc(const CUtensorMap* map, uint64_t* bar, void* dst,
+                                               int32_t c0, int32_t c1, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_id_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t n_clusters_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+
 // UMMA shared-memory matrix descriptor, SWIZZLE_128B, Blackwell version 1.
 //   K-major  : rows of 128 B (64 bf16 along K); 8-row groups SBO = 1024 B apart.
 //   MN-major : 64 MN-elements per 128 B row, one row per k; 8-k groups
@@ -141,6 +187,15 @@ __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t a, uint64_t 
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(a), "l"(b), "r"(idesc), "r"(accum));
+}
+
+// Arrive on the barrier at the same smem offset in every CTA of `mask`.
+__device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"(mask)
+      : "memory");
 }
 
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
@@ -247,19 +302,20 @@ struct TileCoord {
   int kb0, kb1;
 };
 
-// Tile t of the launch: problems back to back; inside a problem
-// (split, m_tile, n_tile) with n fastest, so concurrently running CTAs share
-// the same A rows.
-__device__ __forceinline__ TileCoord decode(const Launch& L, int t) {
+// Cluster tile t of the launch: problems back to back; inside a problem
+// (split, m group, n group) with n fastest. CTA (ci, cj) of the cluster takes
+// tile (mg * cm + ci, ng * cn + cj); tiles past M / N compute on zero-filled
+// operands (they still source their multicast pieces) and store nothing.
+__device__ __forceinline__ TileCoord decode(const Launch& L, int t, int ci, int cj) {
   TileCoord c;
   c.prob = (L.n_problems > 1 && t >= L.p[0].tiles) ? 1 : 0;
   const Problem& P = L.p[c.prob];
   const int local = c.prob ? t - L.p[0].tiles : t;
-  const int per = P.m_tiles * P.n_tiles;
+  const int per = P.mg_tiles * P.ng_tiles;
   const int split = local / per;
   const int r = local - split * per;
-  c.m0 = static_cast<int64_t>(r / P.n_tiles) * kBM;
-  c.n0 = static_cast<int64_t>(r % P.n_tiles) * P.bn;
+  c.m0 = static_cast<int64_t>((r / P.ng_tiles) * P.cm + ci) * kBM;
+  c.n0 = static_cast<int64_t>((r % P.ng_tiles) * P.cn + cj) * P.bn;
   c.kb0 = split * P.kb_per_split;
   c.kb1 = min(c.kb0 + P.kb_per_split, P.num_kb);
   return c;
@@ -279,14 +335,26 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const int csize = L.cm * L.cn;
+  const int crank = csize > 1 ? static_cast<int>(cluster_ctarank()) : 0;
+  const int ci = crank / L.cn, cj = crank % L.cn;
+  const int cid = csize > 1 ? static_cast<int>(cluster_id_x()) : static_cast<int>(blockIdx.x);
+  const int ncl = csize > 1 ? static_cast<int>(n_clusters_x()) : static_cast<int>(gridDim.x);
+  // CTAs sharing this CTA's A tile (same row) and B tile (same column).
+  uint16_t row_mask = 0, col_mask = 0;
+  for (int j = 0; j < L.cn; ++j) row_mask |= static_cast<uint16_t>(1u << (ci * L.cn + j));
+  for (int i = 0; i < L.cm; ++i) col_mask |= static_cast<uint16_t>(1u << (i * L.cn + cj));
 
+  uint64_t* tr = L.trace ? L.trace + blockIdx.x * 8 : nullptr;
+  if (tr && threadIdx.x == 0) tr[0] = globaltimer();  // CTA start
   // Let the next kernel in the stream start its prologue as soon as SMs free.
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      // released by every CTA this CTA multicasts into (its row and column)
+      mbar_init(&empty[s], static_cast<uint32_t>(L.cm + L.cn - 1));
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tmem_full[a], 1);
@@ -307,19 +375,34 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
-  __syncthreads();
+  if (csize > 1)
+    cluster_sync();  // peers' barriers are initialised before any multicast
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (tr && threadIdx.x == 0) tr[1] = globaltimer();  // prologue done
   // Everything above overlaps the previous kernel; memory is touched only now.
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (tr && threadIdx.x == 0) tr[2] = globaltimer();  // dependency released
 
   if (warp == 0) {
     if (lane == 0) {
       uint32_t g = 0;
-      for (int t = blockIdx.x; t < L.total_tiles; t += gridDim.x) {
-        const TileCoord tc = decode(L, t);
+      for (int t = cid; t < L.total_tiles; t += ncl) {
+        const TileCoord tc = decode(L, t, ci, cj);
         const Problem& P = L.p[tc.prob];
-        for (int kb = tc.kb0; kb < tc.kb1; ++kb, ++g) {
+        const int nk = tc.kb1 - tc.kb0;
+        // (uniform within a cluster: multicast pieces of a stage share one k-block)
+#ifdef DEAR_GEMM_NO_ROTATE
+        const int rot = 0;
+#else
+        const int rot = nk > 0 ? (t * 5) % nk : 0;
+#endif
+        for (int i = 0; i < nk; ++i, ++g) {
+          // Rotated k order: CTAs sharing an operand tile read different
+          // k-blocks at any moment instead of hammering the same L2 lines.
+          const int kb = tc.kb0 + (i + rot) % nk;
           const int s = g % stages;
           const uint32_t ph = (g / stages) & 1;
           mbar_wait(&empty[s], ph ^ 1);
@@ -327,13 +410,30 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           const int kc = kb * kBK;
           uint8_t* sA = smem + s * stage_bytes;
           uint8_t* sB = sA + kAStage;
-          tma_load_2d(&P.tmA, &full[s], sA, kc, static_cast<int32_t>(tc.m0));
+          // A: this CTA's piece (rows cj*a_rows ..) of its row's tile.
+          const int32_t am = static_cast<int32_t>(tc.m0) + cj * P.a_rows;
+          uint8_t* dA = sA + cj * P.a_rows * 128;
+          if (P.cn > 1)
+            tma_load_2d_mc(&P.tmA, &full[s], dA, kc, am, row_mask);
+          else
+            tma_load_2d(&P.tmA, &full[s], dA, kc, am);
           if (!P.b_mn_major) {
-            tma_load_2d(&P.tmB, &full[s], sB, kc, static_cast<int32_t>(tc.n0));
+            const int32_t bn0 = static_cast<int32_t>(tc.n0) + ci * P.b_rows;
+            uint8_t* dB = sB + ci * P.b_rows * 128;
+            if (P.cm > 1)
+              tma_load_2d_mc(&P.tmB, &full[s], dB, kc, bn0, col_mask);
+            else
+              tma_load_2d(&P.tmB, &full[s], dB, kc, bn0);
           } else {
-            for (int j = 0; j < P.b_boxes; ++j)
-              tma_load_2d(&P.tmB, &full[s], sB + j * 8192, static_cast<int32_t>(tc.n0 + 64 * j),
-                          kc);
+            for (int j = 0; j < P.b_boxes; ++j) {
+              uint8_t* dB = sB + j * 8192 + ci * P.b_rows * 128;
+              const int32_t c0 = static_cast<int32_t>(tc.n0 + 64 * j);
+              const int32_t c1 = kc + ci * P.b_rows;
+              if (P.cm > 1)
+                tma_load_2d_mc(&P.tmB, &full[s], dB, c0, c1, col_mask);
+              else
+                tma_load_2d(&P.tmB, &full[s], dB, c0, c1);
+            }
           }
         }
       }
@@ -341,18 +441,20 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   } else if (warp == 1) {
     if (lane == 0) {
       uint32_t g = 0, j = 0;
-      for (int t = blockIdx.x; t < L.total_tiles; t += gridDim.x, ++j) {
-        const TileCoord tc = decode(L, t);
+      for (int t = cid; t < L.total_tiles; t += ncl, ++j) {
+        const TileCoord tc = decode(L, t, ci, cj);
         const Problem& P = L.p[tc.prob];
         const uint32_t acc = j & 1, aph = (j >> 1) & 1;
         mbar_wait(&tmem_empty[acc], aph ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem + acc * kAccCols;
-        for (int kb = tc.kb0; kb < tc.kb1; ++kb, ++g) {
+        const int nk = tc.kb1 - tc.kb0;
+        for (int i = 0; i < nk; ++i, ++g) {
           const int s = g % stages;
           const uint32_t ph = (g / stages) & 1;
           mbar_wait(&full[s], ph);
           tc_fence_after();
+          if (tr && g == 0) tr[3] = globaltimer();  // first stage landed
           const uint32_t a_base = smem_u32(smem + s * stage_bytes);
           const uint32_t b_base = a_base + kAStage;
 #pragma unroll
@@ -360,19 +462,23 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             const uint64_t ad = sdesc(a_base + k * 32, 16, 1024);
             const uint64_t bd = P.b_mn_major ? sdesc(b_base + k * 2048, 8192, 1024)
                                              : sdesc(b_base + k * 32, 16, 1024);
-            umma_bf16(d_tmem, ad, bd, P.idesc, (kb != tc.kb0 || k != 0) ? 1u : 0u);
+            umma_bf16(d_tmem, ad, bd, P.idesc, (i != 0 || k != 0) ? 1u : 0u);
           }
-          umma_commit(&empty[s]);
+          if (csize > 1)
+            umma_commit_mc(&empty[s], static_cast<uint16_t>(row_mask | col_mask));
+          else
+            umma_commit(&empty[s]);
         }
         umma_commit(&tmem_full[acc]);
       }
+      if (tr) tr[4] = globaltimer();  // last MMA issued
     }
     __syncwarp();
   } else {
     const int q = warp & 3;
     uint32_t j = 0;
-    for (int t = blockIdx.x; t < L.total_tiles; t += gridDim.x, ++j) {
-      const TileCoord tc = decode(L, t);
+    for (int t = cid; t < L.total_tiles; t += ncl, ++j) {
+      const TileCoord tc = decode(L, t, ci, cj);
       const Problem& P = L.p[tc.prob];
       const uint32_t acc = j & 1, aph = (j >> 1) & 1;
       mbar_wait(&tmem_full[acc], aph);
@@ -389,9 +495,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       __syncwarp();
       if (lane == 0) mbar_arrive(&tmem_empty[acc]);
     }
+    if (tr && warp == 2 && lane == 0) tr[5] = globaltimer();  // epilogue done
   }
   tc_fence_before();
-  __syncthreads();
+  if (csize > 1)
+    cluster_sync();  // nobody exits while peers may still multicast into it
+  else
+    __syncthreads();
+  if (tr && threadIdx.x == 0) tr[6] = globaltimer();  // CTA end
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
@@ -434,30 +545,49 @@ void make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer
   }
 }
 
-// Tile width: the fewest N tiles (<= 256 wide) unless more, narrower tiles
-// fill the persistent grid markedly better (fewer waves of work per SM).
-int choose_bn(int64_t M, int64_t N, int splits) {
+struct TileChoice {
+  int bn, cm, cn;
+};
+
+int max_active_clusters(int csize);
+
+// Joint choice of the tile width BN and the cluster shape (cm x cn) for one
+// problem: estimated time = waves x k-blocks x max(MMA cycles, L2->SM operand
+// cycles) + per-tile overhead, where a cluster fetches each A tile once per
+// row (multicast to cn CTAs) and each B tile once per column (to cm CTAs),
+// and a wave is every resident cluster running one cluster tile. Constraints:
+// BN a multiple of 16 (of 8*cm for split B pieces), <= 256.
+TileChoice choose_tiles(int64_t M, int64_t N, int kb_per_tile, int splits, bool mn_major,
+                        bool allow_clusters) {
   const int64_t m_tiles = (M + kBM - 1) / kBM;
-  auto waves_cost = [&](int64_t bn) {
-    const int64_t nt = (N + bn - 1) / bn;
-    const int64_t tiles = m_tiles * nt * splits;
-    const int64_t waves = (tiles + kSms - 1) / kSms;
-    // per-tile mainloop cost ~ max(bn, 64) columns + fixed overhead
-    return waves * (std::max<int64_t>(bn, 64) + 48);
-  };
-  const int64_t nt0 = (N + kBNMax - 1) / kBNMax;
-  int64_t best_bn = ((N + nt0 - 1) / nt0 + 15) / 16 * 16;
-  int64_t best = waves_cost(best_bn);
-  for (int64_t nt = nt0 + 1; nt <= nt0 * 4; ++nt) {
-    const int64_t bn = ((N + nt - 1) / nt + 15) / 16 * 16;
-    if (bn < 64) break;
-    const int64_t c = waves_cost(bn);
-    if (c < best) {
-      best = c;
-      best_bn = bn;
+  const double l2_bytes_per_cycle_per_sm = 42.0;  // LTS cap / 148 SMs (B300_MICROARCH)
+  TileChoice best{256, 1, 1};
+  double best_cost = 1e300;
+  const int shapes[4][2] = {{1, 1}, {2, 1}, {1, 2}, {2, 2}};
+  for (const auto& sh : shapes) {
+    const int cm = sh[0], cn = sh[1];
+    if (!allow_clusters && cm * cn > 1) continue;
+    if (cm > m_tiles) continue;
+    const int active = max_active_clusters(cm * cn);
+    for (int bn = 256; bn >= 48; bn -= 16) {
+      if (bn % (8 * cm)) continue;
+      if (mn_major && 64 % cm) continue;
+      const int64_t n_tiles = (N + bn - 1) / bn;
+      if (cn > n_tiles) continue;
+      // too-wide tiles waste MMA columns on padding; skip if > 1 tile of slack
+      if (n_tiles > 1 && (n_tiles - 1) * bn >= N) continue;
+      const int64_t groups = ((m_tiles + cm - 1) / cm) * ((n_tiles + cn - 1) / cn) * splits;
+      const int64_t waves = (groups + active - 1) / active;
+      const double mma = 2.0 * bn;  // 4 x (128 x bn / 256) cycles per 64-deep k-block
+      const double mem = (16384.0 / cn + 128.0 * bn / cm) / l2_bytes_per_cycle_per_sm;
+      const double cost = waves * (kb_per_tile * std::max(mma, mem) + 1500.0);
+      if (cost < best_cost * 0.999) {
+        best_cost = cost;
+        best = {bn, cm, cn};
+      }
     }
   }
-  return static_cast<int>(best_bn);
+  return best;
 }
 
 }  // namespace gemm
@@ -467,29 +597,77 @@ struct dear_gemm_plan {
   dear::gemm::Problem p;
 };
 
+namespace {
+uint64_t* g_trace = nullptr;  // device buffer: 8 timestamps per CTA (profiling only)
+}
+
 using dear::Error;
+
+namespace {
+
+}  // namespace
+
+namespace dear {
+namespace gemm {
+void set_smem_attr() {
+  static bool done = false;
+  if (!done) {
+    if (cudaFuncSetAttribute(gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kSmemBytes) != cudaSuccess)
+      throw Error(DEAR_EINTERNAL, "cudaFuncSetAttribute(gemm smem)");
+    if (cudaFuncSetAttribute(gemm_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+        cudaSuccess)
+      (void)cudaGetLastError();
+    done = true;
+  }
+}
+
+int max_active_clusters(int csize) {
+  static int cache[17] = {0};
+  if (csize <= 1) return kSms;
+  if (cache[csize]) return cache[csize];
+  set_smem_attr();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(csize * (kSms / csize)));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmemBytes;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = static_cast<unsigned>(csize);
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, gemm_kernel, &cfg) != cudaSuccess || n < 1)
+    n = kSms / csize / 2;
+  cache[csize] = n;
+  return n;
+}
+}  // namespace gemm
+}  // namespace dear
 
 namespace {
 
 void launch(const dear::gemm::Launch& L, cudaStream_t stream) {
   using namespace dear::gemm;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             kSmemBytes) != cudaSuccess)
-      throw Error(DEAR_EINTERNAL, "cudaFuncSetAttribute(gemm smem)");
-    attr = true;
-  }
+  set_smem_attr();
+  const int csize = L.cm * L.cn;
+  const int clusters = std::min(L.total_tiles, dear::gemm::max_active_clusters(csize));
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(static_cast<unsigned>(std::min(L.total_tiles, kSms)));
+  cfg.gridDim = dim3(static_cast<unsigned>(clusters * csize));
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = kSmemBytes;
   cfg.stream = stream;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
+  at[1].id = cudaLaunchAttributeClusterDimension;
+  at[1].val.clusterDim.x = static_cast<unsigned>(csize);
+  at[1].val.clusterDim.y = 1;
+  at[1].val.clusterDim.z = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = csize > 1 ? 2 : 1;
   const cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_kernel, L);
   if (e != cudaSuccess) throw Error(DEAR_EINTERNAL, std::string("gemm launch: ") + cudaGetErrorString(e));
 }
@@ -535,7 +713,17 @@ int dear_gemm_plan_create(const void* A, int64_t lda, const void* B, int64_t ldb
   }
   const int kb_per = (num_kb + splits - 1) / splits;
   splits = (num_kb + kb_per - 1) / kb_per;
-  const int bn = choose_bn(M, N, splits);
+  // Clusters are opt-in (DEAR_GEMM_CLUSTER=1): on the per-layer shapes they cut
+  // L2->SM traffic but their scheduling spread costs more than they save
+  // (profiles/r01_gemm_trace.md).
+  const char* env = std::getenv("DEAR_GEMM_CLUSTER");
+  const bool clusters = env && env[0] == '1';
+  TileChoice tch = choose_tiles(M, N, kb_per, splits, b_mn_major != 0, clusters);
+  if (const char* fb = std::getenv("DEAR_GEMM_BN")) {  // tuning experiments only
+    const int v = std::atoi(fb);
+    if (v >= 16 && v <= 256 && v % 16 == 0) tch = {v, 1, 1};
+  }
+  const int bn = tch.bn;
   p.D = D;
   p.ldd = ldd;
   p.M = M;
@@ -547,7 +735,6 @@ int dear_gemm_plan_create(const void* A, int64_t lda, const void* B, int64_t ldb
   p.bn = bn;
   p.m_tiles = static_cast<int32_t>(m_tiles);
   p.n_tiles = static_cast<int32_t>((N + bn - 1) / bn);
-  p.tiles = p.m_tiles * p.n_tiles * splits;
   p.b_mn_major = b_mn_major ? 1 : 0;
   p.d_fp32 = d_fp32 ? 1 : 0;
   p.accumulate = accumulate ? 1 : 0;
@@ -555,15 +742,23 @@ int dear_gemm_plan_create(const void* A, int64_t lda, const void* B, int64_t ldb
             (static_cast<uint32_t>(bn >> 3) << 17) | (static_cast<uint32_t>(kBM >> 4) << 24);
   p.b_boxes = (bn + 63) / 64;
   p.tx_bytes = kAStage + (b_mn_major ? p.b_boxes * 8192 : static_cast<uint32_t>(bn) * kBK * 2);
+  // Cluster shape from the cost model (DEAR_GEMM_CLUSTER=0 disables clusters).
+  p.cm = tch.cm;
+  p.cn = tch.cn;
+  p.mg_tiles = (p.m_tiles + p.cm - 1) / p.cm;
+  p.ng_tiles = (p.n_tiles + p.cn - 1) / p.cn;
+  p.tiles = p.mg_tiles * p.ng_tiles * splits;  // cluster tiles
+  p.a_rows = kBM / p.cn;
+  p.b_rows = b_mn_major ? 64 / p.cm : bn / p.cm;
   try {
     make_map(&p.tmA, A, static_cast<uint64_t>(K), static_cast<uint64_t>(M),
-             static_cast<uint64_t>(lda), kBK, kBM);
+             static_cast<uint64_t>(lda), kBK, static_cast<uint32_t>(p.a_rows));
     if (!b_mn_major)
       make_map(&p.tmB, B, static_cast<uint64_t>(K), static_cast<uint64_t>(N),
-               static_cast<uint64_t>(ldb), kBK, static_cast<uint32_t>(bn));
+               static_cast<uint64_t>(ldb), kBK, static_cast<uint32_t>(p.b_rows));
     else
       make_map(&p.tmB, B, static_cast<uint64_t>(N), static_cast<uint64_t>(K),
-               static_cast<uint64_t>(ldb), 64, kBK);
+               static_cast<uint64_t>(ldb), 64, static_cast<uint32_t>(p.b_rows));
   } catch (...) {
     delete plan;
     throw;
@@ -576,6 +771,13 @@ int dear_gemm_run_group(dear_gemm_plan* const* plans, int32_t n, void* stream) {
   DEAR_API_BEGIN
   using namespace dear::gemm;
   if (!plans || n < 1 || n > kMaxProblems) throw Error(DEAR_EINVAL, "dear_gemm_run_group: 1 or 2 plans");
+  if (n == 2 && plans[0] && plans[1] &&
+      (plans[0]->p.cm != plans[1]->p.cm || plans[0]->p.cn != plans[1]->p.cn)) {
+    // Different cluster shapes cannot share a launch.
+    const int r0 = dear_gemm_run_group(plans, 1, stream);
+    if (r0 != DEAR_OK) return r0;
+    return dear_gemm_run_group(plans + 1, 1, stream);
+  }
   Launch L;
   L.n_problems = n;
   L.total_tiles = 0;
@@ -589,7 +791,15 @@ int dear_gemm_run_group(dear_gemm_plan* const* plans, int32_t n, void* stream) {
     b_stage = std::max(b_stage, bs);
   }
   L.stage_bytes = kAStage + b_stage;
+#ifdef DEAR_GEMM_FIXED_STAGES
+  L.stage_bytes = kAStage + kBStage;
+  L.stages = DEAR_GEMM_FIXED_STAGES;
+#else
   L.stages = std::min(kMaxStages, kRingBytes / L.stage_bytes);
+#endif
+  L.cm = plans[0]->p.cm;
+  L.cn = plans[0]->p.cn;
+  L.trace = g_trace;
   launch(L, static_cast<cudaStream_t>(stream));
   DEAR_API_END
 }
@@ -606,6 +816,21 @@ int dear_gemm_plan_info(dear_gemm_plan* plan, int32_t* bn, int32_t* n_tiles, int
   if (n_tiles) *n_tiles = plan->p.n_tiles;
   if (m_tiles) *m_tiles = plan->p.m_tiles;
   if (splits) *splits = plan->p.splits;
+  DEAR_API_END
+}
+
+int dear_gemm_plan_cluster(dear_gemm_plan* plan, int32_t* cm, int32_t* cn, int32_t* resident) {
+  DEAR_API_BEGIN
+  if (!plan) throw Error(DEAR_EINVAL, "null plan");
+  if (cm) *cm = plan->p.cm;
+  if (cn) *cn = plan->p.cn;
+  if (resident) *resident = dear::gemm::max_active_clusters(plan->p.cm * plan->p.cn);
+  DEAR_API_END
+}
+
+int dear_gemm_set_trace(void* device_buffer) {
+  DEAR_API_BEGIN
+  g_trace = static_cast<uint64_t*>(device_buffer);
   DEAR_API_END
 }
 

@@ -21,7 +21,10 @@ namespace dear {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kUnroll = 4;
+#ifndef DEAR_HBM_UNROLL
+#define DEAR_HBM_UNROLL 4
+#endif
+constexpr int kUnroll = DEAR_HBM_UNROLL;
 constexpr int kCtasPerSm = kSlices / 148;
 constexpr int kSms = 148;
 
@@ -459,13 +462,13 @@ cudaError_t launch_rs_update_peer(const Unit* units, const Slice* slices, int64_
                                   cudaStream_t s) {
   (void)total;
   if (use_momentum && use_wd)
-    rs_update_peer_kernel<true, true><<<kSlices, kThreads, 0, s>>>(units, slices, hp, has_momentum_buf, pa, flags);
+    rs_update_peer_kernel<true, true><<<kPeerSlices, kThreads, 0, s>>>(units, slices, hp, has_momentum_buf, pa, flags);
   else if (use_momentum)
-    rs_update_peer_kernel<true, false><<<kSlices, kThreads, 0, s>>>(units, slices, hp, has_momentum_buf, pa, flags);
+    rs_update_peer_kernel<true, false><<<kPeerSlices, kThreads, 0, s>>>(units, slices, hp, has_momentum_buf, pa, flags);
   else if (use_wd)
-    rs_update_peer_kernel<false, true><<<kSlices, kThreads, 0, s>>>(units, slices, hp, has_momentum_buf, pa, flags);
+    rs_update_peer_kernel<false, true><<<kPeerSlices, kThreads, 0, s>>>(units, slices, hp, has_momentum_buf, pa, flags);
   else
-    rs_update_peer_kernel<false, false><<<kSlices, kThreads, 0, s>>>(units, slices, hp, has_momentum_buf, pa, flags);
+    rs_update_peer_kernel<false, false><<<kPeerSlices, kThreads, 0, s>>>(units, slices, hp, has_momentum_buf, pa, flags);
   return cudaGetLastError();
 }
 
@@ -474,9 +477,9 @@ cudaError_t launch_ag_unpack_peer(const Unit* units, const Slice* slices, int64_
                                   cudaStream_t s) {
   (void)total;
   if (with_shadow)
-    ag_unpack_peer_kernel<true><<<kSlices, kThreads, 0, s>>>(units, slices, pa, flags);
+    ag_unpack_peer_kernel<true><<<kPeerSlices, kThreads, 0, s>>>(units, slices, pa, flags);
   else
-    ag_unpack_peer_kernel<false><<<kSlices, kThreads, 0, s>>>(units, slices, pa, flags);
+    ag_unpack_peer_kernel<false><<<kPeerSlices, kThreads, 0, s>>>(units, slices, pa, flags);
   return cudaGetLastError();
 }
 
@@ -505,12 +508,12 @@ cudaError_t launch_unpack(const Unit* units, const Slice* slices, int64_t total,
   return cudaGetLastError();
 }
 
-void make_slices(const Unit* units, int n_units, int64_t total, Slice* out) {
-  int64_t per = (total + kSlices - 1) / kSlices;
+void make_slices(const Unit* units, int n_units, int64_t total, Slice* out, int n_slices) {
+  int64_t per = (total + n_slices - 1) / n_slices;
   per = (per + 3) / 4 * 4;
   int u = 0;
   int64_t base = 0;  // start of unit u
-  for (int c = 0; c < kSlices; ++c) {
+  for (int c = 0; c < n_slices; ++c) {
     const int64_t lo = static_cast<int64_t>(c) * per;
     const int64_t cnt = lo >= total ? 0 : (total - lo < per ? total - lo : per);
     while (u < n_units && base + units[u].len <= lo && cnt > 0) {

@@ -98,6 +98,7 @@ struct Bucket {
   int n_pack = 0, n_upd = 0, n_unpack = 0;
   int64_t e_pack = 0, e_upd = 0, e_unpack = 0;  // elements per op
   Slice *pack_s = nullptr, *upd_s = nullptr, *unpack_s = nullptr;  // kSlices each
+  Slice *upd_ps = nullptr, *unpack_ps = nullptr;  // kPeerSlices each (peer kernels)
   BucketFlags* flags = nullptr;  // peer backend completion counters (in the arena)
   bool any_shadow = false;
   bool mom_init = false;
@@ -378,7 +379,7 @@ void dear_ctx::exec(const Op& op) {
         // Fused reduce-scatter + update over NVLink (OP_UPDATE becomes a no-op).
         cuda_check(launch_wait_peers(&B->flags->packed, &B->flags->packed, pa, comm_stream),
                    "wait kernel");
-        cuda_check(launch_rs_update_peer(B->upd_u, B->upd_s, B->e_upd, hp_dev, B->mom_init ? 1 : 0,
+        cuda_check(launch_rs_update_peer(B->upd_u, B->upd_ps, B->e_upd, hp_dev, B->mom_init ? 1 : 0,
                                          cfg.momentum != 0.0, cfg.weight_decay != 0.0, pa,
                                          B->flags, comm_stream),
                    "rs+update kernel");
@@ -405,7 +406,7 @@ void dear_ctx::exec(const Op& op) {
         // Fused all-gather + unpack over NVLink (OP_UNPACK becomes a no-op).
         cuda_check(launch_wait_peers(&B->flags->updated, &B->flags->updated, pa, comm_stream),
                    "wait kernel");
-        cuda_check(launch_ag_unpack_peer(B->unpack_u, B->unpack_s, B->e_unpack,
+        cuda_check(launch_ag_unpack_peer(B->unpack_u, B->unpack_ps, B->e_unpack,
                                          B->any_shadow ? 1 : 0, pa, B->flags, comm_stream),
                    "ag+unpack kernel");
       } else if (!local && P > 1 && B->stride > 0) {
@@ -717,7 +718,8 @@ int dear_finalize(dear_ctx* ctx) {
   }
   const size_t float_bytes = (floats * sizeof(float) + 255) / 256 * 256;
   const size_t unit_bytes = (units * sizeof(Unit) + 255) / 256 * 256;
-  const size_t n_slices = plan.size() * 3 * static_cast<size_t>(kSlices);
+  const size_t per_bucket_slices = 3 * static_cast<size_t>(kSlices) + 2 * kPeerSlices;
+  const size_t n_slices = plan.size() * per_bucket_slices;
   const size_t slice_bytes = (n_slices * sizeof(Slice) + 255) / 256 * 256;
   // Layout: [bucket buffers + momentum][flags] is identical on every rank (the
   // region peers address through IPC); unit/slice tables (rank-specific)
@@ -788,13 +790,19 @@ int dear_finalize(dear_ctx* ctx) {
     B.n_unpack = static_cast<int>(host_units.size() - static_cast<size_t>(B.unpack_u - up));
     B.e_unpack = set_starts(host_units, static_cast<size_t>(B.unpack_u - up));
     // Equal element slices per CTA for each op (one wave of kSlices CTAs).
-    Slice* hs = host_slices.data() + g * 3 * kSlices;
+    Slice* hs = host_slices.data() + g * per_bucket_slices;
     make_slices(host_units.data() + (B.pack_u - up), B.n_pack, B.e_pack, hs);
     make_slices(host_units.data() + (B.upd_u - up), B.n_upd, B.e_upd, hs + kSlices);
     make_slices(host_units.data() + (B.unpack_u - up), B.n_unpack, B.e_unpack, hs + 2 * kSlices);
-    B.pack_s = sp + g * 3 * kSlices;
+    make_slices(host_units.data() + (B.upd_u - up), B.n_upd, B.e_upd, hs + 3 * kSlices,
+                kPeerSlices);
+    make_slices(host_units.data() + (B.unpack_u - up), B.n_unpack, B.e_unpack,
+                hs + 3 * kSlices + kPeerSlices, kPeerSlices);
+    B.pack_s = sp + g * per_bucket_slices;
     B.upd_s = B.pack_s + kSlices;
     B.unpack_s = B.upd_s + kSlices;
+    B.upd_ps = B.unpack_s + kSlices;
+    B.unpack_ps = B.upd_ps + kPeerSlices;
     B.ag_done = new_event(false);
     for (int k = 0; k < T_COUNT; ++k) B.t[k] = new_event(true);
     B.layers_left = B.high - B.low + 1;

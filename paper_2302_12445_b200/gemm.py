@@ -28,11 +28,20 @@ def _bind():
     L.dear_gemm_run_group.argtypes = [C.POINTER(P), C.c_int32, P]
     L.dear_gemm_plan_info.argtypes = [P] + [C.POINTER(C.c_int32)] * 4
     L.dear_gemm_plan_destroy.argtypes = [P]
+    L.dear_gemm_plan_cluster.argtypes = [P] + [C.POINTER(C.c_int32)] * 3
+    L.dear_gemm_set_trace.argtypes = [P]
     for f in ("dear_gemm_plan_create", "dear_gemm_run", "dear_gemm_run_group",
-              "dear_gemm_plan_info", "dear_gemm_plan_destroy"):
+              "dear_gemm_plan_info", "dear_gemm_plan_cluster", "dear_gemm_set_trace",
+              "dear_gemm_plan_destroy"):
         getattr(L, f).restype = C.c_int
     _bound = True
     return L
+
+
+def set_trace(buf: "torch.Tensor | None") -> None:
+    """Profiling: per-CTA %globaltimer phase stamps of every later launch go to
+    `buf` (int64 CUDA tensor, >= 8 x 148 entries); None disables."""
+    check(_bind().dear_gemm_set_trace(buf.data_ptr() if buf is not None else None))
 
 
 class GemmPlan:
@@ -71,7 +80,11 @@ class GemmPlan:
     def info(self) -> dict:
         v = [C.c_int32() for _ in range(4)]
         check(_bind().dear_gemm_plan_info(self._plan, *[C.byref(x) for x in v]))
-        return dict(zip(("bn", "n_tiles", "m_tiles", "splits"), (x.value for x in v)))
+        out = dict(zip(("bn", "n_tiles", "m_tiles", "splits"), (x.value for x in v)))
+        c = [C.c_int32() for _ in range(3)]
+        check(_bind().dear_gemm_plan_cluster(self._plan, *[C.byref(x) for x in c]))
+        out.update(zip(("cm", "cn", "resident_clusters"), (x.value for x in c)))
+        return out
 
     @property
     def flops(self) -> int:

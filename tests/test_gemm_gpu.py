@@ -6,6 +6,13 @@ import torch
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(params=["cluster", "no-cluster"], autouse=True)
+def cluster_mode(request, monkeypatch):
+    """Every case runs with TMA-multicast clusters (opt-in) and without (default)."""
+    monkeypatch.setenv("DEAR_GEMM_CLUSTER", "1" if request.param == "cluster" else "0")
+    return request.param
+
+
 def _ref(a, b, mn_major):
     bb = b.float().t() if mn_major else b.float()
     return a.float() @ bb.t()

@@ -27,6 +27,9 @@ def main():
     ap.add_argument("--max-mb", type=int, default=256)
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "peer"],
+                    help="peer: fused RS+update / AG+unpack NVLink kernels (times include "
+                         "the update / unpack they fuse)")
     a = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -46,7 +49,7 @@ def main():
         n = size // 4
         p = torch.zeros(n, device="cuda")
         g = torch.ones(n, device="cuda")
-        rt = dear.Runtime(comm, rank, P, policy="DEAR", lr=0.0, stream=s)
+        rt = dear.Runtime(comm, rank, P, policy="DEAR", lr=0.0, stream=s, backend=a.backend)
         rt.register(1, p, g)
         rt.finalize()
         rt.set_timing(True)
@@ -68,7 +71,7 @@ def main():
         dist.all_reduce(t_rs, op=dist.ReduceOp.MAX)
         dist.all_reduce(t_ag, op=dist.ReduceOp.MAX)
         bus = (P - 1) * stride * 4
-        pt = {"bytes": size, "P": P, "rs_ms": t_rs.item(), "ag_ms": t_ag.item(),
+        pt = {"backend": a.backend, "bytes": size, "P": P, "rs_ms": t_rs.item(), "ag_ms": t_ag.item(),
               "rs_busbw_gbs": bus / (t_rs.item() / 1e3) / 1e9,
               "ag_busbw_gbs": bus / (t_ag.item() / 1e3) / 1e9}
         points.append(pt)
@@ -77,7 +80,7 @@ def main():
         size *= 2
     if rank == 0:
         cal = calibrate_alpha_beta([(p["bytes"], (p["rs_ms"] + p["ag_ms"]) / 1e3) for p in points], P)
-        print(json.dumps({"calibration": cal, "P": P,
+        print(json.dumps({"backend": a.backend, "calibration": cal, "P": P,
                           "link_GBps_from_beta": (1 / cal["beta"] / 1e9) if cal["beta"] else None}),
               flush=True)
     comm.close()
