@@ -186,6 +186,12 @@ int dear_set_timing(dear_ctx* ctx, int32_t enable);
  * timed iteration; out is n_buckets x 5 (pack, rs, update, ag, unpack),
  * -1 where a stage did not run. */
 int dear_get_timings(dear_ctx* ctx, float* out, int32_t n_buckets);
+/* Measured timeline of the last timed iteration: for every bucket the
+ * milliseconds from `base_event` (a cudaEvent_t recorded earlier, as void*)
+ * to its 7 comm-stream stamps: pack start, pack end (= RS start), RS end,
+ * update end, AG start, AG end (= unpack start), unpack end; -1 where a stage
+ * did not run. out is n_buckets x 7. */
+int dear_get_timeline(dear_ctx* ctx, void* base_event, float* out, int32_t n_buckets);
 /* Replica check — the GPU analogue of sgd_step's "replica divergence"
  * rejection (collective.cpp:172-181): hashes every registered parameter
  * and compares across ranks. *identical = 1 when all ranks agree. */

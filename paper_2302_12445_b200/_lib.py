@@ -73,6 +73,7 @@ _SIGNATURES = {
     "dear_get_timings": [_P, C.POINTER(C.c_float), C.c_int32],
     "dear_check_replicas": [_P, C.POINTER(C.c_int32)],
     "dear_peer_handle": [_P, C.c_char_p],
+    "dear_get_timeline": [_P, _P, C.POINTER(C.c_float), C.c_int32],
     "dear_peer_connect": [_P, C.c_char_p, C.c_int32],
 }
 

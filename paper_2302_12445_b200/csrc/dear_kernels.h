@@ -42,9 +42,9 @@ constexpr int kSlices = 148 * DEAR_SLICES_PER_SM;
 constexpr int kPeerSlices = 64;
 
 struct Slice {
-  int32_t unit;   // first unit of this CTA's slice
+  Unit first;     // the slice's first piece, pointers pre-offset (one load per CTA)
+  int32_t unit;   // index of that unit; later pieces continue at unit + 1
   int32_t pad;
-  int64_t off;    // offset inside that unit
   int64_t count;  // elements in the slice (multiple of 4 except the last)
 };
 
@@ -71,8 +71,9 @@ cudaError_t launch_unpack(const Unit* units, const Slice* slices, int64_t total,
                           cudaStream_t s);
 // Host: the Slice table (n_slices entries, one per CTA) for a unit list with
 // prefix starts.
+// c_elem_bytes: element size behind Unit::c (4 momentum, 2 bf16 shadow, 0 none).
 void make_slices(const Unit* units, int n_units, int64_t total, Slice* out,
-                 int n_slices = kSlices);
+                 int n_slices, int c_elem_bytes);
 
 // Local-group collectives over P same-device buffers (ring order, in place):
 // rs: bufs[r][r*stride + i] = fold_k bufs[(r+1+k)%P][r*stride + i], k = 0..P-1

@@ -393,16 +393,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         const TileCoord tc = decode(L, t, ci, cj);
         const Problem& P = L.p[tc.prob];
         const int nk = tc.kb1 - tc.kb0;
-        // (uniform within a cluster: multicast pieces of a stage share one k-block)
-#ifdef DEAR_GEMM_NO_ROTATE
-        const int rot = 0;
-#else
-        const int rot = nk > 0 ? (t * 5) % nk : 0;
-#endif
         for (int i = 0; i < nk; ++i, ++g) {
-          // Rotated k order: CTAs sharing an operand tile read different
-          // k-blocks at any moment instead of hammering the same L2 lines.
-          const int kb = tc.kb0 + (i + rot) % nk;
+          const int kb = tc.kb0 + i;
           const int s = g % stages;
           const uint32_t ph = (g / stages) & 1;
           mbar_wait(&empty[s], ph ^ 1);

@@ -140,19 +140,22 @@ __device__ __forceinline__ void run_unit(const float* src, const float* dst, int
   for (int64_t i = head + n4 * 4 + threadIdx.x; i < len; i += kThreads) scalar_fn(i);
 }
 
-// Every CTA walks its equal slice of the op's elements across units.
+// Every CTA walks its equal slice of the op's elements across units. The
+// first piece travels inside the Slice record (pointers already offset), so
+// the common single-unit slice costs one descriptor load.
 template <typename F>
 __device__ __forceinline__ void walk_slice(const Unit* __restrict__ units,
                                            const Slice* __restrict__ slices, F&& f) {
   const Slice sl = slices[blockIdx.x];
-  int64_t left = sl.count;
-  int64_t off = sl.off;
-  for (int u = sl.unit; left > 0; ++u) {
+  if (sl.count <= 0) return;
+  const int64_t n0 = min(sl.first.len, sl.count);
+  f(sl.first, int64_t{0}, n0);
+  int64_t left = sl.count - n0;
+  for (int u = sl.unit + 1; left > 0; ++u) {
     const Unit U = units[u];
-    const int64_t n = min(U.len - off, left);
-    if (n > 0) f(U, off, n);
+    const int64_t n = min(U.len, left);
+    if (n > 0) f(U, int64_t{0}, n);
     left -= n;
-    off = 0;
   }
 }
 
@@ -508,7 +511,8 @@ cudaError_t launch_unpack(const Unit* units, const Slice* slices, int64_t total,
   return cudaGetLastError();
 }
 
-void make_slices(const Unit* units, int n_units, int64_t total, Slice* out, int n_slices) {
+void make_slices(const Unit* units, int n_units, int64_t total, Slice* out, int n_slices,
+                 int c_elem_bytes) {
   int64_t per = (total + n_slices - 1) / n_slices;
   per = (per + 3) / 4 * 4;
   int u = 0;
@@ -516,14 +520,25 @@ void make_slices(const Unit* units, int n_units, int64_t total, Slice* out, int 
   for (int c = 0; c < n_slices; ++c) {
     const int64_t lo = static_cast<int64_t>(c) * per;
     const int64_t cnt = lo >= total ? 0 : (total - lo < per ? total - lo : per);
-    while (u < n_units && base + units[u].len <= lo && cnt > 0) {
+    Slice& sl = out[c];
+    sl = Slice{};
+    sl.count = cnt;
+    if (cnt <= 0) continue;
+    while (u < n_units && base + units[u].len <= lo) {
       base += units[u].len;
       ++u;
     }
-    out[c].unit = cnt > 0 ? u : 0;
-    out[c].pad = 0;
-    out[c].off = cnt > 0 ? lo - base : 0;
-    out[c].count = cnt;
+    const int64_t off = lo - base;
+    const Unit& U = units[u];
+    sl.unit = u;
+    sl.first = U;
+    sl.first.a = U.a ? U.a + off : nullptr;
+    sl.first.b = U.b ? U.b + off : nullptr;
+    // c: momentum (fp32) for update units, bf16 shadow for unpack units.
+    sl.first.c = U.c ? static_cast<void*>(static_cast<char*>(U.c) + off * c_elem_bytes) : nullptr;
+    sl.first.len = U.len - off;
+    sl.first.start = lo;
+    sl.first.pad = static_cast<int32_t>(off & 0x7fffffff);
   }
 }
 

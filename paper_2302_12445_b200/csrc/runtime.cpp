@@ -791,13 +791,14 @@ int dear_finalize(dear_ctx* ctx) {
     B.e_unpack = set_starts(host_units, static_cast<size_t>(B.unpack_u - up));
     // Equal element slices per CTA for each op (one wave of kSlices CTAs).
     Slice* hs = host_slices.data() + g * per_bucket_slices;
-    make_slices(host_units.data() + (B.pack_u - up), B.n_pack, B.e_pack, hs);
-    make_slices(host_units.data() + (B.upd_u - up), B.n_upd, B.e_upd, hs + kSlices);
-    make_slices(host_units.data() + (B.unpack_u - up), B.n_unpack, B.e_unpack, hs + 2 * kSlices);
+    make_slices(host_units.data() + (B.pack_u - up), B.n_pack, B.e_pack, hs, kSlices, 0);
+    make_slices(host_units.data() + (B.upd_u - up), B.n_upd, B.e_upd, hs + kSlices, kSlices, 4);
+    make_slices(host_units.data() + (B.unpack_u - up), B.n_unpack, B.e_unpack, hs + 2 * kSlices,
+                kSlices, 2);
     make_slices(host_units.data() + (B.upd_u - up), B.n_upd, B.e_upd, hs + 3 * kSlices,
-                kPeerSlices);
+                kPeerSlices, 4);
     make_slices(host_units.data() + (B.unpack_u - up), B.n_unpack, B.e_unpack,
-                hs + 3 * kSlices + kPeerSlices, kPeerSlices);
+                hs + 3 * kSlices + kPeerSlices, kPeerSlices, 2);
     B.pack_s = sp + g * per_bucket_slices;
     B.upd_s = B.pack_s + kSlices;
     B.unpack_s = B.upd_s + kSlices;
@@ -1126,6 +1127,27 @@ int dear_get_timings(dear_ctx* ctx, float* out, int32_t n_buckets) {
     o[2] = span(B, T_RS1, T_UPD1);
     o[3] = span(B, T_AG0, T_AG1);
     o[4] = span(B, T_AG1, T_UNPACK1);
+  }
+  DEAR_API_END
+}
+
+int dear_get_timeline(dear_ctx* ctx, void* base_event, float* out, int32_t n_buckets) {
+  DEAR_API_BEGIN
+  need(ctx, true);
+  if (!base_event || !out) invalid("dear_get_timeline: null argument");
+  if (n_buckets != static_cast<int32_t>(ctx->buckets.size()))
+    invalid("dear_get_timeline: bucket count mismatch");
+  cudaEvent_t base = static_cast<cudaEvent_t>(base_event);
+  for (size_t g = 0; g < ctx->buckets.size(); ++g) {
+    const Bucket& B = ctx->buckets[g];
+    for (int k = 0; k < T_COUNT; ++k) {
+      float ms = -1.f;
+      if (B.t_rec[k] && cudaEventElapsedTime(&ms, base, B.t[k]) != cudaSuccess) {
+        (void)cudaGetLastError();
+        ms = -1.f;
+      }
+      out[g * T_COUNT + k] = ms;
+    }
   }
   DEAR_API_END
 }

@@ -212,6 +212,17 @@ class Runtime:
         return [{k: (arr[5 * g + i] if arr[5 * g + i] >= 0 else None)
                  for i, k in enumerate(keys)} for g in range(n)]
 
+    STAMPS = ("pack0", "pack1", "rs1", "update1", "ag0", "ag1", "unpack1")
+
+    def timeline(self, base_event: "torch.cuda.Event") -> list[dict]:
+        """Per bucket: ms from `base_event` to each comm-stream stamp of the last
+        timed iteration (None where the stage did not run)."""
+        n = len(self.buckets())
+        arr = (C.c_float * (7 * n))()
+        check(lib().dear_get_timeline(self._ctx, C.c_void_p(base_event.cuda_event), arr, n))
+        return [{k: (arr[7 * g + i] if arr[7 * g + i] >= 0 else None)
+                 for i, k in enumerate(self.STAMPS)} for g in range(n)]
+
     def check_replicas(self) -> bool:
         ok = C.c_int32(0)
         check(lib().dear_check_replicas(self._ctx, C.byref(ok)))
