@@ -64,6 +64,9 @@ def parse():
     ap.add_argument("--no-ablation", action="store_true", help="skip WFBP / compute-only runs")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--extra-workload", default="bert_large",
+                    help="also measure DeAR vs WFBP on this workload (north-star "
+                         "comparison); 'none' to skip")
     ap.add_argument("--profile-steps", type=int, default=0,
                     help="only run this many graph replays (for ncu launch lists)")
     return ap.parse_args()
@@ -341,6 +344,9 @@ def gpu_arm(a, wl, world, rank, local_rank):
         runc = make_runner(Step(model, None, stream), use_graph, stream)
         res["compute_ms"] = time_loop(runc, a.steps, a.warmup, stream, dist_on)
 
+    extra = None
+    if a.extra_workload != "none" and a.extra_workload != a.workload:
+        extra = compare_policies(a, a.extra_workload, comm, world, rank, stream)
     if rank != 0:
         return None
     samples = batch * world
@@ -398,6 +404,8 @@ def gpu_arm(a, wl, world, rank, local_rank):
                                             res["wfbp_ms"])
     if busbw:
         line["busbw_gbs"] = busbw
+    if extra is not None:
+        line["north_star"] = extra
     if world == 1 and not a.no_cpu:
         line["cpu_baseline"] = reference_arm(a, wl, world, rank, emit=False)
     return line
@@ -453,6 +461,46 @@ def _isolated_stage_times(model, runtime, stream, policy):
     for k in ("pack", "update", "unpack"):
         v = [s[k] for s in st if s[k] is not None]
         out[k] = sum(v) if v else None
+    return out
+
+
+def compare_policies(a, wl_name, comm, world, rank, stream):
+    """DeAR vs WFBP (same kernels, same fusion buffer) and compute-only on a
+    second workload: the north-star comparison (BERT-Large-shaped layers)."""
+    import torch
+
+    import paper_2302_12445_b200 as dear
+    from paper_2302_12445_b200.presets import preset_param_counts
+    from paper_2302_12445_b200.synthetic import SyntheticModel
+
+    wl = WORKLOADS[wl_name]
+    batch = wl["batch"]
+    model = SyntheticModel(preset_param_counts(wl["preset"]), wl["hidden"],
+                           batch * wl["tokens_per_sample"], seed=4321)
+    dist_on = world > 1
+    steps, warm = max(5, a.steps // 2), max(3, a.warmup)
+    out = {"workload": wl["config"], "batch_per_gpu": batch, "fusion_buffer_bytes": a.buffer,
+           "steps": steps, "warmup": warm}
+    for policy in (a.policy, a.baseline_policy):
+        rt = dear.Runtime(comm, rank, world, policy=policy, fusion_buffer_bytes=a.buffer,
+                          lr=a.lr, defer_allgather=True, backend=a.backend, stream=stream)
+        for l in range(1, model.L + 1):
+            rt.register(l, model.params[l - 1], model.grads[l - 1], model.shadows[l - 1])
+        rt.finalize()
+        run = make_runner(Step(model, rt, stream), True, stream)
+        ms = time_loop(run, steps, warm, stream, dist_on)
+        rt.synchronize()
+        rt.close()
+        out[policy] = {"ms_per_step": ms, "samples_per_s": batch * world / (ms / 1e3)}
+    run = make_runner(Step(model, None, stream), True, stream)
+    comp = time_loop(run, steps, warm, stream, dist_on)
+    d, w = out[a.policy]["ms_per_step"], out[a.baseline_policy]["ms_per_step"]
+    out.update({"compute_only_ms": comp, "dear_over_wfbp": w / d,
+                "exposed_comm_pct": max(0.0, 100 * (d - comp) / d),
+                "wfbp_exposed_comm_pct": max(0.0, 100 * (w - comp) / w)})
+    model.close()
+    del model
+    torch.cuda.empty_cache()
     return out
 
 

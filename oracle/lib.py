@@ -158,6 +158,9 @@ class Reference:
         lib.ref_calibrate.argtypes = [_f64p, _f64p, C.c_int, C.c_int, D, D, C.POINTER(C.c_int)]
         lib.ref_costs.argtypes = [C.c_double, C.c_int, C.c_double, C.c_double, D, D]
         lib.ref_theory.argtypes = [C.c_double] * 4 + [C.c_int, D, D, D]
+        lib.ref_gp.argtypes = [_f64p, _f64p, C.c_int, _f64p, C.c_int, _f64p, _f64p, _f64p]
+        lib.ref_tune_quadratic.argtypes = [C.c_double, C.c_double, C.c_double, C.c_int, C.c_int,
+                                           _f64p, _f64p, C.POINTER(C.c_int)]
         self.lib = lib
 
     def _check(self, rc):
@@ -255,6 +258,22 @@ class Reference:
         self._check(self.lib.ref_theory(t_ff, t_bp, t_rs, t_ag, workers, C.byref(d), C.byref(b),
                                         C.byref(s)))
         return {"dear": d.value, "baseline": b.value, "smax": s.value}
+
+    def gp(self, obs, queries):
+        xb = np.ascontiguousarray([o[0] for o in obs], np.float64)
+        ty = np.ascontiguousarray([o[1] for o in obs], np.float64)
+        q = np.ascontiguousarray(queries, np.float64)
+        m, v, e = (np.zeros(len(q)) for _ in range(3))
+        self._check(self.lib.ref_gp(xb, ty, len(xb), q, len(q), m, v, e))
+        return m, v, e
+
+    def tune_quadratic(self, opt_mb, width_mb, peak, max_trials=20, measure_steps=1):
+        b = np.zeros(max_trials + 2)
+        t = np.zeros(max_trials + 2)
+        n = C.c_int(0)
+        self._check(self.lib.ref_tune_quadratic(opt_mb, width_mb, peak, max_trials,
+                                                measure_steps, b, t, C.byref(n)))
+        return b[:n.value].copy(), t[:n.value].copy()
 
     def time_sgd_steps(self, bucket_elems, P: int, threads: int, steps: int,
                        seed: int = 1, lr: float = 0.05) -> np.ndarray:

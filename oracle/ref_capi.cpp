@@ -23,6 +23,8 @@
 
 #include "dearsim/analysis.hpp"
 #include "dearsim/cost_model.hpp"
+#include "dearsim/gp.hpp"
+#include "dearsim/tuner.hpp"
 #include "dearsim/collective.hpp"
 #include "dearsim/fusion.hpp"
 #include "dearsim/model.hpp"
@@ -288,6 +290,50 @@ int ref_costs(double bytes, int workers, double alpha, double beta, double* rs, 
     const ClusterSpec c{"capi", workers, alpha, beta};
     *rs = reduce_scatter_time(bytes, c);
     *ar = all_reduce_time(bytes, c);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+// gp_fit + predict (gp.cpp:46-158) and expected_improvement (:172-183) on
+// caller observations; defaults of GpHyperParams / TunerConfig bounds.
+int ref_gp(const double* xb, const double* ty, int n, const double* q, int m, double* mean,
+           double* var, double* ei) {
+  try {
+    std::vector<Observation> obs;
+    for (int i = 0; i < n; ++i) obs.push_back({xb[i], ty[i], 1});
+    const GpPosterior gp = gp_fit(obs, GpHyperParams{}, 1e6, 1e8);
+    for (int j = 0; j < m; ++j) {
+      const auto p = gp.predict(q[j]);
+      mean[j] = p.mean;
+      var[j] = p.variance;
+      ei[j] = expected_improvement(gp, q[j], gp.best_throughput(), 0.1);
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+// tune (tuner.cpp:176-203) on the analytic objective
+// peak - ((x/1e6 - opt_mb) / width_mb)^2; writes the trial trace.
+int ref_tune_quadratic(double opt_mb, double width_mb, double peak, int max_trials,
+                       int measure_steps, double* buffers, double* thr, int* n) {
+  try {
+    TunerConfig cfg;
+    cfg.max_trials = max_trials;
+    cfg.measure_steps = measure_steps;
+    auto obj = [&](double x) {
+      const double r = (x / 1e6 - opt_mb) / width_mb;
+      return peak - r * r;
+    };
+    const TuneResult res = tune(obj, cfg);
+    *n = static_cast<int>(res.trace.size());
+    for (size_t i = 0; i < res.trace.size(); ++i) {
+      buffers[i] = res.trace[i].buffer_bytes;
+      thr[i] = res.trace[i].throughput;
+    }
     return 0;
   } catch (const std::exception& e) {
     return fail(e);

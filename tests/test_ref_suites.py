@@ -8,7 +8,8 @@ import pytest
 
 REF = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref")
 SUITES = {"test_collective": 47656, "test_model_fusion": 2464, "test_task_graph": 83,
-          "test_simulate": 602, "test_cost_model": 2939, "test_analysis": 3776}
+          "test_simulate": 602, "test_cost_model": 2939, "test_analysis": 3776,
+          "test_gp": 1102, "test_tuner": 146}
 
 
 @pytest.mark.parametrize("suite", sorted(SUITES))
