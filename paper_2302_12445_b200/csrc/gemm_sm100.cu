@@ -645,7 +645,14 @@ void launch(const dear::gemm::Launch& L, cudaStream_t stream) {
   using namespace dear::gemm;
   set_smem_attr();
   const int csize = L.cm * L.cn;
-  const int clusters = std::min(L.total_tiles, dear::gemm::max_active_clusters(csize));
+  // DEAR_GEMM_MAX_CTAS caps the persistent grid (leaves SMs to comm kernels).
+  static const int cap = [] {
+    const char* e = std::getenv("DEAR_GEMM_MAX_CTAS");
+    return e ? std::atoi(e) : 0;
+  }();
+  int resident = dear::gemm::max_active_clusters(csize);
+  if (cap > 0) resident = std::max(1, std::min(resident, cap / csize));
+  const int clusters = std::min(L.total_tiles, resident);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(clusters * csize));
   cfg.blockDim = dim3(kThreads);

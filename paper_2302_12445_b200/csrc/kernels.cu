@@ -15,6 +15,8 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 
+#include <cstdlib>
+
 #include "dear_kernels.h"
 
 namespace dear {
@@ -144,9 +146,7 @@ __device__ __forceinline__ void run_unit(const float* src, const float* dst, int
 // first piece travels inside the Slice record (pointers already offset), so
 // the common single-unit slice costs one descriptor load.
 template <typename F>
-__device__ __forceinline__ void walk_slice(const Unit* __restrict__ units,
-                                           const Slice* __restrict__ slices, F&& f) {
-  const Slice sl = slices[blockIdx.x];
+__device__ __forceinline__ void walk_one(const Unit* __restrict__ units, const Slice& sl, F&& f) {
   if (sl.count <= 0) return;
   const int64_t n0 = min(sl.first.len, sl.count);
   f(sl.first, int64_t{0}, n0);
@@ -157,6 +157,15 @@ __device__ __forceinline__ void walk_slice(const Unit* __restrict__ units,
     if (n > 0) f(U, int64_t{0}, n);
     left -= n;
   }
+}
+
+// Each CTA walks slices blockIdx.x, blockIdx.x + gridDim.x, ... of the op's
+// n_slices equal slices (one slice per CTA at the full grid).
+template <typename F>
+__device__ __forceinline__ void walk_slice(const Unit* __restrict__ units,
+                                           const Slice* __restrict__ slices, int n_slices,
+                                           F&& f) {
+  for (int i = blockIdx.x; i < n_slices; i += gridDim.x) walk_one(units, slices[i], f);
 }
 
 // ------------------------------------------------------ peer signalling ----
@@ -205,7 +214,7 @@ template <bool kSignal>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm) pack_kernel(const Unit* __restrict__ units,
                                                            const Slice* __restrict__ slices,
                                                            float scale, BucketFlags* flags) {
-  walk_slice(units, slices, [&](const Unit& U, int64_t off, int64_t n) {
+  walk_slice(units, slices, kSlices, [&](const Unit& U, int64_t off, int64_t n) {
     const float* src = U.a + off;
     float* dst = U.b + off;
     run_unit<Hint::kStream>(
@@ -245,7 +254,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) update_kernel(const Unit
                                                              const HyperParams* __restrict__ hpp,
                                                              int has_buf) {
   const HyperParams hp = *hpp;
-  walk_slice(units, slices, [&](const Unit& U, int64_t off, int64_t n) {
+  walk_slice(units, slices, kSlices, [&](const Unit& U, int64_t off, int64_t n) {
     const float* w = U.a + off;
     float* g = U.b + off;
     float* mom = kMom ? static_cast<float*>(U.c) + off : nullptr;
@@ -275,7 +284,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) update_kernel(const Unit
 template <bool kShadow>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm) unpack_kernel(const Unit* __restrict__ units,
                                                              const Slice* __restrict__ slices) {
-  walk_slice(units, slices, [&](const Unit& U, int64_t off, int64_t n) {
+  walk_slice(units, slices, kSlices, [&](const Unit& U, int64_t off, int64_t n) {
     const float* src = U.a + off;
     float* dst = U.b + off;
     __nv_bfloat16* sh = (kShadow && U.c) ? static_cast<__nv_bfloat16*>(U.c) + off : nullptr;
@@ -311,7 +320,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
                           BucketFlags* flags) {
   const HyperParams hp = *hpp;
   const int k0 = (pa.rank + 1) % pa.P;
-  walk_slice(units, slices, [&](const Unit& U, int64_t off, int64_t n) {
+  walk_slice(units, slices, kPeerSlices, [&](const Unit& U, int64_t off, int64_t n) {
     const float* w = U.a + off;
     float* g = U.b + off;
     float* mom = kMom ? static_cast<float*>(U.c) + off : nullptr;
@@ -361,7 +370,7 @@ template <bool kShadow>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     ag_unpack_peer_kernel(const Unit* __restrict__ units, const Slice* __restrict__ slices,
                           PeerArgs pa, BucketFlags* flags) {
-  walk_slice(units, slices, [&](const Unit& U, int64_t off, int64_t n) {
+  walk_slice(units, slices, kPeerSlices, [&](const Unit& U, int64_t off, int64_t n) {
     const float* src = at_peer(U.a + off, pa.delta[U.peer]);
     float* dst = U.b + off;
     __nv_bfloat16* sh = (kShadow && U.c) ? static_cast<__nv_bfloat16*>(U.c) + off : nullptr;
@@ -437,19 +446,30 @@ __global__ void hash_kernel(const float* __restrict__ x, int64_t n, uint64_t sal
   if ((threadIdx.x & 31) == 0) atomicAdd(acc, static_cast<unsigned long long>(h));
 }
 
+// Grid of the bucket kernels: kSlices (one slice per CTA) unless
+// DEAR_BUCKET_CTAS caps it (CTAs then walk several slices), which leaves SMs
+// to concurrently running GEMMs.
+int bucket_grid(int n_slices) {
+  static int cap = [] {
+    const char* e = std::getenv("DEAR_BUCKET_CTAS");
+    return e ? std::atoi(e) : 0;
+  }();
+  return cap > 0 && cap < n_slices ? cap : n_slices;
+}
+
 }  // namespace
 
 cudaError_t launch_pack(const Unit* units, const Slice* slices, int64_t total, float scale,
                         cudaStream_t s) {
   if (total <= 0) return cudaSuccess;
-  pack_kernel<false><<<kSlices, kThreads, 0, s>>>(units, slices, scale, nullptr);
+  pack_kernel<false><<<bucket_grid(kSlices), kThreads, 0, s>>>(units, slices, scale, nullptr);
   return cudaGetLastError();
 }
 
 cudaError_t launch_pack_signal(const Unit* units, const Slice* slices, int64_t total, float scale,
                                BucketFlags* flags, cudaStream_t s) {
   (void)total;  // the signal must fire even for an empty bucket
-  pack_kernel<true><<<kSlices, kThreads, 0, s>>>(units, slices, scale, flags);
+  pack_kernel<true><<<bucket_grid(kSlices), kThreads, 0, s>>>(units, slices, scale, flags);
   return cudaGetLastError();
 }
 
@@ -465,13 +485,13 @@ cudaError_t launch_rs_update_peer(const Unit* units, const Slice* slices, int64_
                                   cudaStream_t s) {
   (void)total;
   if (use_momentum && use_wd)
-    rs_update_peer_kernel<true, true><<<kPeerSlices, kThreads, 0, s>>>(units, slices, hp, has_momentum_buf, pa, flags);
+    rs_update_peer_kernel<true, true><<<bucket_grid(kPeerSlices), kThreads, 0, s>>>(units, slices, hp, has_momentum_buf, pa, flags);
   else if (use_momentum)
-    rs_update_peer_kernel<true, false><<<kPeerSlices, kThreads, 0, s>>>(units, slices, hp, has_momentum_buf, pa, flags);
+    rs_update_peer_kernel<true, false><<<bucket_grid(kPeerSlices), kThreads, 0, s>>>(units, slices, hp, has_momentum_buf, pa, flags);
   else if (use_wd)
-    rs_update_peer_kernel<false, true><<<kPeerSlices, kThreads, 0, s>>>(units, slices, hp, has_momentum_buf, pa, flags);
+    rs_update_peer_kernel<false, true><<<bucket_grid(kPeerSlices), kThreads, 0, s>>>(units, slices, hp, has_momentum_buf, pa, flags);
   else
-    rs_update_peer_kernel<false, false><<<kPeerSlices, kThreads, 0, s>>>(units, slices, hp, has_momentum_buf, pa, flags);
+    rs_update_peer_kernel<false, false><<<bucket_grid(kPeerSlices), kThreads, 0, s>>>(units, slices, hp, has_momentum_buf, pa, flags);
   return cudaGetLastError();
 }
 
@@ -480,9 +500,9 @@ cudaError_t launch_ag_unpack_peer(const Unit* units, const Slice* slices, int64_
                                   cudaStream_t s) {
   (void)total;
   if (with_shadow)
-    ag_unpack_peer_kernel<true><<<kPeerSlices, kThreads, 0, s>>>(units, slices, pa, flags);
+    ag_unpack_peer_kernel<true><<<bucket_grid(kPeerSlices), kThreads, 0, s>>>(units, slices, pa, flags);
   else
-    ag_unpack_peer_kernel<false><<<kPeerSlices, kThreads, 0, s>>>(units, slices, pa, flags);
+    ag_unpack_peer_kernel<false><<<bucket_grid(kPeerSlices), kThreads, 0, s>>>(units, slices, pa, flags);
   return cudaGetLastError();
 }
 
@@ -491,13 +511,13 @@ cudaError_t launch_update(const Unit* units, const Slice* slices, int64_t total,
                           int use_wd, cudaStream_t s) {
   if (total <= 0) return cudaSuccess;
   if (use_momentum && use_wd)
-    update_kernel<true, true><<<kSlices, kThreads, 0, s>>>(units, slices, hp, has_momentum_buf);
+    update_kernel<true, true><<<bucket_grid(kSlices), kThreads, 0, s>>>(units, slices, hp, has_momentum_buf);
   else if (use_momentum)
-    update_kernel<true, false><<<kSlices, kThreads, 0, s>>>(units, slices, hp, has_momentum_buf);
+    update_kernel<true, false><<<bucket_grid(kSlices), kThreads, 0, s>>>(units, slices, hp, has_momentum_buf);
   else if (use_wd)
-    update_kernel<false, true><<<kSlices, kThreads, 0, s>>>(units, slices, hp, has_momentum_buf);
+    update_kernel<false, true><<<bucket_grid(kSlices), kThreads, 0, s>>>(units, slices, hp, has_momentum_buf);
   else
-    update_kernel<false, false><<<kSlices, kThreads, 0, s>>>(units, slices, hp, has_momentum_buf);
+    update_kernel<false, false><<<bucket_grid(kSlices), kThreads, 0, s>>>(units, slices, hp, has_momentum_buf);
   return cudaGetLastError();
 }
 
@@ -505,9 +525,9 @@ cudaError_t launch_unpack(const Unit* units, const Slice* slices, int64_t total,
                           cudaStream_t s) {
   if (total <= 0) return cudaSuccess;
   if (with_shadow)
-    unpack_kernel<true><<<kSlices, kThreads, 0, s>>>(units, slices);
+    unpack_kernel<true><<<bucket_grid(kSlices), kThreads, 0, s>>>(units, slices);
   else
-    unpack_kernel<false><<<kSlices, kThreads, 0, s>>>(units, slices);
+    unpack_kernel<false><<<bucket_grid(kSlices), kThreads, 0, s>>>(units, slices);
   return cudaGetLastError();
 }
 
