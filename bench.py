@@ -59,8 +59,9 @@ def parse():
     ap.add_argument("--lr", type=float, default=0.05)
     ap.add_argument("--momentum", type=float, default=0.0)
     ap.add_argument("--no-graph", action="store_true")
-    ap.add_argument("--backend", default="nccl", choices=["nccl", "peer"],
-                    help="bucket collectives: NCCL RS/AG, or fused NVLink peer kernels")
+    ap.add_argument("--backend", default="auto", choices=["auto", "nccl", "peer"],
+                    help="bucket collectives: fused NVLink peer kernels (auto when N > 1) "
+                         "or NCCL RS/AG")
     ap.add_argument("--no-ablation", action="store_true", help="skip WFBP / compute-only runs")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -292,6 +293,7 @@ def gpu_arm(a, wl, world, rank, local_rank):
     res = {}
     # --- headline: DeAR, inputs resident ---------------------------------
     rt = runtime(a.policy)
+    backend_used = rt.backend
     buckets = rt.buckets()
     run = make_runner(Step(model, rt, stream), use_graph, stream)
     if a.profile_steps:
@@ -377,7 +379,7 @@ def gpu_arm(a, wl, world, rank, local_rank):
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": res["dear_ms"],
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic",
-        "config": {"workload": wl["config"], "policy": a.policy, "collectives": a.backend,
+        "config": {"workload": wl["config"], "policy": a.policy, "collectives": backend_used,
                    "fusion_buffer_bytes": a.buffer, "buckets": len(buckets),
                    "batch_per_gpu": batch, "global_batch": samples, "tokens_per_gpu": tokens,
                    "hidden": wl["hidden"], "params": D, "cuda_graph": use_graph,

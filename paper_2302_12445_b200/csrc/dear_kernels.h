@@ -62,13 +62,14 @@ struct HyperParams {
 
 // Launchers (stream-ordered, no host sync). n_units may be 0; total is the
 // sum of the units' lengths.
+// `grid` <= kSlices CTAs (each walks slices blockIdx.x, +grid, ...); 0 = kSlices.
 cudaError_t launch_pack(const Unit* units, const Slice* slices, int64_t total, float scale,
-                        cudaStream_t s);
+                        int grid, cudaStream_t s);
 cudaError_t launch_update(const Unit* units, const Slice* slices, int64_t total,
                           const HyperParams* hp, int has_momentum_buf, int use_momentum,
-                          int use_wd, cudaStream_t s);
+                          int use_wd, int grid, cudaStream_t s);
 cudaError_t launch_unpack(const Unit* units, const Slice* slices, int64_t total, int with_shadow,
-                          cudaStream_t s);
+                          int grid, cudaStream_t s);
 // Host: the Slice table (n_slices entries, one per CTA) for a unit list with
 // prefix starts.
 // c_elem_bytes: element size behind Unit::c (4 momentum, 2 bf16 shadow, 0 none).
@@ -111,7 +112,7 @@ cudaError_t launch_wait_peers(const uint32_t* mine, const uint32_t* watch, const
                               cudaStream_t s);
 // pack with a completion signal (flags->packed += 1 after all CTAs finish).
 cudaError_t launch_pack_signal(const Unit* units, const Slice* slices, int64_t total, float scale,
-                               BucketFlags* flags, cudaStream_t s);
+                               BucketFlags* flags, int grid, cudaStream_t s);
 // Fused reduce-scatter + shard SGD update: for each own-shard element, sum the
 // peers' slot-`rank` values in ring order (rank+1, ..., rank), update, write
 // w' into the own slot; then flags->updated += 1.

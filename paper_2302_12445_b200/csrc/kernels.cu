@@ -449,27 +449,28 @@ __global__ void hash_kernel(const float* __restrict__ x, int64_t n, uint64_t sal
 // Grid of the bucket kernels: kSlices (one slice per CTA) unless
 // DEAR_BUCKET_CTAS caps it (CTAs then walk several slices), which leaves SMs
 // to concurrently running GEMMs.
-int bucket_grid(int n_slices) {
+int bucket_grid(int n_slices, int want = 0) {
   static int cap = [] {
     const char* e = std::getenv("DEAR_BUCKET_CTAS");
     return e ? std::atoi(e) : 0;
   }();
-  return cap > 0 && cap < n_slices ? cap : n_slices;
+  const int g = cap > 0 ? cap : want;
+  return g > 0 && g < n_slices ? g : n_slices;
 }
 
 }  // namespace
 
 cudaError_t launch_pack(const Unit* units, const Slice* slices, int64_t total, float scale,
-                        cudaStream_t s) {
+                        int grid, cudaStream_t s) {
   if (total <= 0) return cudaSuccess;
-  pack_kernel<false><<<bucket_grid(kSlices), kThreads, 0, s>>>(units, slices, scale, nullptr);
+  pack_kernel<false><<<bucket_grid(kSlices, grid), kThreads, 0, s>>>(units, slices, scale, nullptr);
   return cudaGetLastError();
 }
 
 cudaError_t launch_pack_signal(const Unit* units, const Slice* slices, int64_t total, float scale,
-                               BucketFlags* flags, cudaStream_t s) {
+                               BucketFlags* flags, int grid, cudaStream_t s) {
   (void)total;  // the signal must fire even for an empty bucket
-  pack_kernel<true><<<bucket_grid(kSlices), kThreads, 0, s>>>(units, slices, scale, flags);
+  pack_kernel<true><<<bucket_grid(kSlices, grid), kThreads, 0, s>>>(units, slices, scale, flags);
   return cudaGetLastError();
 }
 
@@ -508,26 +509,28 @@ cudaError_t launch_ag_unpack_peer(const Unit* units, const Slice* slices, int64_
 
 cudaError_t launch_update(const Unit* units, const Slice* slices, int64_t total,
                           const HyperParams* hp, int has_momentum_buf, int use_momentum,
-                          int use_wd, cudaStream_t s) {
+                          int use_wd, int grid, cudaStream_t s) {
   if (total <= 0) return cudaSuccess;
+  const int ug = bucket_grid(kSlices, grid);
   if (use_momentum && use_wd)
-    update_kernel<true, true><<<bucket_grid(kSlices), kThreads, 0, s>>>(units, slices, hp, has_momentum_buf);
+    update_kernel<true, true><<<ug, kThreads, 0, s>>>(units, slices, hp, has_momentum_buf);
   else if (use_momentum)
-    update_kernel<true, false><<<bucket_grid(kSlices), kThreads, 0, s>>>(units, slices, hp, has_momentum_buf);
+    update_kernel<true, false><<<ug, kThreads, 0, s>>>(units, slices, hp, has_momentum_buf);
   else if (use_wd)
-    update_kernel<false, true><<<bucket_grid(kSlices), kThreads, 0, s>>>(units, slices, hp, has_momentum_buf);
+    update_kernel<false, true><<<ug, kThreads, 0, s>>>(units, slices, hp, has_momentum_buf);
   else
-    update_kernel<false, false><<<bucket_grid(kSlices), kThreads, 0, s>>>(units, slices, hp, has_momentum_buf);
+    update_kernel<false, false><<<ug, kThreads, 0, s>>>(units, slices, hp, has_momentum_buf);
   return cudaGetLastError();
 }
 
 cudaError_t launch_unpack(const Unit* units, const Slice* slices, int64_t total, int with_shadow,
-                          cudaStream_t s) {
+                          int grid, cudaStream_t s) {
   if (total <= 0) return cudaSuccess;
+  const int ug = bucket_grid(kSlices, grid);
   if (with_shadow)
-    unpack_kernel<true><<<bucket_grid(kSlices), kThreads, 0, s>>>(units, slices);
+    unpack_kernel<true><<<ug, kThreads, 0, s>>>(units, slices);
   else
-    unpack_kernel<false><<<bucket_grid(kSlices), kThreads, 0, s>>>(units, slices);
+    unpack_kernel<false><<<ug, kThreads, 0, s>>>(units, slices);
   return cudaGetLastError();
 }
 

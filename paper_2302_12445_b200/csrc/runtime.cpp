@@ -35,6 +35,19 @@
 namespace dear {
 
 namespace {
+
+// SMs of the (single) device this process drives; the peer-path pack runs one
+// CTA per SM.
+int sm_count() {
+  static const int n = [] {
+    int d = 0, v = 0;
+    if (cudaGetDevice(&d) != cudaSuccess ||
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d) != cudaSuccess || v <= 0)
+      v = 148;
+    return v;
+  }();
+  return n;
+}
 thread_local std::string g_last_error;
 }
 
@@ -364,11 +377,14 @@ void dear_ctx::exec(const Op& op) {
         // Our buffer may be rewritten only once every peer gathered from it.
         cuda_check(launch_wait_peers(&B->flags->packed, &B->flags->gathered, pa, comm_stream),
                    "wait kernel");
+        // One CTA per SM: the pack overlaps backprop GEMMs and the fused peer
+        // kernels; a full 4-CTA/SM grid would hold every SM's register file
+        // and stall the persistent GEMM (profiles/r01_n4_interference_matrix.log).
         cuda_check(launch_pack_signal(B->pack_u, B->pack_s, B->e_pack, pack_scale, B->flags,
-                                      comm_stream),
+                                      sm_count(), comm_stream),
                    "pack kernel");
       } else {
-        cuda_check(launch_pack(B->pack_u, B->pack_s, B->e_pack, pack_scale, comm_stream),
+        cuda_check(launch_pack(B->pack_u, B->pack_s, B->e_pack, pack_scale, 0, comm_stream),
                    "pack kernel");
       }
       cuda_check(cudaEventRecord(packed_ev, comm_stream), "cudaEventRecord");
@@ -395,7 +411,7 @@ void dear_ctx::exec(const Op& op) {
     case OP_UPDATE:
       if (peer) break;
       cuda_check(launch_update(B->upd_u, B->upd_s, B->e_upd, hp_dev, B->mom_init ? 1 : 0,
-                               cfg.momentum != 0.0, cfg.weight_decay != 0.0, comm_stream),
+                               cfg.momentum != 0.0, cfg.weight_decay != 0.0, 0, comm_stream),
                  "update kernel");
       if (cfg.momentum != 0.0) B->mom_init = true;
       record_t(op.bucket, T_UPD1);
@@ -418,7 +434,7 @@ void dear_ctx::exec(const Op& op) {
       break;
     case OP_UNPACK:
       if (peer) break;
-      cuda_check(launch_unpack(B->unpack_u, B->unpack_s, B->e_unpack, B->any_shadow ? 1 : 0,
+      cuda_check(launch_unpack(B->unpack_u, B->unpack_s, B->e_unpack, B->any_shadow ? 1 : 0, 0,
                                comm_stream),
                  "unpack kernel");
       record_t(op.bucket, T_UNPACK1);

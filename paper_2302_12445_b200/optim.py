@@ -36,7 +36,7 @@ class DistOptim:
     def __init__(self, optimizer: torch.optim.Optimizer, model: Optional[torch.nn.Module] = None,
                  *, comm=None, rank: int = 0, policy: str = "DEAR_FUSED",
                  fusion_buffer_bytes: int = 25_000_000, defer_allgather: bool = False,
-                 stream: Optional[torch.cuda.Stream] = None):
+                 backend: str = "auto", stream: Optional[torch.cuda.Stream] = None):
         if not isinstance(optimizer, torch.optim.SGD):
             raise TypeError("DistOptim supports torch.optim.SGD (the reference's update rule)")
         if len(optimizer.param_groups) != 1:
@@ -65,7 +65,8 @@ class DistOptim:
                                dampening=float(g.get("dampening", 0.0)),
                                weight_decay=float(g.get("weight_decay", 0.0)),
                                nesterov=bool(g.get("nesterov", False)),
-                               defer_allgather=defer_allgather, stream=stream)
+                               defer_allgather=defer_allgather, backend=backend,
+                               stream=stream)
         self._layer_of = {}
         self._grad_ptr = {}
         for layer, p in enumerate(params, start=1):

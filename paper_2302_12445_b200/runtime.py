@@ -23,6 +23,12 @@ import torch
 from ._lib import POLICIES, DearCfg, check, lib
 
 
+def _dist_ready() -> bool:
+    import torch.distributed as dist
+
+    return dist.is_available() and dist.is_initialized()
+
+
 def _stream_ptr(stream: Optional[torch.cuda.Stream]) -> int:
     if stream is None:
         stream = torch.cuda.current_stream()
@@ -97,12 +103,17 @@ class Runtime:
                  lr: float = 0.05, momentum: float = 0.0, dampening: float = 0.0,
                  weight_decay: float = 0.0, nesterov: bool = False,
                  dear_group_dependency: bool = False, defer_allgather: bool = False,
-                 backend: str = "nccl", stream: Optional[torch.cuda.Stream] = None):
+                 backend: str = "auto", stream: Optional[torch.cuda.Stream] = None):
         if policy not in POLICIES:
             raise ValueError(f"unknown policy kind {policy!r}; expected one of "
                              f"{', '.join(POLICIES)}")
-        if backend not in ("nccl", "peer"):
-            raise ValueError("backend must be 'nccl' or 'peer'")
+        if backend not in ("auto", "nccl", "peer"):
+            raise ValueError("backend must be 'auto', 'nccl' or 'peer'")
+        if backend == "auto":
+            # The NVLink peer path (fused RS+update / AG+unpack kernels) when
+            # several processes share torch.distributed; NCCL otherwise.
+            backend = "peer" if (isinstance(comm, Communicator) and comm.world_size > 1
+                                 and _dist_ready()) else "nccl"
         if backend == "peer" and isinstance(comm, LocalGroup):
             raise ValueError("the peer backend needs one process per GPU (not a LocalGroup)")
         self.policy = policy

@@ -33,7 +33,7 @@ def close(a, b, tol=1e-5):
     return bool(np.all(np.abs(a - b) <= tol * np.maximum(1.0, np.abs(b))))
 
 
-def run_runtime(comm, rank, P, policy, buf, steps, lr, backend="nccl", **kw):
+def run_runtime(comm, rank, P, policy, buf, steps, lr, backend="nccl", **kw):  # explicit
     o = Restated()
     numels = RAGGED
     offs = np.concatenate([[0], np.cumsum(numels)]).astype(np.int64)
