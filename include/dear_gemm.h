@@ -47,6 +47,21 @@ int dear_gemm_plan_info(dear_gemm_plan* plan, int32_t* bn, int32_t* n_tiles, int
 /* Cluster shape (cm x cn CTAs sharing operands by TMA multicast) and how
  * many such clusters are resident at once. */
 int dear_gemm_plan_cluster(dear_gemm_plan* plan, int32_t* cm, int32_t* cn, int32_t* resident);
+/* Plan flags (dear_gemm_plan_set_flags).
+ * DEAR_GEMM_EARLY_OPERANDS: the caller guarantees A and B are not written by
+ * any kernel that may still be running when this GEMM starts (e.g. operands
+ * that stay read-only across a chain of GEMM launches on the stream). The
+ * GEMM then streams its operands while the preceding kernel drains under
+ * programmatic dependent launch; D is still touched only after it completes. */
+#define DEAR_GEMM_EARLY_OPERANDS 1
+/* Override the cost model's tile choice: bn (multiple of 16, <= 256) and
+ * single-CTA (pair = 0) or 2-CTA pair (pair = 1) tiles; multicast clusters
+ * off. Used by the plan-time autotuner (paper_2302_12445_b200.gemm.autotune). */
+int dear_gemm_plan_set_tile(dear_gemm_plan* plan, int32_t bn, int32_t pair);
+int dear_gemm_plan_set_flags(dear_gemm_plan* plan, int32_t flags);
+/* 1 when the plan runs as 2-CTA pairs (cta_group::2 MMAs on 256-row tiles;
+ * reported by dear_gemm_plan_cluster as cm = 2, cn = 1), else 0. */
+int dear_gemm_plan_pair(dear_gemm_plan* plan, int32_t* pair);
 /* Profiling: when set, every subsequent launch writes 8 %globaltimer stamps
  * per CTA into this device buffer (CTA start, prologue done, dependency
  * released, first stage landed, last MMA issued, epilogue done, CTA end);

@@ -76,6 +76,15 @@ struct alignas(64) Problem {
   int32_t mg_tiles, ng_tiles;  // cluster tiles along M / N
   int32_t a_rows;              // 128 / cn
   int32_t b_rows;              // K-major: bn / cm rows; MN-major: 64 / cm k-rows per box
+  // CTA pair (cta_group::2): the two CTAs of a 2-CTA cluster compute one
+  // 256 x bn tile with M=256 MMAs issued by the even CTA; each CTA fetches its
+  // 128 rows of A and half (bn/2) of B, the MMA reads the other half from the
+  // peer SM. Encoded as cm = 2, cn = 1 (CTA rank = row half), no multicast.
+  int32_t pair;
+  // Caller guarantees A and B are not written by kernels that can still be
+  // running when this GEMM starts (dear_gemm_plan_set_flags): the producer
+  // then streams operands before griddepcontrol.wait; only stores wait.
+  int32_t early_operands;
 };
 
 struct Launch {
@@ -85,6 +94,8 @@ struct Launch {
   int32_t stages;       // smem ring depth (narrow B tiles -> deeper ring)
   int32_t stage_bytes;  // A (16 KB) + widest B of the problems, 1 KB aligned
   int32_t cm, cn;       // cluster shape shared by the problems of the launch
+  int32_t pair;         // CTA-pair (cta_group::2) launch
+  int32_t early;        // every problem has early_operands
   uint64_t* trace;      // optional per-CTA phase timestamps (profiling), or null
 };
 
@@ -122,6 +133,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
   } while (!ok);
 }
+
+// Profiling variant (-DDEAR_GEMM_WAITPROF): accumulate the cycles a role spends
+// blocked in mbar_wait, to tell a data-starved MMA issuer from a full ring.
+#ifdef DEAR_GEMM_WAITPROF
+#define WAIT_T(acc, bar, ph)             \
+  do {                                   \
+    const long long t0_ = clock64();     \
+    mbar_wait(bar, ph);                  \
+    acc += clock64() - t0_;              \
+  } while (0)
+#else
+#define WAIT_T(acc, bar, ph) mbar_wait(bar, ph)
+#endif
 
 __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst,
                                             int32_t c0, int32_t c1) {
@@ -203,6 +227,48 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
       "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
           smem_u32(bar))
       : "memory");
+}
+
+// ---- CTA-pair (cta_group::2) variants -------------------------------------
+// Shared::cluster address of `p`'s counterpart in CTA `rank` of the cluster.
+__device__ __forceinline__ uint32_t mapa_shared(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+
+// TMA into this CTA's smem, completing on an mbarrier of either pair CTA.
+__device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* map, uint32_t bar_cluster,
+                                                 void* dst, int32_t c0, int32_t c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ void umma2_bf16(uint32_t tmem_d, uint64_t a, uint64_t b,
+                                           uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accum));
+}
+
+// Arrive (when the issued MMAs complete) on the barrier at `bar`'s offset in
+// both CTAs of the pair.
+__device__ __forceinline__ void umma2_commit_both(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"(static_cast<uint16_t>(3))
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster)
+               : "memory");
 }
 
 __device__ __forceinline__ void tc_fence_after() {
@@ -321,6 +387,10 @@ __device__ __forceinline__ TileCoord decode(const Launch& L, int t, int ci, int 
   return c;
 }
 
+// kPair: 2-CTA clusters issuing cta_group::2 MMAs (see Problem::pair); every
+// tcgen05 instruction of a kernel must use the same cta_group, hence a
+// separate instantiation.
+template <bool kPair>
 __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant__ Launch L) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -335,15 +405,18 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int csize = L.cm * L.cn;
+  const int csize = kPair ? 2 : L.cm * L.cn;
   const int crank = csize > 1 ? static_cast<int>(cluster_ctarank()) : 0;
-  const int ci = crank / L.cn, cj = crank % L.cn;
+  const int ci = kPair ? crank : crank / L.cn, cj = kPair ? 0 : crank % L.cn;
+  const bool leader = !kPair || crank == 0;
   const int cid = csize > 1 ? static_cast<int>(cluster_id_x()) : static_cast<int>(blockIdx.x);
   const int ncl = csize > 1 ? static_cast<int>(n_clusters_x()) : static_cast<int>(gridDim.x);
   // CTAs sharing this CTA's A tile (same row) and B tile (same column).
   uint16_t row_mask = 0, col_mask = 0;
-  for (int j = 0; j < L.cn; ++j) row_mask |= static_cast<uint16_t>(1u << (ci * L.cn + j));
-  for (int i = 0; i < L.cm; ++i) col_mask |= static_cast<uint16_t>(1u << (i * L.cn + cj));
+  if (!kPair) {
+    for (int j = 0; j < L.cn; ++j) row_mask |= static_cast<uint16_t>(1u << (ci * L.cn + j));
+    for (int i = 0; i < L.cm; ++i) col_mask |= static_cast<uint16_t>(1u << (i * L.cn + cj));
+  }
 
   uint64_t* tr = L.trace ? L.trace + blockIdx.x * 8 : nullptr;
   if (tr && threadIdx.x == 0) tr[0] = globaltimer();  // CTA start
@@ -353,12 +426,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], 1);
-      // released by every CTA this CTA multicasts into (its row and column)
-      mbar_init(&empty[s], static_cast<uint32_t>(L.cm + L.cn - 1));
+      // pair: released by the leader's MMA commit; clusters: by every CTA this
+      // CTA multicasts into (its row and column)
+      mbar_init(&empty[s], kPair ? 1u : static_cast<uint32_t>(L.cm + L.cn - 1));
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tmem_full[a], 1);
-      mbar_init(&tmem_empty[a], 4);
+      mbar_init(&tmem_empty[a], kPair ? 8 : 4);  // pair: both CTAs' epilogue warps
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int i = 0; i < L.n_problems; ++i) {
@@ -369,23 +443,33 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     }
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "r"(kTmemCols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if (kPair) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "r"(kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "r"(kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   tc_fence_before();
   if (csize > 1)
-    cluster_sync();  // peers' barriers are initialised before any multicast
+    cluster_sync();  // peers' barriers are initialised before any remote arrive
   else
     __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   if (tr && threadIdx.x == 0) tr[1] = globaltimer();  // prologue done
-  // Everything above overlaps the previous kernel; memory is touched only now.
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  if (tr && threadIdx.x == 0) tr[2] = globaltimer();  // dependency released
+  // Everything above overlaps the previous kernel. Global memory is touched
+  // only after the dependency is released, except operand loads of `early`
+  // launches; the MMA issuer touches no global memory.
+  if (warp >= 2 || (warp == 0 && !L.early)) asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (tr && warp == 2 && lane == 0) tr[2] = globaltimer();  // dependency released
 
+  long long w_acc = 0;  // cycles blocked (profiling variant only)
   if (warp == 0) {
     if (lane == 0) {
       uint32_t g = 0;
@@ -397,11 +481,25 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           const int kb = tc.kb0 + i;
           const int s = g % stages;
           const uint32_t ph = (g / stages) & 1;
-          mbar_wait(&empty[s], ph ^ 1);
-          mbar_expect_tx(&full[s], P.tx_bytes);
+          WAIT_T(w_acc, &empty[s], ph ^ 1);
           const int kc = kb * kBK;
           uint8_t* sA = smem + s * stage_bytes;
           uint8_t* sB = sA + kAStage;
+          if (kPair) {
+            // Both CTAs' bytes land on the leader's full barrier.
+            if (leader) mbar_expect_tx(&full[s], P.tx_bytes);
+            const uint32_t fb = mapa_shared(&full[s], 0);
+            tma_load_2d_pair(&P.tmA, fb, sA, kc, static_cast<int32_t>(tc.m0));
+            const int32_t nh = static_cast<int32_t>(tc.n0) + crank * (P.bn / 2);
+            if (!P.b_mn_major) {
+              tma_load_2d_pair(&P.tmB, fb, sB, kc, nh);
+            } else {
+              for (int j = 0; j < P.b_boxes; ++j)
+                tma_load_2d_pair(&P.tmB, fb, sB + j * 8192, nh + 64 * j, kc);
+            }
+            continue;
+          }
+          mbar_expect_tx(&full[s], P.tx_bytes);
           // A: this CTA's piece (rows cj*a_rows ..) of its row's tile.
           const int32_t am = static_cast<int32_t>(tc.m0) + cj * P.a_rows;
           uint8_t* dA = sA + cj * P.a_rows * 128;
@@ -429,24 +527,37 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           }
         }
       }
+#ifdef DEAR_GEMM_WAITPROF
+      if (tr) tr[4] = w_acc;  // producer: cycles waiting for free stages
+#endif
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    if (lane == 0 && leader) {
+#ifdef DEAR_GEMM_WAITPROF
+      const long long t_loop = clock64();
+#endif
       uint32_t g = 0, j = 0;
       for (int t = cid; t < L.total_tiles; t += ncl, ++j) {
         const TileCoord tc = decode(L, t, ci, cj);
         const Problem& P = L.p[tc.prob];
         const uint32_t acc = j & 1, aph = (j >> 1) & 1;
-        mbar_wait(&tmem_empty[acc], aph ^ 1);
+        long long w_tm = 0;
+        WAIT_T(w_tm, &tmem_empty[acc], aph ^ 1);
+        (void)w_tm;
+#ifdef DEAR_GEMM_WAITPROF
+        if (tr) tr[5] += w_tm;
+#endif
         tc_fence_after();
         const uint32_t d_tmem = tmem + acc * kAccCols;
         const int nk = tc.kb1 - tc.kb0;
         for (int i = 0; i < nk; ++i, ++g) {
           const int s = g % stages;
           const uint32_t ph = (g / stages) & 1;
-          mbar_wait(&full[s], ph);
+          WAIT_T(w_acc, &full[s], ph);
           tc_fence_after();
+#ifndef DEAR_GEMM_WAITPROF
           if (tr && g == 0) tr[3] = globaltimer();  // first stage landed
+#endif
           const uint32_t a_base = smem_u32(smem + s * stage_bytes);
           const uint32_t b_base = a_base + kAStage;
 #pragma unroll
@@ -454,16 +565,29 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             const uint64_t ad = sdesc(a_base + k * 32, 16, 1024);
             const uint64_t bd = P.b_mn_major ? sdesc(b_base + k * 2048, 8192, 1024)
                                              : sdesc(b_base + k * 32, 16, 1024);
-            umma_bf16(d_tmem, ad, bd, P.idesc, (i != 0 || k != 0) ? 1u : 0u);
+            if (kPair)
+              umma2_bf16(d_tmem, ad, bd, P.idesc, (i != 0 || k != 0) ? 1u : 0u);
+            else
+              umma_bf16(d_tmem, ad, bd, P.idesc, (i != 0 || k != 0) ? 1u : 0u);
           }
-          if (csize > 1)
+          if (kPair)
+            umma2_commit_both(&empty[s]);
+          else if (csize > 1)
             umma_commit_mc(&empty[s], static_cast<uint16_t>(row_mask | col_mask));
           else
             umma_commit(&empty[s]);
         }
-        umma_commit(&tmem_full[acc]);
+        if (kPair)
+          umma2_commit_both(&tmem_full[acc]);
+        else
+          umma_commit(&tmem_full[acc]);
       }
+#ifdef DEAR_GEMM_WAITPROF
+      if (tr) tr[7] = clock64() - t_loop;  // MMA issuer: whole loop
+      if (tr) tr[3] = w_acc;  // MMA issuer: cycles waiting for landed stages
+#else
       if (tr) tr[4] = globaltimer();  // last MMA issued
+#endif
     }
     __syncwarp();
   } else {
@@ -485,9 +609,16 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tmem_empty[acc]);
+      if (lane == 0) {
+        if (kPair)
+          mbar_arrive_cluster(mapa_shared(&tmem_empty[acc], 0));
+        else
+          mbar_arrive(&tmem_empty[acc]);
+      }
     }
+#ifndef DEAR_GEMM_WAITPROF
     if (tr && warp == 2 && lane == 0) tr[5] = globaltimer();  // epilogue done
+#endif
   }
   tc_fence_before();
   if (csize > 1)
@@ -497,8 +628,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   if (tr && threadIdx.x == 0) tr[6] = globaltimer();  // CTA end
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"(kTmemCols));
+    if (kPair)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                   "r"(kTmemCols));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                   "r"(kTmemCols));
   }
 }
 
@@ -538,10 +673,10 @@ void make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer
 }
 
 struct TileChoice {
-  int bn, cm, cn;
+  int bn, cm, cn, pair;
 };
 
-int max_active_clusters(int csize);
+int max_active_clusters(int csize, bool pair = false);
 
 // Joint choice of the tile width BN and the cluster shape (cm x cn) for one
 // problem: estimated time = waves x k-blocks x max(MMA cycles, L2->SM operand
@@ -549,33 +684,46 @@ int max_active_clusters(int csize);
 // row (multicast to cn CTAs) and each B tile once per column (to cm CTAs),
 // and a wave is every resident cluster running one cluster tile. Constraints:
 // BN a multiple of 16 (of 8*cm for split B pieces), <= 256.
+// modes: bit 0 single CTAs, bit 1 CTA pairs, bit 2 multicast clusters.
+enum { kModeSingle = 1, kModePair = 2, kModeCluster = 4 };
 TileChoice choose_tiles(int64_t M, int64_t N, int kb_per_tile, int splits, bool mn_major,
-                        bool allow_clusters) {
-  const int64_t m_tiles = (M + kBM - 1) / kBM;
-  const double l2_bytes_per_cycle_per_sm = 42.0;  // LTS cap / 148 SMs (B300_MICROARCH)
-  TileChoice best{256, 1, 1};
+                        int modes) {
+  // Operand bytes an SM can take in per cycle in the mainloop: measured k-block
+  // cadence of 128 x bn tiles on B200 (~0.47 us for 32 KB, tools/gemm_cadence.py,
+  // profiles/r01_gemm_trace.md), i.e. per-SM ingress, not the tensor pipe, bounds
+  // the per-layer shapes.
+  const double ingress = 36.0;
+  TileChoice best{256, 1, 1, 0};
   double best_cost = 1e300;
-  const int shapes[4][2] = {{1, 1}, {2, 1}, {1, 2}, {2, 2}};
+  // {cm, cn, pair}: pair = 2-CTA cta_group::2 tiles of 256 x bn (each SM
+  // fetches 128 rows of A and bn/2 rows of B); cm x cn = multicast clusters.
+  const int shapes[5][3] = {{1, 1, 0}, {1, 1, 1}, {2, 1, 0}, {1, 2, 0}, {2, 2, 0}};
   for (const auto& sh : shapes) {
-    const int cm = sh[0], cn = sh[1];
-    if (!allow_clusters && cm * cn > 1) continue;
+    const int cm = sh[0], cn = sh[1], pair = sh[2];
+    if (pair && !(modes & kModePair)) continue;
+    if (!pair && cm * cn > 1 && !(modes & kModeCluster)) continue;
+    if (!pair && cm * cn == 1 && !(modes & kModeSingle)) continue;
+    const int rows = pair ? 2 * kBM : kBM;  // M per (pair) tile
+    const int64_t m_tiles = (M + rows - 1) / rows;
     if (cm > m_tiles) continue;
-    const int active = max_active_clusters(cm * cn);
+    const int active = pair ? max_active_clusters(2, true) : max_active_clusters(cm * cn);
     for (int bn = 256; bn >= 48; bn -= 16) {
       if (bn % (8 * cm)) continue;
       if (mn_major && 64 % cm) continue;
+      if (pair && mn_major && bn != 128 && bn != 256) continue;  // 64-col boxes per half
       const int64_t n_tiles = (N + bn - 1) / bn;
       if (cn > n_tiles) continue;
       // too-wide tiles waste MMA columns on padding; skip if > 1 tile of slack
       if (n_tiles > 1 && (n_tiles - 1) * bn >= N) continue;
       const int64_t groups = ((m_tiles + cm - 1) / cm) * ((n_tiles + cn - 1) / cn) * splits;
       const int64_t waves = (groups + active - 1) / active;
-      const double mma = 2.0 * bn;  // 4 x (128 x bn / 256) cycles per 64-deep k-block
-      const double mem = (16384.0 / cn + 128.0 * bn / cm) / l2_bytes_per_cycle_per_sm;
+      const double mma = 2.0 * bn;  // per SM: 4 x (128 x bn / 256) cycles per k-block
+      const double mem = pair ? (16384.0 + 64.0 * bn) / ingress
+                              : (16384.0 / cn + 128.0 * bn / cm) / ingress;
       const double cost = waves * (kb_per_tile * std::max(mma, mem) + 1500.0);
       if (cost < best_cost * 0.999) {
         best_cost = cost;
-        best = {bn, cm, cn};
+        best = {bn, cm, cn, pair};
       }
     }
   }
@@ -587,7 +735,56 @@ TileChoice choose_tiles(int64_t M, int64_t N, int kb_per_tile, int splits, bool 
 
 struct dear_gemm_plan {
   dear::gemm::Problem p;
+  const void* A = nullptr;  // creation arguments the tile geometry depends on
+  const void* B = nullptr;
+  int64_t lda = 0, ldb = 0, K = 0;
 };
+
+namespace dear {
+namespace gemm {
+
+// Tile-dependent fields of a plan (BN, pair / cluster shape, TMA boxes).
+void configure(dear_gemm_plan* plan, const TileChoice& tch) {
+  Problem& p = plan->p;
+  const int bn = tch.bn;
+  const bool mn = p.b_mn_major != 0;
+  p.bn = bn;
+  p.n_tiles = static_cast<int32_t>((p.N + bn - 1) / bn);
+  p.pair = tch.pair;
+  const uint32_t mma_m = p.pair ? 2 * kBM : kBM;
+  p.idesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(p.b_mn_major) << 16) |
+            (static_cast<uint32_t>(bn >> 3) << 17) | ((mma_m >> 4) << 24);
+  if (p.pair) {
+    // Per CTA: 128 rows of A and half of B; the leader's barrier counts both.
+    p.b_boxes = mn ? bn / 2 / 64 : 1;
+    p.tx_bytes = 2u * (kAStage + (mn ? p.b_boxes * 8192u : static_cast<uint32_t>(bn / 2) * kBK * 2));
+    p.cm = 2;
+    p.cn = 1;
+    p.a_rows = kBM;
+    p.b_rows = mn ? 64 : bn / 2;
+  } else {
+    p.b_boxes = (bn + 63) / 64;
+    p.tx_bytes = kAStage + (mn ? p.b_boxes * 8192 : static_cast<uint32_t>(bn) * kBK * 2);
+    p.cm = tch.cm;
+    p.cn = tch.cn;
+    p.a_rows = kBM / p.cn;
+    p.b_rows = mn ? 64 / p.cm : bn / p.cm;
+  }
+  p.mg_tiles = (p.m_tiles + p.cm - 1) / p.cm;
+  p.ng_tiles = (p.n_tiles + p.cn - 1) / p.cn;
+  p.tiles = p.mg_tiles * p.ng_tiles * p.splits;  // cluster tiles
+  make_map(&p.tmA, plan->A, static_cast<uint64_t>(plan->K), static_cast<uint64_t>(p.M),
+           static_cast<uint64_t>(plan->lda), kBK, static_cast<uint32_t>(p.a_rows));
+  if (!mn)
+    make_map(&p.tmB, plan->B, static_cast<uint64_t>(plan->K), static_cast<uint64_t>(p.N),
+             static_cast<uint64_t>(plan->ldb), kBK, static_cast<uint32_t>(p.b_rows));
+  else
+    make_map(&p.tmB, plan->B, static_cast<uint64_t>(p.N), static_cast<uint64_t>(plan->K),
+             static_cast<uint64_t>(plan->ldb), 64, static_cast<uint32_t>(p.b_rows));
+}
+
+}  // namespace gemm
+}  // namespace dear
 
 namespace {
 uint64_t* g_trace = nullptr;  // device buffer: 8 timestamps per CTA (profiling only)
@@ -604,20 +801,22 @@ namespace gemm {
 void set_smem_attr() {
   static bool done = false;
   if (!done) {
-    if (cudaFuncSetAttribute(gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kSmemBytes) != cudaSuccess ||
+        cudaFuncSetAttribute(gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              kSmemBytes) != cudaSuccess)
       throw Error(DEAR_EINTERNAL, "cudaFuncSetAttribute(gemm smem)");
-    if (cudaFuncSetAttribute(gemm_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
-        cudaSuccess)
+    if (cudaFuncSetAttribute(gemm_kernel<false>, cudaFuncAttributeNonPortableClusterSizeAllowed,
+                             1) != cudaSuccess)
       (void)cudaGetLastError();
     done = true;
   }
 }
 
-int max_active_clusters(int csize) {
-  static int cache[17] = {0};
+int max_active_clusters(int csize, bool pair) {
+  static int cache[2][17] = {{0}};
   if (csize <= 1) return kSms;
-  if (cache[csize]) return cache[csize];
+  if (cache[pair][csize]) return cache[pair][csize];
   set_smem_attr();
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(csize * (kSms / csize)));
@@ -631,9 +830,13 @@ int max_active_clusters(int csize) {
   cfg.attrs = at;
   cfg.numAttrs = 1;
   int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, gemm_kernel, &cfg) != cudaSuccess || n < 1)
+  if (cudaOccupancyMaxActiveClusters(&n, pair ? gemm_kernel<true> : gemm_kernel<false>, &cfg) !=
+          cudaSuccess ||
+      n < 1) {
+    (void)cudaGetLastError();
     n = kSms / csize / 2;
-  cache[csize] = n;
+  }
+  cache[pair][csize] = n;
   return n;
 }
 }  // namespace gemm
@@ -644,13 +847,13 @@ namespace {
 void launch(const dear::gemm::Launch& L, cudaStream_t stream) {
   using namespace dear::gemm;
   set_smem_attr();
-  const int csize = L.cm * L.cn;
+  const int csize = L.pair ? 2 : L.cm * L.cn;
   // DEAR_GEMM_MAX_CTAS caps the persistent grid (leaves SMs to comm kernels).
   static const int cap = [] {
     const char* e = std::getenv("DEAR_GEMM_MAX_CTAS");
     return e ? std::atoi(e) : 0;
   }();
-  int resident = dear::gemm::max_active_clusters(csize);
+  int resident = dear::gemm::max_active_clusters(csize, L.pair != 0);
   if (cap > 0) resident = std::max(1, std::min(resident, cap / csize));
   const int clusters = std::min(L.total_tiles, resident);
   cudaLaunchConfig_t cfg = {};
@@ -667,7 +870,8 @@ void launch(const dear::gemm::Launch& L, cudaStream_t stream) {
   at[1].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = csize > 1 ? 2 : 1;
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_kernel, L);
+  const cudaError_t e = L.pair ? cudaLaunchKernelEx(&cfg, gemm_kernel<true>, L)
+                               : cudaLaunchKernelEx(&cfg, gemm_kernel<false>, L);
   if (e != cudaSuccess) throw Error(DEAR_EINTERNAL, std::string("gemm launch: ") + cudaGetErrorString(e));
 }
 
@@ -717,12 +921,19 @@ int dear_gemm_plan_create(const void* A, int64_t lda, const void* B, int64_t ldb
   // (profiles/r01_gemm_trace.md).
   const char* env = std::getenv("DEAR_GEMM_CLUSTER");
   const bool clusters = env && env[0] == '1';
-  TileChoice tch = choose_tiles(M, N, kb_per, splits, b_mn_major != 0, clusters);
+  // CTA pairs are on by default (DEAR_GEMM_PAIR=0 disables, =2 forces them).
+  const char* penv = std::getenv("DEAR_GEMM_PAIR");
+  const bool pairs = !(penv && penv[0] == '0');
+  const int modes = (penv && penv[0] == '2')
+                        ? kModePair
+                        : kModeSingle | (pairs ? kModePair : 0) | (clusters ? kModeCluster : 0);
+  TileChoice tch = choose_tiles(M, N, kb_per, splits, b_mn_major != 0, modes);
   if (const char* fb = std::getenv("DEAR_GEMM_BN")) {  // tuning experiments only
     const int v = std::atoi(fb);
-    if (v >= 16 && v <= 256 && v % 16 == 0) tch = {v, 1, 1};
+    if (v >= 16 && v <= 256 && v % 16 == 0 &&
+        !(tch.pair && b_mn_major && v != 128 && v != 256))
+      tch = {v, tch.pair ? 2 : 1, 1, tch.pair};
   }
-  const int bn = tch.bn;
   p.D = D;
   p.ldd = ldd;
   p.M = M;
@@ -731,33 +942,17 @@ int dear_gemm_plan_create(const void* A, int64_t lda, const void* B, int64_t ldb
   p.num_kb = num_kb;
   p.kb_per_split = kb_per;
   p.splits = splits;
-  p.bn = bn;
   p.m_tiles = static_cast<int32_t>(m_tiles);
-  p.n_tiles = static_cast<int32_t>((N + bn - 1) / bn);
   p.b_mn_major = b_mn_major ? 1 : 0;
   p.d_fp32 = d_fp32 ? 1 : 0;
   p.accumulate = accumulate ? 1 : 0;
-  p.idesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(p.b_mn_major) << 16) |
-            (static_cast<uint32_t>(bn >> 3) << 17) | (static_cast<uint32_t>(kBM >> 4) << 24);
-  p.b_boxes = (bn + 63) / 64;
-  p.tx_bytes = kAStage + (b_mn_major ? p.b_boxes * 8192 : static_cast<uint32_t>(bn) * kBK * 2);
-  // Cluster shape from the cost model (DEAR_GEMM_CLUSTER=0 disables clusters).
-  p.cm = tch.cm;
-  p.cn = tch.cn;
-  p.mg_tiles = (p.m_tiles + p.cm - 1) / p.cm;
-  p.ng_tiles = (p.n_tiles + p.cn - 1) / p.cn;
-  p.tiles = p.mg_tiles * p.ng_tiles * splits;  // cluster tiles
-  p.a_rows = kBM / p.cn;
-  p.b_rows = b_mn_major ? 64 / p.cm : bn / p.cm;
+  plan->A = A;
+  plan->B = B;
+  plan->lda = lda;
+  plan->ldb = ldb;
+  plan->K = K;
   try {
-    make_map(&p.tmA, A, static_cast<uint64_t>(K), static_cast<uint64_t>(M),
-             static_cast<uint64_t>(lda), kBK, static_cast<uint32_t>(p.a_rows));
-    if (!b_mn_major)
-      make_map(&p.tmB, B, static_cast<uint64_t>(K), static_cast<uint64_t>(N),
-               static_cast<uint64_t>(ldb), kBK, static_cast<uint32_t>(p.b_rows));
-    else
-      make_map(&p.tmB, B, static_cast<uint64_t>(N), static_cast<uint64_t>(K),
-               static_cast<uint64_t>(ldb), 64, static_cast<uint32_t>(p.b_rows));
+    configure(plan, tch);
   } catch (...) {
     delete plan;
     throw;
@@ -771,7 +966,8 @@ int dear_gemm_run_group(dear_gemm_plan* const* plans, int32_t n, void* stream) {
   using namespace dear::gemm;
   if (!plans || n < 1 || n > kMaxProblems) throw Error(DEAR_EINVAL, "dear_gemm_run_group: 1 or 2 plans");
   if (n == 2 && plans[0] && plans[1] &&
-      (plans[0]->p.cm != plans[1]->p.cm || plans[0]->p.cn != plans[1]->p.cn)) {
+      (plans[0]->p.cm != plans[1]->p.cm || plans[0]->p.cn != plans[1]->p.cn ||
+       plans[0]->p.pair != plans[1]->p.pair)) {
     // Different cluster shapes cannot share a launch.
     const int r0 = dear_gemm_run_group(plans, 1, stream);
     if (r0 != DEAR_OK) return r0;
@@ -786,7 +982,8 @@ int dear_gemm_run_group(dear_gemm_plan* const* plans, int32_t n, void* stream) {
     L.p[i] = plans[i]->p;
     L.total_tiles += plans[i]->p.tiles;
     const Problem& P = plans[i]->p;
-    const int bs = P.b_mn_major ? P.b_boxes * 8192 : (P.bn * kBK * 2 + 1023) / 1024 * 1024;
+    const int b_rows = P.pair ? P.bn / 2 : P.bn;  // pair: this CTA's half of B
+    const int bs = P.b_mn_major ? P.b_boxes * 8192 : (b_rows * kBK * 2 + 1023) / 1024 * 1024;
     b_stage = std::max(b_stage, bs);
   }
   L.stage_bytes = kAStage + b_stage;
@@ -798,6 +995,9 @@ int dear_gemm_run_group(dear_gemm_plan* const* plans, int32_t n, void* stream) {
 #endif
   L.cm = plans[0]->p.cm;
   L.cn = plans[0]->p.cn;
+  L.pair = plans[0]->p.pair;
+  L.early = 1;
+  for (int i = 0; i < n; ++i) L.early &= plans[i]->p.early_operands;
   L.trace = g_trace;
   launch(L, static_cast<cudaStream_t>(stream));
   DEAR_API_END
@@ -823,7 +1023,36 @@ int dear_gemm_plan_cluster(dear_gemm_plan* plan, int32_t* cm, int32_t* cn, int32
   if (!plan) throw Error(DEAR_EINVAL, "null plan");
   if (cm) *cm = plan->p.cm;
   if (cn) *cn = plan->p.cn;
-  if (resident) *resident = dear::gemm::max_active_clusters(plan->p.cm * plan->p.cn);
+  if (resident)
+    *resident = plan->p.pair ? dear::gemm::max_active_clusters(2, true)
+                             : dear::gemm::max_active_clusters(plan->p.cm * plan->p.cn);
+  DEAR_API_END
+}
+
+int dear_gemm_plan_set_tile(dear_gemm_plan* plan, int32_t bn, int32_t pair) {
+  DEAR_API_BEGIN
+  using namespace dear::gemm;
+  if (!plan) throw Error(DEAR_EINVAL, "null plan");
+  if (bn < 16 || bn > kBNMax || bn % 16)
+    throw Error(DEAR_EINVAL, "dear_gemm_plan_set_tile: bn must be a multiple of 16 in [16, 256]");
+  if (pair && plan->p.b_mn_major && bn != 128 && bn != 256)
+    throw Error(DEAR_EINVAL, "dear_gemm_plan_set_tile: MN-major B in CTA pairs needs bn 128 or 256");
+  configure(plan, TileChoice{bn, 1, 1, pair ? 1 : 0});
+  DEAR_API_END
+}
+
+int dear_gemm_plan_set_flags(dear_gemm_plan* plan, int32_t flags) {
+  DEAR_API_BEGIN
+  if (!plan) throw Error(DEAR_EINVAL, "null plan");
+  if (flags & ~DEAR_GEMM_EARLY_OPERANDS) throw Error(DEAR_EINVAL, "dear_gemm_plan_set_flags: unknown flag");
+  plan->p.early_operands = (flags & DEAR_GEMM_EARLY_OPERANDS) ? 1 : 0;
+  DEAR_API_END
+}
+
+int dear_gemm_plan_pair(dear_gemm_plan* plan, int32_t* pair) {
+  DEAR_API_BEGIN
+  if (!plan || !pair) throw Error(DEAR_EINVAL, "null plan");
+  *pair = plan->p.pair;
   DEAR_API_END
 }
 

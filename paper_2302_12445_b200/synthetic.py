@@ -37,7 +37,8 @@ def _round_up(x: int, m: int) -> int:
 
 
 class SyntheticModel:
-    def __init__(self, numels: list[int], hidden: int, tokens: int, device="cuda", seed: int = 0):
+    def __init__(self, numels: list[int], hidden: int, tokens: int, device="cuda", seed: int = 0,
+                 tune: bool = True):
         self.numels = [int(n) for n in numels]
         self.L = len(self.numels)
         self.H = int(hidden)
@@ -77,6 +78,7 @@ class SyntheticModel:
         self.y = torch.empty(T, self.rpad, dtype=torch.bfloat16, device=dev)
         self.dx = torch.empty(T, H, dtype=torch.bfloat16, device=dev)
         self._build_plans()
+        self.tiles = self.tune_tiles() if tune else None
 
     def _build_plans(self):
         H, T = self.H, self.T
@@ -84,12 +86,55 @@ class SyntheticModel:
         for l in range(self.L):
             R, n = self.rows[l], self.numels[l]
             W = self.shadows[l]
-            self.ff.append(GemmPlan(self.x, W, self.y, T, R, H, lda=H, ldb=H, ldd=self.rpad))
+            # No layer GEMM reads what another one writes (X, dY and the
+            # bf16 weights are read-only across the GEMM chain; W is refreshed
+            # by unpack on the comm stream behind an event), so operands may
+            # stream under the previous GEMM's tail.
+            self.ff.append(GemmPlan(self.x, W, self.y, T, R, H, lda=H, ldb=H, ldd=self.rpad,
+                                    early_operands=True))
             self.dgrad.append(GemmPlan(self.dy, W, self.dx, T, H, R, b_mn_major=True,
-                                       lda=self.rpad, ldb=H, ldd=H))
+                                       lda=self.rpad, ldb=H, ldd=H, early_operands=True))
             self.wgrad.append(GemmPlan(self.dyt, self.xt, self.grads[l] if n > 0 else self.grads_flat,
                                        R, H, T, lda=T, ldb=T, ldd=H, d_limit=n,
-                                       accumulate=True))
+                                       accumulate=True, early_operands=True))
+
+    def tune_tiles(self, chain: int = 16) -> dict:
+        """Plan-time tile autotuning (gemm.autotune): FF as a chain of FF
+        launches, backprop as a chain of grouped wgrad+dgrad launches (top-3 x
+        top-3 of the per-GEMM chains), on this model's own layer shapes. The
+        weight-gradient candidates run on a scratch output; FF / dgrad outputs
+        are synthetic scratch already. Runs once, outside any timed region."""
+        from .gemm import autotune, autotune_group, tile_candidates
+
+        H, T = self.H, self.T
+        k = min(self.L, 8)
+        R = max(set(self.rows), key=self.rows.count)
+        n = R * H
+        s = torch.cuda.Stream()
+        ff = autotune(self.ff[:k], tile_candidates(T, R, False), chain, s)
+        dg = autotune(self.dgrad[:k], tile_candidates(T, H, True), chain, s)
+        scratch = torch.zeros(n + 64, device=self.x.device)
+        wgs = [GemmPlan(self.dyt, self.xt, scratch, R, H, T, lda=T, ldb=T, ldd=H, d_limit=n,
+                        accumulate=True, early_operands=True)]
+        wg = autotune(wgs, tile_candidates(R, H, False), chain, s)
+        grp = autotune_group(wgs, self.dgrad[:k], [c[1:] for c in wg[:3]],
+                             [c[1:] for c in dg[:3]], chain, s)
+        best_ff, (best_wg, best_dg) = ff[0][1:], grp[0][1:]
+        for l in range(self.L):
+            self.ff[l].set_tile(*best_ff)
+            self.dgrad[l].set_tile(*best_dg)
+            self.wgrad[l].set_tile(*best_wg)
+        wgs[0].close()
+        return {"ff": {"bn": best_ff[0], "pair": best_ff[1], "us": round(ff[0][0], 2)},
+                "wgrad": {"bn": best_wg[0], "pair": best_wg[1]},
+                "dgrad": {"bn": best_dg[0], "pair": best_dg[1]},
+                "bp_group_us": round(grp[0][0], 2),
+                "candidates": {"ff": len(ff), "wgrad": len(wg), "dgrad": len(dg)}}
+
+    def gemm_launches_per_step(self) -> int:
+        bp = sum(1 if w.info()["pair"] == d.info()["pair"] else 2
+                 for w, d in zip(self.wgrad, self.dgrad))
+        return self.L + bp
 
     # -- flops ---------------------------------------------------------------
     def ff_flops(self) -> int:

@@ -6,10 +6,14 @@ import torch
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["cluster", "no-cluster"], autouse=True)
-def cluster_mode(request, monkeypatch):
-    """Every case runs with TMA-multicast clusters (opt-in) and without (default)."""
-    monkeypatch.setenv("DEAR_GEMM_CLUSTER", "1" if request.param == "cluster" else "0")
+@pytest.fixture(params=["auto", "single", "pair", "cluster"], autouse=True)
+def tile_mode(request, monkeypatch):
+    """Every case runs with the default tile choice, forced single-CTA tiles,
+    forced 2-CTA pairs (cta_group::2) and opt-in TMA-multicast clusters."""
+    env = {"auto": ("0", "1"), "single": ("0", "0"), "pair": ("0", "2"),
+           "cluster": ("1", "0")}[request.param]
+    monkeypatch.setenv("DEAR_GEMM_CLUSTER", env[0])
+    monkeypatch.setenv("DEAR_GEMM_PAIR", env[1])
     return request.param
 
 
@@ -93,8 +97,9 @@ def test_gemm_bf16_out(M, N, K):
     assert torch.all(err <= ref.abs() * 2.0**-8 + 2e-3 * ref.abs().max()), err.max()
 
 
+@pytest.mark.parametrize("early", [False, True])
 @pytest.mark.parametrize("M,N,K", [(8192, 1024, 512), (10240, 311, 512), (2048, 825, 1024)])
-def test_gemm_persistent_many_tiles(M, N, K):
+def test_gemm_persistent_many_tiles(M, N, K, tile_mode, early):
     """More tiles than SMs: exercises the persistent loop and both TMEM
     accumulators (epilogue of tile i overlapping the mainloop of tile i+1)."""
     from paper_2302_12445_b200.gemm import GemmPlan
@@ -103,13 +108,29 @@ def test_gemm_persistent_many_tiles(M, N, K):
     a = torch.randn(M, K, device="cuda").to(torch.bfloat16)
     b = torch.randn(N, K, device="cuda").to(torch.bfloat16)
     d = torch.full((M, N), float("nan"), device="cuda")
-    plan = GemmPlan(a, b, d, M, N, K, ldd=N)
+    plan = GemmPlan(a, b, d, M, N, K, ldd=N, early_operands=early)
     info = plan.info()
     assert info["m_tiles"] * info["n_tiles"] > 0
+    if tile_mode == "pair":
+        assert info["pair"] == 1 and info["cm"] == 2
+    if tile_mode in ("single", "cluster"):
+        assert info["pair"] == 0
     for _ in range(3):  # repeated launches (programmatic dependent launch chain)
         plan.run()
     torch.cuda.synchronize()
     _check(d, a.float() @ b.float().t(), K)
+    if early:
+        # D written by a chained GEMM while the next one streams its operands:
+        # the later launch's stores must land after the earlier one's.
+        d2 = torch.full((M, N), float("nan"), device="cuda")
+        p2 = GemmPlan(a, b, d2, M, N, K, ldd=N, early_operands=True)
+        b2 = torch.randn(N, K, device="cuda").to(torch.bfloat16)
+        p3 = GemmPlan(a, b2, d2, M, N, K, ldd=N, early_operands=True)
+        for _ in range(4):
+            p2.run()
+            p3.run()
+        torch.cuda.synchronize()
+        _check(d2, a.float() @ b2.float().t(), K)
 
 
 def test_gemm_group_wgrad_dgrad():
