@@ -62,6 +62,12 @@ def parse():
     ap.add_argument("--backend", default="auto", choices=["auto", "nccl", "peer"],
                     help="bucket collectives: fused NVLink peer kernels (auto when N > 1) "
                          "or NCCL RS/AG")
+    ap.add_argument("--group-dependency", type=int, default=1,
+                    help="DEAR with dear_group_dependency (AG_g <- RS_g) and the comm "
+                         "dispatch order simulated on measured times (0: global barrier)")
+    ap.add_argument("--contention", type=float, default=1.3,
+                    help="comm-stage slow-down next to the GEMMs assumed when planning the "
+                         "group-dependency dispatch order")
     ap.add_argument("--no-ablation", action="store_true", help="skip WFBP / compute-only runs")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -258,6 +264,73 @@ def make_runner(step, use_graph, stream):
     return replay
 
 
+def make_runtime(a, model, comm, rank, world, stream, policy, defer):
+    """Runtime over the model's tensors. For DEAR policies with
+    --group-dependency (the reference's dear_group_dependency, policy.hpp:44),
+    the comm stream's dispatch order is planned by the reference's scheduler
+    (costmodel.predict_iteration = simulate.cpp:65-159) on this run's own
+    measurements: per-layer GEMM chain times from the tile tuner and per-bucket
+    RS-side (pack+RS+update) / AG-side (AG+unpack) stage times of one
+    instrumented step. Rank 0's order is broadcast (collectives must be issued
+    in the same order on every rank)."""
+    import torch
+
+    import paper_2302_12445_b200 as dear
+    from paper_2302_12445_b200 import costmodel
+
+    gd = bool(a.group_dependency) and policy.startswith("DEAR")
+    rt = dear.Runtime(comm, rank, world, policy=policy, fusion_buffer_bytes=a.buffer,
+                      lr=a.lr, momentum=a.momentum, defer_allgather=defer,
+                      backend=a.backend, stream=stream, dear_group_dependency=gd)
+    for l in range(1, model.L + 1):
+        rt.register(l, model.params[l - 1], model.grads[l - 1], model.shadows[l - 1])
+    rt.finalize()
+    rt.comm_order_info = None
+    if not gd:
+        return rt
+    # Stage times of comm-only iterations (gradients reported back to back, no
+    # GEMMs): the pure comm-stream cost per bucket, scaled by --contention for
+    # the slow-down next to the layer GEMMs.
+    rt.set_timing(True)
+    for _ in range(3):
+        with torch.cuda.stream(stream):
+            for l in range(1, model.L + 1):
+                rt.param_wait(l, stream)
+            for l in range(model.L, 0, -1):
+                rt.grad_ready(l, stream)
+            rt.step(stream)
+        rt.synchronize()
+    torch.cuda.synchronize()
+    st = rt.timings()
+    rt.set_timing(False)
+    k = a.contention / 1e3
+    rs = [k * sum(v for v in (x["pack"], x["rs"], x["update"]) if v) for x in st]
+    ag = [k * sum(v for v in (x["ag"], x["unpack"]) if v) for x in st]
+    tiles = model.tiles or {}
+    t_ff = (tiles.get("ff", {}).get("us") or 10.0) * 1e-6
+    t_bp = (tiles.get("bp_group_us") or 20.0) * 1e-6
+    sim = costmodel.predict_iteration([4 * n for n in model.numels], [t_ff] * model.L,
+                                      [t_bp] * model.L, policy, a.buffer, world, 0.0, 0.0,
+                                      group_dependency=True, rs_times=rs, ag_times=ag)
+    order = torch.tensor(sim["comm_order"], dtype=torch.int32, device="cuda")
+    if world > 1:
+        torch.distributed.broadcast(order, 0)
+    order = order.cpu().tolist()
+    rt.set_comm_order(order)
+    last_rs = max(i for i, v in enumerate(order) if v > 0)
+    rt.comm_order_info = {"source": "reference scheduler simulated on measured times",
+                          "contention": a.contention,
+                          "ags_during_backprop": sum(1 for v in order[:last_rs] if v < 0),
+                          "rs_side_us_mean": 1e6 / a.contention * sum(rs) / len(rs),
+                          "ag_side_us_mean": 1e6 / a.contention * sum(ag) / len(ag),
+                          "stage_us_mean": {k: sum(x[k] or 0.0 for x in st) * 1e3 / len(st)
+                                            for k in ("pack", "rs", "update", "ag", "unpack")},
+                          "t_ff_us": t_ff * 1e6, "t_bp_us": t_bp * 1e6,
+                          "buckets": len(st),
+                          "predicted_ms": sim["iteration_seconds"] * 1e3}
+    return rt
+
+
 def gpu_arm(a, wl, world, rank, local_rank):
     import torch
 
@@ -282,18 +355,13 @@ def gpu_arm(a, wl, world, rank, local_rank):
     hbm, tf_burst, tf_sus, peak_kind = peaks()
 
     def runtime(policy):
-        rt = dear.Runtime(comm, rank, world, policy=policy, fusion_buffer_bytes=a.buffer,
-                          lr=a.lr, momentum=a.momentum, defer_allgather=use_graph,
-                          backend=a.backend, stream=stream)
-        for l in range(1, model.L + 1):
-            rt.register(l, model.params[l - 1], model.grads[l - 1], model.shadows[l - 1])
-        rt.finalize()
-        return rt
+        return make_runtime(a, model, comm, rank, world, stream, policy, use_graph)
 
     res = {}
     # --- headline: DeAR, inputs resident ---------------------------------
     rt = runtime(a.policy)
     backend_used = rt.backend
+    rt_order_info = rt.comm_order_info
     buckets = rt.buckets()
     run = make_runner(Step(model, rt, stream), use_graph, stream)
     if a.profile_steps:
@@ -388,6 +456,8 @@ def gpu_arm(a, wl, world, rank, local_rank):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic",
         "config": {"workload": wl["config"], "policy": a.policy, "collectives": backend_used,
+                   "dear_group_dependency": bool(a.group_dependency),
+                   "comm_order": rt_order_info,
                    "fusion_buffer_bytes": a.buffer, "buckets": len(buckets),
                    "batch_per_gpu": batch, "global_batch": samples, "tokens_per_gpu": tokens,
                    "hidden": wl["hidden"], "params": D, "cuda_graph": use_graph,
@@ -499,11 +569,9 @@ def compare_policies(a, wl_name, comm, world, rank, stream):
     out = {"workload": wl["config"], "batch_per_gpu": batch, "fusion_buffer_bytes": a.buffer,
            "steps": steps, "warmup": warm}
     for policy in (a.policy, a.baseline_policy):
-        rt = dear.Runtime(comm, rank, world, policy=policy, fusion_buffer_bytes=a.buffer,
-                          lr=a.lr, defer_allgather=True, backend=a.backend, stream=stream)
-        for l in range(1, model.L + 1):
-            rt.register(l, model.params[l - 1], model.grads[l - 1], model.shadows[l - 1])
-        rt.finalize()
+        rt = make_runtime(a, model, comm, rank, world, stream, policy, True)
+        if rt.comm_order_info:
+            out["comm_order"] = rt.comm_order_info
         run = make_runner(Step(model, rt, stream), True, stream)
         ms = time_loop(run, steps, warm, stream, dist_on)
         rt.synchronize()

@@ -138,6 +138,20 @@ int dear_param_wait(dear_ctx* ctx, int32_t layer, void* stream);
  * work already on `stream`, and `stream` waits until every gradient has been
  * packed (so gradients may be zeroed / overwritten afterwards). */
 int dear_step(dear_ctx* ctx, void* stream);
+/* dear_group_dependency (policy.hpp:44; task_graph.cpp:195-206): AG_g depends
+ * on RS_g only and the comm resource dispatches ready work by issue order
+ * (simulate.cpp:65-159), so all-gathers back-fill the comm stream during
+ * backprop. A CUDA stream is in-order, so the dispatch sequence is fixed per
+ * iteration: seq[0..2G) lists the comm tasks as the reference's scheduler
+ * dispatches them (v > 0: RS of bucket v, v < 0: AG of bucket -v, 1-based plan
+ * order; RS in plan order, each AG after its RS), e.g. from simulating the
+ * iteration on measured times (costmodel.predict_iteration). AGs between two
+ * RS entries are enqueued right behind the first during backprop; the AGs
+ * after the last RS at dear_step (or, deferred, at the next dear_param_wait),
+ * in seq order, where they overlap the next feed-forward. n = 0 restores the default (all AGs at dear_step in feed-forward
+ * order). Requires a DEAR policy with dear_group_dependency; call between
+ * iterations. */
+int dear_set_comm_order(dear_ctx* ctx, const int32_t* seq, int32_t n);
 
 /* `stream` waits for all comm-stream work enqueued so far (graph capture
  * join point). */

@@ -61,6 +61,7 @@ _SIGNATURES = {
     "dear_grad_ready": [_P, C.c_int32, _P],
     "dear_param_wait": [_P, C.c_int32, _P],
     "dear_step": [_P, _P],
+    "dear_set_comm_order": [_P, C.POINTER(C.c_int32), C.c_int32],
     "dear_join": [_P, _P],
     "dear_synchronize": [_P],
     "dear_destroy": [_P],

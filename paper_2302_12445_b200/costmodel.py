@@ -84,11 +84,18 @@ def exposed_comm(iteration: float, t_ff_total: float, t_bp_total: float) -> floa
 
 
 def predict_iteration(layer_bytes, t_ff, t_bp, policy: str, buffer_bytes: int, P: int,
-                      alpha: float, beta: float, group_dependency: bool = False) -> dict:
+                      alpha: float, beta: float, group_dependency: bool = False,
+                      rs_times=None, ag_times=None) -> dict:
     """Simulated steady-state iteration (seconds) of one worker: BP_L..BP_1 and
     FF_1..FF_L on the compute stream, RS/AG/AR on the comm stream, issue order
     and dependencies of task_graph.cpp:127-210, non-preemptive list
-    scheduling by (issue_order, id) as simulate.cpp:65-159."""
+    scheduling by (issue_order, id) as simulate.cpp:65-159.
+
+    rs_times / ag_times (seconds per fusion group, plan order) replace the
+    alpha-beta durations, e.g. with the runtime's measured per-bucket stage
+    times. Also returns the comm stream's dispatch sequence ("comm_order":
+    +g = RS / AR of group g, -g = AG of group g, 1-based), the input of
+    Runtime.set_comm_order."""
     L = len(layer_bytes)
     tasks = []  # (kind, subject, duration, deps, order, resource)
 
@@ -117,8 +124,9 @@ def predict_iteration(layer_bytes, t_ff, t_bp, policy: str, buffer_bytes: int, P
     elif policy.startswith("DEAR"):
         rs = []
         for gi in range(len(plan)):
-            rs.append(add("RS", gi + 1, reduce_scatter_time(gbytes[gi], P, alpha, beta),
-                          deps_bp[gi], order))
+            t_rs = (rs_times[gi] if rs_times is not None
+                    else reduce_scatter_time(gbytes[gi], P, alpha, beta))
+            rs.append(add("RS", gi + 1, t_rs, deps_bp[gi], order))
             order += 1
         bar = -1
         if not group_dependency:
@@ -126,8 +134,9 @@ def predict_iteration(layer_bytes, t_ff, t_bp, policy: str, buffer_bytes: int, P
             order += 1
         for gi in range(len(plan) - 1, -1, -1):
             lo, hi = plan[gi]
-            t = add("AG", gi + 1, all_gather_time(gbytes[gi], P, alpha, beta),
-                    [bar] if bar >= 0 else [rs[gi]], order)
+            t_ag = (ag_times[gi] if ag_times is not None
+                    else all_gather_time(gbytes[gi], P, alpha, beta))
+            t = add("AG", gi + 1, t_ag, [bar] if bar >= 0 else [rs[gi]], order)
             order += 1
             for l in range(lo, hi + 1):
                 tasks[ff[l]][3].append(t)
@@ -144,6 +153,7 @@ def predict_iteration(layer_bytes, t_ff, t_bp, policy: str, buffer_bytes: int, P
     heapq.heapify(ev)
     ready, running, end_at = [[], []], [-1, -1], [0.0] * n
     done = 0
+    dispatched = []
     while ev:
         now = ev[0][0]
         while ev and ev[0][0] == now:
@@ -162,10 +172,13 @@ def predict_iteration(layer_bytes, t_ff, t_bp, policy: str, buffer_bytes: int, P
             if running[r] == -1 and ready[r]:
                 _, i = heapq.heappop(ready[r])
                 running[r] = i
+                if r == 1 and tasks[i][0] != "BARRIER":
+                    dispatched.append(-tasks[i][1] if tasks[i][0] == "AG" else tasks[i][1])
                 end_at[i] = now + tasks[i][2]
                 heapq.heappush(ev, (end_at[i], 0, i))
     if done != n:
         raise RuntimeError("simulate: cycle detected")
     it = max(end_at)
     return {"iteration_seconds": it, "buckets": len(plan),
-            "exposed_comm_seconds": exposed_comm(it, float(sum(t_ff)), float(sum(t_bp)))}
+            "exposed_comm_seconds": exposed_comm(it, float(sum(t_ff)), float(sum(t_bp))),
+            "comm_order": dispatched}

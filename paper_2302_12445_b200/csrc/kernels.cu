@@ -27,6 +27,11 @@ constexpr int kThreads = 256;
 #define DEAR_HBM_UNROLL 4
 #endif
 constexpr int kUnroll = DEAR_HBM_UNROLL;
+// Remote (NVLink) source streams keep more loads in flight per lane.
+#ifndef DEAR_PEER_UNROLL
+#define DEAR_PEER_UNROLL 8
+#endif
+constexpr int kPeerUnroll = DEAR_PEER_UNROLL;
 constexpr int kCtasPerSm = kSlices / 148;
 constexpr int kSms = 148;
 
@@ -68,7 +73,7 @@ __device__ __forceinline__ float4 ld4(const float4* p) {
 // body(q, v) runs on every lane whose q < n4. All loads of one round (kUnroll
 // vectors per lane, plus the one vector past the round that lane 31 needs
 // when M != 0) are issued before any is consumed: no dependent second trip.
-template <int M, Hint H, typename Body>
+template <int M, Hint H, int kUnroll, typename Body>
 __device__ __forceinline__ void warp_stream(const float* src_floor, int64_t n4, int64_t qmax,
                                             Body&& body) {
   const float4* s4 = reinterpret_cast<const float4*>(src_floor);
@@ -111,7 +116,7 @@ __device__ __forceinline__ void warp_stream(const float* src_floor, int64_t n4, 
 
 // Peels `dst` to 16 B alignment (scalar head via head_fn), then dispatches the
 // vector walk on the source misalignment, then the scalar tail.
-template <Hint H, typename HeadFn, typename VecFn>
+template <Hint H, int KU = kUnroll, typename HeadFn, typename VecFn>
 __device__ __forceinline__ void run_unit(const float* src, const float* dst, int64_t len,
                                          HeadFn&& scalar_fn, VecFn&& vec_fn) {
   int64_t head = ((16 - (reinterpret_cast<uintptr_t>(dst) & 15)) & 15) >> 2;
@@ -126,16 +131,16 @@ __device__ __forceinline__ void run_unit(const float* src, const float* dst, int
     const int64_t qmax = (m + rest - 1) >> 2;
     switch (m) {
       case 0:
-        warp_stream<0, H>(floor, n4, qmax, [&](int64_t q, float4 v) { vec_fn(head, q, v); });
+        warp_stream<0, H, KU>(floor, n4, qmax, [&](int64_t q, float4 v) { vec_fn(head, q, v); });
         break;
       case 1:
-        warp_stream<1, H>(floor, n4, qmax, [&](int64_t q, float4 v) { vec_fn(head, q, v); });
+        warp_stream<1, H, KU>(floor, n4, qmax, [&](int64_t q, float4 v) { vec_fn(head, q, v); });
         break;
       case 2:
-        warp_stream<2, H>(floor, n4, qmax, [&](int64_t q, float4 v) { vec_fn(head, q, v); });
+        warp_stream<2, H, KU>(floor, n4, qmax, [&](int64_t q, float4 v) { vec_fn(head, q, v); });
         break;
       default:
-        warp_stream<3, H>(floor, n4, qmax, [&](int64_t q, float4 v) { vec_fn(head, q, v); });
+        warp_stream<3, H, KU>(floor, n4, qmax, [&](int64_t q, float4 v) { vec_fn(head, q, v); });
         break;
     }
   }
@@ -310,11 +315,71 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) unpack_kernel(const Unit
 }
 
 // ------------------------------------------- fused peer RS+update --------
+// Peer reduce-scatter streaming for a compile-time world size: per round each
+// lane issues its KU parameter loads (realigned to the slot like warp_stream)
+// and all KU x P slot loads from the P ranks' buffers before using any, so
+// the NVLink round trips overlap (a runtime-P loop issues them one by one:
+// the compiler cannot move a peer load above the previous vector's store).
+// pg[j] is the slot vector base on rank (rank+1+j) % P: ring order.
+template <int M, int P, int KU, typename Body>
+__device__ __forceinline__ void warp_stream_rs(const float* w_floor, const float4* const* pg,
+                                               int64_t n4, int64_t qmax, Body&& body) {
+  const float4* s4 = reinterpret_cast<const float4*>(w_floor);
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  constexpr int kWarps = kThreads / 32;
+  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int64_t base = static_cast<int64_t>(warp) * 32 * KU; base < n4;
+       base += static_cast<int64_t>(kWarps) * 32 * KU) {
+    float4 a[KU];
+    float4 v[KU][P];
+#pragma unroll
+    for (int k = 0; k < KU; ++k) {
+      const int64_t q = base + k * 32 + lane;
+      a[k] = q <= qmax ? __ldg(s4 + q) : zero;
+#pragma unroll
+      for (int j = 0; j < P; ++j) v[k][j] = q < n4 ? __ldcg(pg[j] + q) : zero;
+    }
+    float4 extra = zero;
+    if constexpr (M != 0) {
+      const int64_t qx = base + KU * 32;
+      if (lane == 31 && qx <= qmax) extra = __ldg(s4 + qx);
+    }
+#pragma unroll
+    for (int k = 0; k < KU; ++k) {
+      const int64_t q = base + k * 32 + lane;
+      float4 b = a[k];
+      if constexpr (M != 0) {
+        b = shfl_down4(a[k]);
+        float4 nxt = extra;
+        if (k + 1 < KU) {
+          nxt.x = __shfl_sync(0xffffffffu, a[k + 1 < KU ? k + 1 : k].x, 0);
+          nxt.y = __shfl_sync(0xffffffffu, a[k + 1 < KU ? k + 1 : k].y, 0);
+          nxt.z = __shfl_sync(0xffffffffu, a[k + 1 < KU ? k + 1 : k].z, 0);
+          nxt.w = __shfl_sync(0xffffffffu, a[k + 1 < KU ? k + 1 : k].w, 0);
+        }
+        if (lane == 31) b = nxt;
+      }
+      float4 acc = v[k][0];
+#pragma unroll
+      for (int j = 1; j < P; ++j) {
+        acc.x = __fadd_rn(acc.x, v[k][j].x);
+        acc.y = __fadd_rn(acc.y, v[k][j].y);
+        acc.z = __fadd_rn(acc.z, v[k][j].z);
+        acc.w = __fadd_rn(acc.w, v[k][j].w);
+      }
+      if (q < n4) body(q, realign<M>(a[k], b), acc);
+    }
+  }
+}
+
 // Ring-order sum (collective.cpp:70-90): chunk (rank+1)%P starts on rank
 // rank+1 and picks up rank+2, ..., rank — the same fold as the local-group
 // kernel, so the result is bit-exact with the fp32 restatement.
-template <bool kMom, bool kWd>
-__global__ void __launch_bounds__(kThreads, kCtasPerSm)
+// One CTA per SM at most (kPeerSlices CTAs): registers for the in-flight
+// peer loads instead of occupancy.
+template <int PC, bool kMom, bool kWd>
+__global__ void __launch_bounds__(kThreads, 1)
     rs_update_peer_kernel(const Unit* __restrict__ units, const Slice* __restrict__ slices,
                           const HyperParams* __restrict__ hpp, int has_buf, PeerArgs pa,
                           BucketFlags* flags) {
@@ -333,6 +398,51 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
       }
       return acc;
     };
+    auto scalar = [&](int64_t i) {
+      float m = kMom ? mom[i] : 0.f;
+      g[i] = sgd_elem<kMom, kWd>(sum1(g + i), w[i], m, hp, has_buf);
+      if (kMom) mom[i] = m;
+    };
+    if constexpr (PC > 0) {
+      // Compile-time P: all peer loads of a round in flight (warp_stream_rs).
+      constexpr int KU = PC <= 4 ? 4 : 2;
+      int64_t head = ((16 - (reinterpret_cast<uintptr_t>(g) & 15)) & 15) >> 2;
+      if (head > n) head = n;
+      if (threadIdx.x < head) scalar(static_cast<int64_t>(threadIdx.x));
+      const int64_t rest = n - head;
+      const int64_t n4 = rest >> 2;
+      if (n4 > 0) {
+        const float4* pg[PC];
+#pragma unroll
+        for (int j = 0; j < PC; ++j) {
+          const int r = (k0 + j) % PC;
+          pg[j] = at_peer(reinterpret_cast<const float4*>(g + head), pa.delta[r]);
+        }
+        const float* ws = w + head;
+        const int m = static_cast<int>((reinterpret_cast<uintptr_t>(ws) & 15) >> 2);
+        const int64_t qmax = (m + rest - 1) >> 2;
+        float4* g4 = reinterpret_cast<float4*>(g + head);
+        float4* m4 = kMom ? reinterpret_cast<float4*>(mom + head) : nullptr;
+        auto body = [&](int64_t q, float4 wv, float4 acc) {
+          float4 mv = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (kMom && has_buf) mv = m4[q];
+          acc.x = sgd_elem<kMom, kWd>(acc.x, wv.x, mv.x, hp, has_buf);
+          acc.y = sgd_elem<kMom, kWd>(acc.y, wv.y, mv.y, hp, has_buf);
+          acc.z = sgd_elem<kMom, kWd>(acc.z, wv.z, mv.z, hp, has_buf);
+          acc.w = sgd_elem<kMom, kWd>(acc.w, wv.w, mv.w, hp, has_buf);
+          g4[q] = acc;
+          if (kMom) m4[q] = mv;
+        };
+        switch (m) {
+          case 0: warp_stream_rs<0, PC, KU>(ws - m, pg, n4, qmax, body); break;
+          case 1: warp_stream_rs<1, PC, KU>(ws - m, pg, n4, qmax, body); break;
+          case 2: warp_stream_rs<2, PC, KU>(ws - m, pg, n4, qmax, body); break;
+          default: warp_stream_rs<3, PC, KU>(ws - m, pg, n4, qmax, body); break;
+        }
+      }
+      for (int64_t i = head + n4 * 4 + threadIdx.x; i < n; i += kThreads) scalar(i);
+      return;
+    }
     run_unit<Hint::kKeep>(
         w, g, n,
         [&](int64_t i) {
@@ -367,14 +477,14 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
 
 // ------------------------------------------- fused peer AG+unpack ---------
 template <bool kShadow>
-__global__ void __launch_bounds__(kThreads, kCtasPerSm)
+__global__ void __launch_bounds__(kThreads, 1)
     ag_unpack_peer_kernel(const Unit* __restrict__ units, const Slice* __restrict__ slices,
                           PeerArgs pa, BucketFlags* flags) {
   walk_slice(units, slices, kPeerSlices, [&](const Unit& U, int64_t off, int64_t n) {
     const float* src = at_peer(U.a + off, pa.delta[U.peer]);
     float* dst = U.b + off;
     __nv_bfloat16* sh = (kShadow && U.c) ? static_cast<__nv_bfloat16*>(U.c) + off : nullptr;
-    run_unit<Hint::kStream>(
+    run_unit<Hint::kStream, kPeerUnroll>(
         src, dst, n,
         [&](int64_t i) {
           const float v = src[i];
@@ -480,19 +590,32 @@ cudaError_t launch_wait_peers(const uint32_t* mine, const uint32_t* watch, const
   return cudaGetLastError();
 }
 
+template <int PC>
+void launch_rs_update_peer_p(const Unit* units, const Slice* slices, const HyperParams* hp,
+                             int has_momentum_buf, int use_momentum, int use_wd,
+                             const PeerArgs& pa, BucketFlags* flags, cudaStream_t s) {
+  const int grid = bucket_grid(kPeerSlices);
+  if (use_momentum && use_wd)
+    rs_update_peer_kernel<PC, true, true><<<grid, kThreads, 0, s>>>(units, slices, hp, has_momentum_buf, pa, flags);
+  else if (use_momentum)
+    rs_update_peer_kernel<PC, true, false><<<grid, kThreads, 0, s>>>(units, slices, hp, has_momentum_buf, pa, flags);
+  else if (use_wd)
+    rs_update_peer_kernel<PC, false, true><<<grid, kThreads, 0, s>>>(units, slices, hp, has_momentum_buf, pa, flags);
+  else
+    rs_update_peer_kernel<PC, false, false><<<grid, kThreads, 0, s>>>(units, slices, hp, has_momentum_buf, pa, flags);
+}
+
 cudaError_t launch_rs_update_peer(const Unit* units, const Slice* slices, int64_t total,
                                   const HyperParams* hp, int has_momentum_buf, int use_momentum,
                                   int use_wd, const PeerArgs& pa, BucketFlags* flags,
                                   cudaStream_t s) {
   (void)total;
-  if (use_momentum && use_wd)
-    rs_update_peer_kernel<true, true><<<bucket_grid(kPeerSlices), kThreads, 0, s>>>(units, slices, hp, has_momentum_buf, pa, flags);
-  else if (use_momentum)
-    rs_update_peer_kernel<true, false><<<bucket_grid(kPeerSlices), kThreads, 0, s>>>(units, slices, hp, has_momentum_buf, pa, flags);
-  else if (use_wd)
-    rs_update_peer_kernel<false, true><<<bucket_grid(kPeerSlices), kThreads, 0, s>>>(units, slices, hp, has_momentum_buf, pa, flags);
-  else
-    rs_update_peer_kernel<false, false><<<bucket_grid(kPeerSlices), kThreads, 0, s>>>(units, slices, hp, has_momentum_buf, pa, flags);
+  switch (pa.P) {
+    case 2: launch_rs_update_peer_p<2>(units, slices, hp, has_momentum_buf, use_momentum, use_wd, pa, flags, s); break;
+    case 4: launch_rs_update_peer_p<4>(units, slices, hp, has_momentum_buf, use_momentum, use_wd, pa, flags, s); break;
+    case 8: launch_rs_update_peer_p<8>(units, slices, hp, has_momentum_buf, use_momentum, use_wd, pa, flags, s); break;
+    default: launch_rs_update_peer_p<0>(units, slices, hp, has_momentum_buf, use_momentum, use_wd, pa, flags, s); break;
+  }
   return cudaGetLastError();
 }
 

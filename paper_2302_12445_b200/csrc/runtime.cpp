@@ -172,6 +172,11 @@ struct dear_ctx {
   bool timing = false;
   std::vector<std::string> trace;
   std::deque<Op> queue;  // local mode: ops not yet executed
+  // dear_group_dependency: comm-stream dispatch sequence of one iteration
+  // (>0: RS of bucket v-1, <0: AG of bucket -v-1), dear_set_comm_order.
+  std::vector<int32_t> comm_order;
+  size_t order_cursor = 0;
+  size_t order_tail = 0;  // first entry after the last RS: the step-time AGs
 
   ~dear_ctx();
   void enqueue(Op op);
@@ -179,6 +184,8 @@ struct dear_ctx {
   void complete_bucket(int b);
   void enqueue_backpipe(int b);
   void enqueue_feedpipe(cudaStream_t fence_stream);
+  void enqueue_ag(int g);
+  void enqueue_ordered_ags();
   void record_t(int b, int which);
   std::string label(const char* kind, int b) const;
 };
@@ -357,7 +364,13 @@ std::string dear_ctx::label(const char* kind, int b) const {
 void dear_ctx::record_t(int b, int which) {
   if (!timing) return;
   Bucket& B = buckets[static_cast<size_t>(b)];
-  cuda_check(cudaEventRecord(B.t[which], comm_stream), "cudaEventRecord");
+  // Inside a CUDA-graph capture the stamp must be an external event node to
+  // be timed after a replay (graph-mode timelines, tools/graph_timeline.py).
+  if (capture_id(comm_stream) != 0)
+    cuda_check(cudaEventRecordWithFlags(B.t[which], comm_stream, cudaEventRecordExternal),
+               "cudaEventRecordWithFlags");
+  else
+    cuda_check(cudaEventRecord(B.t[which], comm_stream), "cudaEventRecord");
   B.t_rec[which] = true;
 }
 
@@ -465,6 +478,7 @@ void dear_ctx::enqueue_backpipe(int b) {
   enqueue({OP_UPDATE, b, nullptr});
   if (is_dear(cfg.policy)) {
     trace.push_back(label("RS", b));
+    if (!comm_order.empty()) enqueue_ordered_ags();
   } else {
     trace.push_back(label("AR", b));
     enqueue({OP_AG, b, nullptr});
@@ -482,19 +496,40 @@ void dear_ctx::enqueue_feedpipe(cudaStream_t fence_stream) {
   // deferred — the start of the next forward, which keeps the comm stream
   // inside a CUDA-graph capture of that stream).
   cuda_check(cudaEventRecord(step_ev, fence_stream), "cudaEventRecord");
-  // Reverse plan order = feed-forward order (task_graph.cpp:199-206).
   enqueue({OP_FENCE_STEP, -1, nullptr});
-  for (int g = static_cast<int>(buckets.size()) - 1; g >= 0; --g) {
-    Bucket& B = buckets[static_cast<size_t>(g)];
-    enqueue({OP_AG, g, nullptr});
-    enqueue({OP_UNPACK, g, nullptr});
-    enqueue({OP_AG_DONE, g, nullptr});
-    trace.push_back(label("AG", g));
-    B.ag_live = true;
-    B.waited_valid = false;
+  if (!comm_order.empty()) {
+    // Group dependency: the all-gathers not dispatched during backprop, in
+    // the simulated dispatch order.
+    for (; order_cursor < comm_order.size(); ++order_cursor)
+      enqueue_ag(-comm_order[order_cursor] - 1);
+    order_cursor = 0;
+  } else {
+    // Reverse plan order = feed-forward order (task_graph.cpp:199-206).
+    for (int g = static_cast<int>(buckets.size()) - 1; g >= 0; --g) enqueue_ag(g);
   }
   ags_deferred = false;
   if (local) group->drain();
+}
+
+void dear_ctx::enqueue_ag(int g) {
+  Bucket& B = buckets[static_cast<size_t>(g)];
+  enqueue({OP_AG, g, nullptr});
+  enqueue({OP_UNPACK, g, nullptr});
+  enqueue({OP_AG_DONE, g, nullptr});
+  trace.push_back(label("AG", g));
+  B.ag_live = true;
+  B.waited_valid = false;
+}
+
+// After RS_g was enqueued: the all-gathers the dispatch order puts before the
+// next reduce-scatter run now, behind it on the comm stream (AG_g <- RS_g,
+// task_graph.cpp:201-203; their layers are already backpropagated).
+void dear_ctx::enqueue_ordered_ags() {
+  ++order_cursor;  // the RS just enqueued
+  while (order_cursor < order_tail && comm_order[order_cursor] < 0) {
+    enqueue_ag(-comm_order[order_cursor] - 1);
+    ++order_cursor;
+  }
 }
 
 void dear_ctx::complete_bucket(int b) {
@@ -903,6 +938,49 @@ int dear_grad_ready(dear_ctx* ctx, int32_t layer, void* stream) {
   DEAR_API_END
 }
 
+int dear_set_comm_order(dear_ctx* ctx, const int32_t* seq, int32_t n) {
+  DEAR_API_BEGIN
+  need(ctx, true);
+  dear_ctx& c = *ctx;
+  if (!is_dear(c.cfg.policy)) invalid("dear_set_comm_order: needs a DEAR policy");
+  if (!c.cfg.dear_group_dependency)
+    invalid("dear_set_comm_order: needs dear_group_dependency (AG_g waits on RS_g only)");
+  if (c.reported != 0 || c.ags_deferred)
+    invalid("dear_set_comm_order: call between iterations");
+  const int G = static_cast<int>(c.buckets.size());
+  if (n == 0) {
+    c.comm_order.clear();
+    c.order_cursor = c.order_tail = 0;
+    return DEAR_OK;
+  }
+  if (!seq || n != 2 * G) invalid("dear_set_comm_order: need 2 x buckets entries");
+  // Reduce-scatters in plan order; every all-gather once, after its RS.
+  std::vector<char> rs_seen(static_cast<size_t>(G), 0), ag_seen(static_cast<size_t>(G), 0);
+  int next_rs = 0;
+  if (seq[0] != 1) invalid("dear_set_comm_order: must start with RS of bucket 1");
+  for (int32_t i = 0; i < n; ++i) {
+    const int32_t v = seq[i];
+    if (v > 0) {
+      if (v > G) invalid("dear_set_comm_order: entry out of range");
+      if (v != next_rs + 1) invalid("dear_set_comm_order: reduce-scatters must follow plan order");
+      rs_seen[static_cast<size_t>(next_rs++)] = 1;
+    } else if (v < 0 && -v <= G) {
+      const int g = -v - 1;
+      if (!rs_seen[static_cast<size_t>(g)]) invalid("dear_set_comm_order: AG before its RS");
+      if (ag_seen[static_cast<size_t>(g)]) invalid("dear_set_comm_order: AG listed twice");
+      ag_seen[static_cast<size_t>(g)] = 1;
+    } else {
+      invalid("dear_set_comm_order: entry out of range");
+    }
+  }
+  c.comm_order.assign(seq, seq + n);
+  c.order_cursor = 0;
+  c.order_tail = 0;
+  for (int32_t i = 0; i < n; ++i)
+    if (seq[i] > 0) c.order_tail = static_cast<size_t>(i) + 1;
+  DEAR_API_END
+}
+
 int dear_step(dear_ctx* ctx, void* stream) {
   DEAR_API_BEGIN
   need(ctx, true);
@@ -919,7 +997,10 @@ int dear_step(dear_ctx* ctx, void* stream) {
   // caller's backward work.
   c.enqueue({OP_CALLER_WAIT_PACKED, -1, s});
   if (is_dear(c.cfg.policy)) {
-    if (c.cfg.defer_allgather) {
+    if (!c.comm_order.empty() && c.order_cursor >= c.comm_order.size()) {
+      c.order_cursor = 0;  // every all-gather already dispatched during backprop
+      if (c.local) c.group->drain();
+    } else if (c.cfg.defer_allgather) {
       c.ags_deferred = true;
     } else {
       c.enqueue_feedpipe(s);
@@ -958,12 +1039,14 @@ int dear_param_wait(dear_ctx* ctx, int32_t layer, void* stream) {
   if (!B.ag_live) return DEAR_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (B.waited_valid && B.waited == s) return DEAR_OK;
-  // Inside a CUDA-graph capture, an all-gather recorded outside this capture
-  // (the previous iteration of a WFBP schedule) is ordered before the graph
-  // launch by the capture's trailing dear_join; a cross-capture wait is
-  // illegal, so it is dropped.
+  // An all-gather recorded in another capture context than this wait (inside
+  // a capture: the previous iteration of a WFBP schedule, or one issued during
+  // the previous graph's backprop under dear_group_dependency; eagerly: one
+  // recorded while capturing the previous graph) is ordered before this work
+  // by that graph's / this capture's trailing dear_join on the caller's
+  // stream. Waiting on it is illegal, so it is dropped.
   const unsigned long long cap = capture_id(s);
-  if (cap != 0 && B.ag_capture != cap) return DEAR_OK;
+  if (B.ag_capture != cap) return DEAR_OK;
   if (c.local) {
     c.group->drain();
     if (!c.queue.empty()) invalid("dear_param_wait: local group ranks are out of lock-step");

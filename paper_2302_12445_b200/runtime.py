@@ -181,6 +181,14 @@ class Runtime:
     def step(self, stream=None) -> None:
         check(lib().dear_step(self._ctx, _stream_ptr(stream)))
 
+    def set_comm_order(self, seq) -> None:
+        """Comm-stream dispatch sequence for dear_group_dependency
+        (dear_set_comm_order): +g = RS of bucket g, -g = AG of bucket g,
+        1-based plan order; [] restores the default."""
+        seq = [int(v) for v in seq]
+        arr = (C.c_int32 * max(1, len(seq)))(*seq)
+        check(lib().dear_set_comm_order(self._ctx, arr, len(seq)))
+
     def join(self, stream=None) -> None:
         check(lib().dear_join(self._ctx, _stream_ptr(stream)))
 

@@ -66,7 +66,8 @@ def oracle_run(o: Restated, numels, P: int, steps: int, policy: str, buffer_byte
 
 def run_local(numels, P: int, steps: int, policy: str, buffer_bytes: int, lr: float,
               momentum=0.0, dampening=0.0, weight_decay=0.0, nesterov=False,
-              defer_allgather=False, seed0: int = 1000, wseed: int = 77, shadow: bool = False):
+              defer_allgather=False, seed0: int = 1000, wseed: int = 77, shadow: bool = False,
+              comm_order=None):
     """Drive P local-group ranks in lock-step through `steps` iterations of
     backward (layers L..1) + step + forward waits. Returns (params [P, D],
     shadows or None, traces, runtimes-closed)."""
@@ -84,7 +85,8 @@ def run_local(numels, P: int, steps: int, policy: str, buffer_bytes: int, lr: fl
     for r in range(P):
         rt = Runtime(group, r, P, policy=policy, fusion_buffer_bytes=buffer_bytes, lr=lr,
                      momentum=momentum, dampening=dampening, weight_decay=weight_decay,
-                     nesterov=nesterov, defer_allgather=defer_allgather)
+                     nesterov=nesterov, defer_allgather=defer_allgather,
+                     dear_group_dependency=comm_order is not None)
         ps, gs, ss = [], [], []
         for l in range(1, L + 1):
             a, b = offs[l - 1], offs[l]
@@ -101,6 +103,8 @@ def run_local(numels, P: int, steps: int, policy: str, buffer_bytes: int, lr: fl
         shadows.append(ss)
     for rt in rts:
         rt.finalize()
+        if comm_order is not None:
+            rt.set_comm_order(comm_order)
     traces = []
     for s in range(steps):
         G = seeded_grads(o, P, numels, s, seed0)

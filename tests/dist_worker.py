@@ -33,14 +33,15 @@ def close(a, b, tol=1e-5):
     return bool(np.all(np.abs(a - b) <= tol * np.maximum(1.0, np.abs(b))))
 
 
-def run_runtime(comm, rank, P, policy, buf, steps, lr, backend="nccl", **kw):  # explicit
+def run_runtime(comm, rank, P, policy, buf, steps, lr, backend="nccl", comm_order=None,
+                **kw):  # explicit backend
     o = Restated()
     numels = RAGGED
     offs = np.concatenate([[0], np.cumsum(numels)]).astype(np.int64)
     w0 = initial_weights(o, numels)
     s = torch.cuda.Stream()
     rt = dear.Runtime(comm, rank, P, policy=policy, fusion_buffer_bytes=buf, lr=lr, stream=s,
-                      backend=backend, **kw)
+                      backend=backend, dear_group_dependency=comm_order is not None, **kw)
     params, grads = [], []
     for l in range(1, len(numels) + 1):
         p = torch.from_numpy(w0[offs[l - 1]:offs[l]].copy()).cuda()
@@ -49,6 +50,8 @@ def run_runtime(comm, rank, P, policy, buf, steps, lr, backend="nccl", **kw):  #
         params.append(p)
         grads.append(g)
     rt.finalize()
+    if comm_order is not None:
+        rt.set_comm_order(comm_order)
     with torch.cuda.stream(s):
         for step in range(steps):
             G = seeded_grads(o, P, numels, step)
@@ -91,8 +94,29 @@ def case_runtime(rank, P):
         print(f"[runtime P={P}] momentum/wd/nesterov replicas={same} oracle_1e-5={good}",
               flush=True)
     ok &= good
+    # dear_group_dependency: all-gathers back-filled between reduce-scatters
+    from paper_2302_12445_b200 import costmodel as cm
+    L = len(RAGGED)
+    G = cm.predict_iteration([4 * n for n in RAGGED], [1.0] * L, [1.0] * L, "DEAR_FUSED",
+                             100_000, P, 0.0, 0.0)["buckets"]
+    order = cm.predict_iteration([4 * n for n in RAGGED], [0.5] * L, [1.0] * L, "DEAR_FUSED",
+                                 100_000, P, 0.0, 0.0, group_dependency=True,
+                                 rs_times=[1.5] * G, ag_times=[1.0] * G)["comm_order"]
+    w, same, trace = run_runtime(comm, rank, P, "DEAR_FUSED", 100_000, 3, 0.05, "nccl",
+                                 comm_order=order)
+    exp32 = oracle_run(o, RAGGED, P, 3, "DEAR_FUSED", 100_000, 0.05, f32=True)
+    exp64 = oracle_run(o, RAGGED, P, 3, "DEAR_FUSED", 100_000, 0.05, f32=False)
+    want = [("RS g%d" % v) if v > 0 else ("AG g%d" % -v) for v in order]
+    good = same and close(w.astype(np.float64), exp64) and trace == want and \
+        True
+    if rank == 0:
+        print(f"[runtime P={P}] group_dependency order={order[:8]}.. replicas={same} "
+              f"trace_is_order={trace == want} oracle_1e-5={close(w.astype(np.float64), exp64)}",
+              flush=True)
+    ok &= good
     comm.close()
     return ok
+
 
 
 def case_peer(rank, P):
@@ -120,8 +144,29 @@ def case_peer(rank, P):
     if rank == 0:
         print(f"[peer P={P}] momentum/wd/nesterov bit_exact={good}", flush=True)
     ok &= good
+    # dear_group_dependency: all-gathers back-filled between reduce-scatters
+    from paper_2302_12445_b200 import costmodel as cm
+    L = len(RAGGED)
+    G = cm.predict_iteration([4 * n for n in RAGGED], [1.0] * L, [1.0] * L, "DEAR_FUSED",
+                             100_000, P, 0.0, 0.0)["buckets"]
+    order = cm.predict_iteration([4 * n for n in RAGGED], [0.5] * L, [1.0] * L, "DEAR_FUSED",
+                                 100_000, P, 0.0, 0.0, group_dependency=True,
+                                 rs_times=[1.5] * G, ag_times=[1.0] * G)["comm_order"]
+    w, same, trace = run_runtime(comm, rank, P, "DEAR_FUSED", 100_000, 3, 0.05, "peer",
+                                 comm_order=order)
+    exp32 = oracle_run(o, RAGGED, P, 3, "DEAR_FUSED", 100_000, 0.05, f32=True)
+    exp64 = oracle_run(o, RAGGED, P, 3, "DEAR_FUSED", 100_000, 0.05, f32=False)
+    want = [("RS g%d" % v) if v > 0 else ("AG g%d" % -v) for v in order]
+    good = same and close(w.astype(np.float64), exp64) and trace == want and \
+        ("peer" == "nccl" or np.array_equal(w, exp32))
+    if rank == 0:
+        print(f"[peer P={P}] group_dependency order={order[:8]}.. replicas={same} "
+              f"trace_is_order={trace == want} oracle_1e-5={close(w.astype(np.float64), exp64)}",
+              flush=True)
+    ok &= good
     comm.close()
     return ok
+
 
 
 def case_distoptim(rank, P):

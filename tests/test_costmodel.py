@@ -62,3 +62,49 @@ def test_predicted_iterations_match_reference_simulator():
                                    s["policy"], s["buffer"], s["P"], s["alpha"], s["beta"])
         assert got["iteration_seconds"] == pytest.approx(s["result"]["iteration_seconds"],
                                                          rel=1e-12), s["name"]
+
+
+def _labels(order):
+    return [("RS g%d" % v) if v > 0 else ("AG g%d" % -v) for v in order]
+
+
+@pytest.mark.parametrize("gd", [False, True])
+@pytest.mark.parametrize("P,alpha,beta", [(2, 1e-4, 1e-9), (4, 5e-5, 4e-9), (8, 2e-5, 1e-8)])
+def test_comm_order_is_reference_dispatch_order(gd, P, alpha, beta):
+    """The dispatch sequence predict_iteration hands to Runtime.set_comm_order
+    is the reference scheduler's Comm dispatch order (oracle restatement of
+    task_graph.cpp:181-210 + simulate.cpp:65-159), with and without
+    dear_group_dependency."""
+    from oracle.schedule import build_graph, comm_dispatch_order, simulate
+
+    rng = np.random.default_rng(P)
+    counts = [int(x) for x in rng.integers(1, 400_000, size=40)]
+    t_ff = [float(x) for x in rng.uniform(1e-5, 3e-5, size=40)]
+    t_bp = [2 * t for t in t_ff]
+    lb = [4 * c for c in counts]
+    got = cm.predict_iteration(lb, t_ff, t_bp, "DEAR_FUSED", 1_000_000, P, alpha, beta,
+                               group_dependency=gd)
+    tasks, _ = build_graph(lb, t_ff, t_bp, "DEAR_FUSED", 1_000_000, group_dependency=gd, P=P,
+                           alpha=alpha, beta=beta)
+    span, makespan = simulate(tasks)
+    assert _labels(got["comm_order"]) == comm_dispatch_order(tasks, span)
+    assert got["iteration_seconds"] == pytest.approx(makespan, rel=1e-12)
+
+
+def test_comm_order_with_measured_stage_times():
+    """rs_times / ag_times replace the alpha-beta durations per group."""
+    counts = [100_000] * 12
+    lb = [4 * c for c in counts]
+    plan_groups = cm.predict_iteration(lb, [1e-5] * 12, [2e-5] * 12, "DEAR_FUSED", 800_000, 4,
+                                       0.0, 0.0)["buckets"]
+    slow = cm.predict_iteration(lb, [1e-5] * 12, [2e-5] * 12, "DEAR_FUSED", 800_000, 4, 0.0, 0.0,
+                                group_dependency=True, rs_times=[1e-3] * plan_groups,
+                                ag_times=[1e-3] * plan_groups)
+    fast = cm.predict_iteration(lb, [1e-5] * 12, [2e-5] * 12, "DEAR_FUSED", 800_000, 4, 0.0, 0.0,
+                                group_dependency=True, rs_times=[1e-6] * plan_groups,
+                                ag_times=[1e-6] * plan_groups)
+    # comm-bound: every RS first, then the AGs in feed-forward order
+    G = plan_groups
+    assert slow["comm_order"] == list(range(1, G + 1)) + [-g for g in range(G, 0, -1)]
+    # comm much faster than backprop: each AG right behind its RS
+    assert fast["comm_order"] == [v for g in range(1, G + 1) for v in (g, -g)]

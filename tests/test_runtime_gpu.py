@@ -80,3 +80,71 @@ def test_trace_is_reference_dispatch_order():
         want = comm_dispatch_order(tasks, span)
         assert traces[-1][0] == want, policy
         assert traces[-1][1] == want
+
+
+def _gd_order(numels, buf, P, t_bp, rs, ag):
+    """Dispatch order of the reference scheduler with dear_group_dependency."""
+    from paper_2302_12445_b200 import costmodel as cm
+
+    L = len(numels)
+    G = cm.predict_iteration([4 * n for n in numels], [1.0] * L, [1.0] * L, "DEAR_FUSED", buf,
+                             P, 0.0, 0.0)["buckets"]
+    return cm.predict_iteration([4 * n for n in numels], [t_bp / 2] * L, [t_bp] * L,
+                                "DEAR_FUSED", buf, P, 0.0, 0.0, group_dependency=True,
+                                rs_times=[rs] * G, ag_times=[ag] * G)["comm_order"]
+
+
+@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("defer", [False, True])
+@pytest.mark.parametrize("regime", ["backfill", "all_in_backprop", "all_at_step"])
+def test_group_dependency_comm_order(restated, P, defer, regime):
+    """dear_group_dependency with a dispatch order from the reference
+    scheduler: same parameters as the barrier schedule (bit-exact with the
+    fp32 ring restatement), and the rank's comm-stream trace IS that order."""
+    buf, steps, lr = 40_000, 3, 0.05
+    rs, ag = {"backfill": (1.5, 1.0), "all_in_backprop": (0.01, 0.01),
+              "all_at_step": (100.0, 100.0)}[regime]
+    order = _gd_order(RAGGED, buf, P, 1.0, rs, ag)
+    got, _, traces, same = run_local(RAGGED, P, steps, "DEAR_FUSED", buf, lr,
+                                     defer_allgather=defer, comm_order=order)
+    exp32 = oracle_run(restated, RAGGED, P, steps, "DEAR_FUSED", buf, lr, f32=True)
+    for r in range(P):
+        assert np.array_equal(got[r], exp32)
+    assert all(same)
+    want = [("RS g%d" % v) if v > 0 else ("AG g%d" % -v) for v in order]
+    assert traces[-1][0] == want
+    if regime == "backfill":
+        last_rs = max(i for i, v in enumerate(order) if v > 0)
+        assert any(v < 0 for v in order[:last_rs]) and any(v < 0 for v in order[last_rs:])
+
+
+def test_comm_order_validation():
+    import torch
+
+    from paper_2302_12445_b200 import InvalidArgument, LocalGroup, Runtime
+
+    g = LocalGroup(1)
+    p = torch.zeros(3000, device="cuda")
+    gr = torch.zeros(3000, device="cuda")
+    rt = Runtime(g, 0, 1, policy="DEAR_FUSED", fusion_buffer_bytes=4000, lr=0.1,
+                 dear_group_dependency=True)
+    for l in range(3):
+        rt.register(l + 1, p[1000 * l:1000 * (l + 1)], gr[1000 * l:1000 * (l + 1)])
+    rt.finalize()
+    G = len(rt.buckets())
+    assert G == 3
+    for bad in ([1, -1, 2, -2, 3], [1, 2, -3, 3, -1, -2], [2, 1, 3, -1, -2, -3],
+                [1, -1, 2, -1, 3, -3], [1, -1, 2, -2, 3, 4]):
+        with pytest.raises(InvalidArgument):
+            rt.set_comm_order(bad)
+    rt.set_comm_order([1, -1, 2, 3, -3, -2])
+    rt.set_comm_order([])
+    rt.close()
+    rt2 = Runtime(g, 0, 1, policy="DEAR_FUSED", fusion_buffer_bytes=4000, lr=0.1)
+    for l in range(3):
+        rt2.register(l + 1, p[1000 * l:1000 * (l + 1)], gr[1000 * l:1000 * (l + 1)])
+    rt2.finalize()
+    with pytest.raises(InvalidArgument):  # needs dear_group_dependency
+        rt2.set_comm_order([1, -1, 2, -2, 3, -3])
+    rt2.close()
+    g.close()
