@@ -39,7 +39,10 @@ constexpr int64_t kUnitElems = 1 << 20;
 constexpr int kSlices = 148 * DEAR_SLICES_PER_SM;
 // NVLink-bound peer kernels need far fewer CTAs to saturate the links
 // (~1.2 MB in flight); a small grid leaves the SMs to the concurrent GEMMs.
-constexpr int kPeerSlices = 64;
+#ifndef DEAR_PEER_SLICES
+#define DEAR_PEER_SLICES 64
+#endif
+constexpr int kPeerSlices = DEAR_PEER_SLICES;
 
 struct Slice {
   Unit first;     // the slice's first piece, pointers pre-offset (one load per CTA)
@@ -112,7 +115,7 @@ cudaError_t launch_wait_peers(const uint32_t* mine, const uint32_t* watch, const
                               cudaStream_t s);
 // pack with a completion signal (flags->packed += 1 after all CTAs finish).
 cudaError_t launch_pack_signal(const Unit* units, const Slice* slices, int64_t total, float scale,
-                               BucketFlags* flags, int grid, cudaStream_t s);
+                               BucketFlags* flags, const PeerArgs& pa, int grid, cudaStream_t s);
 // Fused reduce-scatter + shard SGD update: for each own-shard element, sum the
 // peers' slot-`rank` values in ring order (rank+1, ..., rank), update, write
 // w' into the own slot; then flags->updated += 1.

@@ -214,15 +214,47 @@ __global__ void wait_peers_kernel(const uint32_t* mine, const uint32_t* watch, P
   }
 }
 
+// In-kernel form of wait_peers_kernel: warp 0 of every CTA spins until each
+// peer's `watch` counter reached our own `mine`, then the CTA proceeds (the
+// acquire + CTA barrier order the CTA's later peer reads after the peers'
+// released writes). Saves a dependent launch per stage on the comm stream.
+__device__ __forceinline__ void cta_wait_peers(const uint32_t* mine, const uint32_t* watch,
+                                               const PeerArgs& pa) {
+  if (threadIdx.x < 32) {
+    const uint32_t target = ld_acquire_sys(mine);
+    const int k = threadIdx.x;
+    if (k < pa.P && k != pa.rank) {
+      const uint32_t* f = at_peer(watch, pa.delta[k]);
+      const long long t0 = clock64();
+      while (static_cast<int32_t>(ld_acquire_sys(f) - target) < 0) {
+        __nanosleep(128);
+        if (clock64() - t0 > 60ll * 2000000000ll) __trap();  // fail loudly, never hang
+      }
+    }
+    __syncwarp();
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+  }
+  __syncthreads();
+}
+
 // ---------------------------------------------------------------- pack ----
+// Peer backend (kSignal): one CTA per SM next to the GEMMs, so each lane keeps
+// kPackPeerUnroll vectors in flight instead of relying on occupancy.
+#ifndef DEAR_PACK_PEER_UNROLL
+#define DEAR_PACK_PEER_UNROLL 16
+#endif
+constexpr int kPackPeerUnroll = DEAR_PACK_PEER_UNROLL;
 template <bool kSignal>
-__global__ void __launch_bounds__(kThreads, kCtasPerSm) pack_kernel(const Unit* __restrict__ units,
+__global__ void __launch_bounds__(kThreads, kSignal ? 1 : kCtasPerSm) pack_kernel(const Unit* __restrict__ units,
                                                            const Slice* __restrict__ slices,
-                                                           float scale, BucketFlags* flags) {
+                                                           float scale, BucketFlags* flags,
+                                                           PeerArgs pa) {
+  // Peer backend: our slots may be rewritten once every peer gathered them.
+  if (kSignal) cta_wait_peers(&flags->packed, &flags->gathered, pa);
   walk_slice(units, slices, kSlices, [&](const Unit& U, int64_t off, int64_t n) {
     const float* src = U.a + off;
     float* dst = U.b + off;
-    run_unit<Hint::kStream>(
+    run_unit<Hint::kStream, kSignal ? kPackPeerUnroll : kUnroll>(
         src, dst, n, [&](int64_t i) { dst[i] = __fmul_rn(src[i], scale); },
         [&](int64_t head, int64_t q, float4 v) {
           v.x = __fmul_rn(v.x, scale);
@@ -383,6 +415,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     rs_update_peer_kernel(const Unit* __restrict__ units, const Slice* __restrict__ slices,
                           const HyperParams* __restrict__ hpp, int has_buf, PeerArgs pa,
                           BucketFlags* flags) {
+  cta_wait_peers(&flags->packed, &flags->packed, pa);  // every rank packed this bucket
   const HyperParams hp = *hpp;
   const int k0 = (pa.rank + 1) % pa.P;
   walk_slice(units, slices, kPeerSlices, [&](const Unit& U, int64_t off, int64_t n) {
@@ -480,6 +513,7 @@ template <bool kShadow>
 __global__ void __launch_bounds__(kThreads, 1)
     ag_unpack_peer_kernel(const Unit* __restrict__ units, const Slice* __restrict__ slices,
                           PeerArgs pa, BucketFlags* flags) {
+  cta_wait_peers(&flags->updated, &flags->updated, pa);  // every owner updated its shard
   walk_slice(units, slices, kPeerSlices, [&](const Unit& U, int64_t off, int64_t n) {
     const float* src = at_peer(U.a + off, pa.delta[U.peer]);
     float* dst = U.b + off;
@@ -573,14 +607,15 @@ int bucket_grid(int n_slices, int want = 0) {
 cudaError_t launch_pack(const Unit* units, const Slice* slices, int64_t total, float scale,
                         int grid, cudaStream_t s) {
   if (total <= 0) return cudaSuccess;
-  pack_kernel<false><<<bucket_grid(kSlices, grid), kThreads, 0, s>>>(units, slices, scale, nullptr);
+  pack_kernel<false><<<bucket_grid(kSlices, grid), kThreads, 0, s>>>(units, slices, scale, nullptr,
+                                                                     PeerArgs{});
   return cudaGetLastError();
 }
 
 cudaError_t launch_pack_signal(const Unit* units, const Slice* slices, int64_t total, float scale,
-                               BucketFlags* flags, int grid, cudaStream_t s) {
+                               BucketFlags* flags, const PeerArgs& pa, int grid, cudaStream_t s) {
   (void)total;  // the signal must fire even for an empty bucket
-  pack_kernel<true><<<bucket_grid(kSlices, grid), kThreads, 0, s>>>(units, slices, scale, flags);
+  pack_kernel<true><<<bucket_grid(kSlices, grid), kThreads, 0, s>>>(units, slices, scale, flags, pa);
   return cudaGetLastError();
 }
 

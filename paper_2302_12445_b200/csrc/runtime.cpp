@@ -387,13 +387,11 @@ void dear_ctx::exec(const Op& op) {
     case OP_PACK:
       record_t(op.bucket, T_PACK0);
       if (peer) {
-        // Our buffer may be rewritten only once every peer gathered from it.
-        cuda_check(launch_wait_peers(&B->flags->packed, &B->flags->gathered, pa, comm_stream),
-                   "wait kernel");
-        // One CTA per SM: the pack overlaps backprop GEMMs and the fused peer
+        // The kernel first waits (in-kernel) until every peer gathered from
+        // our buffer, which it then rewrites. One CTA per SM: the pack overlaps backprop GEMMs and the fused peer
         // kernels; a full 4-CTA/SM grid would hold every SM's register file
         // and stall the persistent GEMM (profiles/r01_n4_interference_matrix.log).
-        cuda_check(launch_pack_signal(B->pack_u, B->pack_s, B->e_pack, pack_scale, B->flags,
+        cuda_check(launch_pack_signal(B->pack_u, B->pack_s, B->e_pack, pack_scale, B->flags, pa,
                                       sm_count(), comm_stream),
                    "pack kernel");
       } else {
@@ -405,9 +403,8 @@ void dear_ctx::exec(const Op& op) {
       break;
     case OP_RS:
       if (peer) {
-        // Fused reduce-scatter + update over NVLink (OP_UPDATE becomes a no-op).
-        cuda_check(launch_wait_peers(&B->flags->packed, &B->flags->packed, pa, comm_stream),
-                   "wait kernel");
+        // Fused reduce-scatter + update over NVLink (OP_UPDATE becomes a no-op);
+        // it waits in-kernel for every rank's pack of this bucket.
         cuda_check(launch_rs_update_peer(B->upd_u, B->upd_ps, B->e_upd, hp_dev, B->mom_init ? 1 : 0,
                                          cfg.momentum != 0.0, cfg.weight_decay != 0.0, pa,
                                          B->flags, comm_stream),
@@ -432,9 +429,8 @@ void dear_ctx::exec(const Op& op) {
     case OP_AG:
       if (!local) record_t(op.bucket, T_AG0);
       if (peer) {
-        // Fused all-gather + unpack over NVLink (OP_UNPACK becomes a no-op).
-        cuda_check(launch_wait_peers(&B->flags->updated, &B->flags->updated, pa, comm_stream),
-                   "wait kernel");
+        // Fused all-gather + unpack over NVLink (OP_UNPACK becomes a no-op);
+        // it waits in-kernel for every owner's update of this bucket.
         cuda_check(launch_ag_unpack_peer(B->unpack_u, B->unpack_ps, B->e_unpack,
                                          B->any_shadow ? 1 : 0, pa, B->flags, comm_stream),
                    "ag+unpack kernel");

@@ -49,7 +49,8 @@ def main():
                            wl["batch"] * wl["tokens_per_sample"], seed=1234)
     stream = torch.cuda.Stream()
     ns = argparse.Namespace(group_dependency=a.group_dependency, buffer=a.buffer, lr=0.05,
-                            momentum=0.0, backend=a.backend, contention=a.contention)
+                            momentum=0.0, backend=a.backend, contention=a.contention,
+                            order_search=1)
     rt = bench.make_runtime(ns, model, comm, rank, world, stream, a.policy, True)
     # external: recorded inside the graph capture, timed after a replay
     ev = {k: torch.cuda.Event(enable_timing=True, external=True)
