@@ -395,9 +395,14 @@ def gpu_arm(a, wl, world, rank, local_rank):
     buckets = rt.buckets()
     run = make_runner(Step(model, rt, stream), use_graph, stream)
     if a.profile_steps:
+        run()  # warm
+        torch.cuda.synchronize()
+        # ncu --nvtx --nvtx-include "dear_profile/" selects exactly these steps
+        torch.cuda.nvtx.range_push("dear_profile")
         for _ in range(a.profile_steps):
             run()
         torch.cuda.synchronize()
+        torch.cuda.nvtx.range_pop()
         rt.synchronize()
         if rank == 0:
             print(json.dumps({"profile_steps": a.profile_steps}), flush=True)
@@ -502,7 +507,7 @@ def gpu_arm(a, wl, world, rank, local_rank):
                                    3 * len(buckets)),
         "roofline": {"bound": "tensor", "kernel": "tcgen05 GEMM chain (FF + grouped wgrad/dgrad)",
                      "achieved": gemm_achieved, "peak": tf_sus, "unit": "TFLOP/s",
-                     "frac": gemm_achieved / tf_sus, "traffic": None,
+                     "frac": gemm_achieved / tf_sus, "traffic": _ncu_traffic(a.workload),
                      "peak_kind": f"{peak_kind} sustained",
                      "flops_per_step": gemm_flops, "gemm_ms_per_step": res["compute_ms"],
                      "isolated_launch_tflops": gemm_isolated},
@@ -526,6 +531,18 @@ def gpu_arm(a, wl, world, rank, local_rank):
     if world == 1 and not a.no_cpu:
         line["cpu_baseline"] = reference_arm(a, wl, world, rank, emit=False)
     return line
+
+
+def _ncu_traffic(workload):
+    """DRAM bytes per GEMM launch from the committed ncu --set full capture
+    (profiles/r01_ncu_traffic.json), or None when none was taken for this workload."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                        "r01_ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f)[workload]["gemm_traffic_bytes_per_launch"]
+    except (OSError, KeyError, ValueError):
+        return None
 
 
 def _time_gemms(model, rt, stream):
