@@ -43,6 +43,8 @@ constexpr int kSlices = 148 * DEAR_SLICES_PER_SM;
 #define DEAR_PEER_SLICES 64
 #endif
 constexpr int kPeerSlices = DEAR_PEER_SLICES;
+// Peer-backend pack: one CTA per SM, one contiguous slice per CTA.
+constexpr int kPackPeerSlices = 148;
 
 struct Slice {
   Unit first;     // the slice's first piece, pointers pre-offset (one load per CTA)
@@ -114,8 +116,9 @@ struct BucketFlags {
 cudaError_t launch_wait_peers(const uint32_t* mine, const uint32_t* watch, const PeerArgs& pa,
                               cudaStream_t s);
 // pack with a completion signal (flags->packed += 1 after all CTAs finish).
+// `slices` holds kPackPeerSlices entries (one per CTA).
 cudaError_t launch_pack_signal(const Unit* units, const Slice* slices, int64_t total, float scale,
-                               BucketFlags* flags, const PeerArgs& pa, int grid, cudaStream_t s);
+                               BucketFlags* flags, const PeerArgs& pa, cudaStream_t s);
 // Fused reduce-scatter + shard SGD update: for each own-shard element, sum the
 // peers' slot-`rank` values in ring order (rank+1, ..., rank), update, write
 // w' into the own slot; then flags->updated += 1.

@@ -186,11 +186,19 @@ __device__ __forceinline__ const T* at_peer(const T* p, int64_t delta) {
 }
 
 // Last CTA of the launch bumps `counter` (release, system scope) once every
-// CTA's writes are globally visible.
+// CTA's writes are visible. Each CTA orders its writes before its `done`
+// increment at GPU scope (peers read this GPU's memory through its L2); the
+// last CTA, which observed every increment, then releases at system scope,
+// which is cumulative over what it observed (PTX memory model), so one
+// system-scope fence per launch suffices.
 __device__ __forceinline__ void signal_done(uint32_t* done, uint32_t* counter) {
   __syncthreads();
   if (threadIdx.x == 0) {
+#ifdef DEAR_SIGNAL_SYS_FENCE_ALL
     __threadfence_system();
+#else
+    __threadfence();
+#endif
     const uint32_t prev = atomicAdd(done, 1u);
     if (prev == gridDim.x - 1) {
       *done = 0;
@@ -232,9 +240,11 @@ __device__ __forceinline__ void cta_wait_peers(const uint32_t* mine, const uint3
       }
     }
     __syncwarp();
+#ifdef DEAR_WAIT_SYS_FENCE
     asm volatile("fence.acq_rel.sys;" ::: "memory");
+#endif
   }
-  __syncthreads();
+  __syncthreads();  // the acquires of warp 0 order the whole CTA's later reads
 }
 
 // ---------------------------------------------------------------- pack ----
@@ -244,17 +254,22 @@ __device__ __forceinline__ void cta_wait_peers(const uint32_t* mine, const uint3
 #define DEAR_PACK_PEER_UNROLL 16
 #endif
 constexpr int kPackPeerUnroll = DEAR_PACK_PEER_UNROLL;
+#ifdef DEAR_PEER_PACK_FULL
+constexpr bool kPeerPackLight = false;  // experiment: peer pack on the full grid
+#else
+constexpr bool kPeerPackLight = true;
+#endif
 template <bool kSignal>
-__global__ void __launch_bounds__(kThreads, kSignal ? 1 : kCtasPerSm) pack_kernel(const Unit* __restrict__ units,
+__global__ void __launch_bounds__(kThreads, (kSignal && kPeerPackLight) ? 1 : kCtasPerSm) pack_kernel(const Unit* __restrict__ units,
                                                            const Slice* __restrict__ slices,
                                                            float scale, BucketFlags* flags,
-                                                           PeerArgs pa) {
+                                                           PeerArgs pa, int n_slices) {
   // Peer backend: our slots may be rewritten once every peer gathered them.
   if (kSignal) cta_wait_peers(&flags->packed, &flags->gathered, pa);
-  walk_slice(units, slices, kSlices, [&](const Unit& U, int64_t off, int64_t n) {
+  walk_slice(units, slices, n_slices, [&](const Unit& U, int64_t off, int64_t n) {
     const float* src = U.a + off;
     float* dst = U.b + off;
-    run_unit<Hint::kStream, kSignal ? kPackPeerUnroll : kUnroll>(
+    run_unit<Hint::kStream, (kSignal && kPeerPackLight) ? kPackPeerUnroll : kUnroll>(
         src, dst, n, [&](int64_t i) { dst[i] = __fmul_rn(src[i], scale); },
         [&](int64_t head, int64_t q, float4 v) {
           v.x = __fmul_rn(v.x, scale);
@@ -608,14 +623,19 @@ cudaError_t launch_pack(const Unit* units, const Slice* slices, int64_t total, f
                         int grid, cudaStream_t s) {
   if (total <= 0) return cudaSuccess;
   pack_kernel<false><<<bucket_grid(kSlices, grid), kThreads, 0, s>>>(units, slices, scale, nullptr,
-                                                                     PeerArgs{});
+                                                                     PeerArgs{}, kSlices);
   return cudaGetLastError();
 }
 
 cudaError_t launch_pack_signal(const Unit* units, const Slice* slices, int64_t total, float scale,
-                               BucketFlags* flags, const PeerArgs& pa, int grid, cudaStream_t s) {
+                               BucketFlags* flags, const PeerArgs& pa, cudaStream_t s) {
   (void)total;  // the signal must fire even for an empty bucket
-  pack_kernel<true><<<bucket_grid(kSlices, grid), kThreads, 0, s>>>(units, slices, scale, flags, pa);
+  if (kPeerPackLight)
+    pack_kernel<true><<<bucket_grid(kPackPeerSlices), kThreads, 0, s>>>(units, slices, scale, flags,
+                                                                       pa, kPackPeerSlices);
+  else
+    pack_kernel<true><<<bucket_grid(kSlices), kThreads, 0, s>>>(units, slices, scale, flags, pa,
+                                                                kSlices);
   return cudaGetLastError();
 }
 

@@ -36,18 +36,6 @@ namespace dear {
 
 namespace {
 
-// SMs of the (single) device this process drives; the peer-path pack runs one
-// CTA per SM.
-int sm_count() {
-  static const int n = [] {
-    int d = 0, v = 0;
-    if (cudaGetDevice(&d) != cudaSuccess ||
-        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d) != cudaSuccess || v <= 0)
-      v = 148;
-    return v;
-  }();
-  return n;
-}
 thread_local std::string g_last_error;
 }
 
@@ -112,6 +100,7 @@ struct Bucket {
   int64_t e_pack = 0, e_upd = 0, e_unpack = 0;  // elements per op
   Slice *pack_s = nullptr, *upd_s = nullptr, *unpack_s = nullptr;  // kSlices each
   Slice *upd_ps = nullptr, *unpack_ps = nullptr;  // kPeerSlices each (peer kernels)
+  Slice* pack_ps = nullptr;                        // kPackPeerSlices (peer pack)
   BucketFlags* flags = nullptr;  // peer backend completion counters (in the arena)
   bool any_shadow = false;
   bool mom_init = false;
@@ -388,11 +377,17 @@ void dear_ctx::exec(const Op& op) {
       record_t(op.bucket, T_PACK0);
       if (peer) {
         // The kernel first waits (in-kernel) until every peer gathered from
-        // our buffer, which it then rewrites. One CTA per SM: the pack overlaps backprop GEMMs and the fused peer
+        // our buffer, which it then rewrites. One CTA per SM, one contiguous
+        // slice each: the pack overlaps backprop GEMMs and the fused peer
         // kernels; a full 4-CTA/SM grid would hold every SM's register file
         // and stall the persistent GEMM (profiles/r01_n4_interference_matrix.log).
+#ifdef DEAR_PEER_PACK_FULL
         cuda_check(launch_pack_signal(B->pack_u, B->pack_s, B->e_pack, pack_scale, B->flags, pa,
-                                      sm_count(), comm_stream),
+                                      comm_stream),
+#else
+        cuda_check(launch_pack_signal(B->pack_u, B->pack_ps, B->e_pack, pack_scale, B->flags, pa,
+                                      comm_stream),
+#endif
                    "pack kernel");
       } else {
         cuda_check(launch_pack(B->pack_u, B->pack_s, B->e_pack, pack_scale, 0, comm_stream),
@@ -765,7 +760,8 @@ int dear_finalize(dear_ctx* ctx) {
   }
   const size_t float_bytes = (floats * sizeof(float) + 255) / 256 * 256;
   const size_t unit_bytes = (units * sizeof(Unit) + 255) / 256 * 256;
-  const size_t per_bucket_slices = 3 * static_cast<size_t>(kSlices) + 2 * kPeerSlices;
+  const size_t per_bucket_slices =
+      3 * static_cast<size_t>(kSlices) + 2 * kPeerSlices + kPackPeerSlices;
   const size_t n_slices = plan.size() * per_bucket_slices;
   const size_t slice_bytes = (n_slices * sizeof(Slice) + 255) / 256 * 256;
   // Layout: [bucket buffers + momentum][flags] is identical on every rank (the
@@ -846,11 +842,14 @@ int dear_finalize(dear_ctx* ctx) {
                 kPeerSlices, 4);
     make_slices(host_units.data() + (B.unpack_u - up), B.n_unpack, B.e_unpack,
                 hs + 3 * kSlices + kPeerSlices, kPeerSlices, 2);
+    make_slices(host_units.data() + (B.pack_u - up), B.n_pack, B.e_pack,
+                hs + 3 * kSlices + 2 * kPeerSlices, kPackPeerSlices, 0);
     B.pack_s = sp + g * per_bucket_slices;
     B.upd_s = B.pack_s + kSlices;
     B.unpack_s = B.upd_s + kSlices;
     B.upd_ps = B.unpack_s + kSlices;
     B.unpack_ps = B.upd_ps + kPeerSlices;
+    B.pack_ps = B.unpack_ps + kPeerSlices;
     B.ag_done = new_event(false);
     for (int k = 0; k < T_COUNT; ++k) B.t[k] = new_event(true);
     B.layers_left = B.high - B.low + 1;
