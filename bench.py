@@ -578,7 +578,13 @@ def _isolated_stage_times(model, runtime, stream, policy):
     back to back, so the comm stream runs the bucket kernels alone."""
     import torch
 
-    rt = runtime(policy)
+    # DEAR_DIRECT=0: at P = 1 keep the separate pack / update / unpack kernels
+    # (what every P > 1 bucket runs) instead of the fused direct update.
+    os.environ["DEAR_DIRECT"] = "0"
+    try:
+        rt = runtime(policy)
+    finally:
+        os.environ.pop("DEAR_DIRECT", None)
     rt.set_timing(True)
     for it in range(3):
         with torch.cuda.stream(stream):
@@ -615,21 +621,40 @@ def compare_policies(a, wl_name, comm, world, rank, stream):
     steps, warm = max(5, a.steps // 2), max(3, a.warmup)
     out = {"workload": wl["config"], "batch_per_gpu": batch, "fusion_buffer_bytes": a.buffer,
            "steps": steps, "warmup": warm}
-    for policy in (a.policy, a.baseline_policy):
-        rt = make_runtime(a, model, comm, rank, world, stream, policy, True)
-        if rt.comm_order_info:
-            out["comm_order"] = rt.comm_order_info
-        run = make_runner(Step(model, rt, stream), True, stream)
-        ms = time_loop(run, steps, warm, stream, dist_on)
-        rt.synchronize()
-        rt.close()
-        out[policy] = {"ms_per_step": ms, "samples_per_s": batch * world / (ms / 1e3)}
     run = make_runner(Step(model, None, stream), True, stream)
     comp = time_loop(run, steps, warm, stream, dist_on)
-    d, w = out[a.policy]["ms_per_step"], out[a.baseline_policy]["ms_per_step"]
-    out.update({"compute_only_ms": comp, "dear_over_wfbp": w / d,
-                "exposed_comm_pct": max(0.0, 100 * (d - comp) / d),
-                "wfbp_exposed_comm_pct": max(0.0, 100 * (w - comp) / w)})
+    out["compute_only_ms"] = comp
+    # The resolved default backend first; with N > 1 also NCCL, the north
+    # star's named transport (DeAR's edge over WFBP grows with comm cost).
+    backends = [None]
+    if world > 1 and a.backend != "nccl":
+        backends.append("nccl")
+    import argparse
+    for be in backends:
+        ab = argparse.Namespace(**vars(a))
+        if be is not None:
+            ab.backend = be
+        res = {}
+        for policy in (a.policy, a.baseline_policy):
+            rt = make_runtime(ab, model, comm, rank, world, stream, policy, True)
+            used = rt.backend
+            if rt.comm_order_info:
+                res["comm_order"] = {k: v for k, v in rt.comm_order_info.items()
+                                     if k in ("ags_during_backprop", "contention")}
+            run = make_runner(Step(model, rt, stream), True, stream)
+            ms = time_loop(run, steps, warm, stream, dist_on)
+            rt.synchronize()
+            rt.close()
+            res[policy] = {"ms_per_step": ms, "samples_per_s": batch * world / (ms / 1e3)}
+        d, w = res[a.policy]["ms_per_step"], res[a.baseline_policy]["ms_per_step"]
+        res.update({"dear_over_wfbp": w / d,
+                    "exposed_comm_pct": max(0.0, 100 * (d - comp) / d),
+                    "wfbp_exposed_comm_pct": max(0.0, 100 * (w - comp) / w)})
+        if be is None:
+            res["collectives"] = used
+            out.update(res)
+        else:
+            out["nccl"] = res
     model.close()
     del model
     torch.cuda.empty_cache()

@@ -116,6 +116,10 @@ struct BucketFlags {
 cudaError_t launch_wait_peers(const uint32_t* mine, const uint32_t* watch, const PeerArgs& pa,
                               cudaStream_t s);
 // pack with a completion signal (flags->packed += 1 after all CTAs finish).
+// P = 1, no momentum: w <- sgd(w, grad) and the bf16 copy, from the layers.
+cudaError_t launch_update_direct(const Unit* units, const Slice* slices, int64_t total,
+                                 const HyperParams* hp, int use_wd, int with_shadow,
+                                 cudaStream_t s);
 // `slices` holds kPackPeerSlices entries (one per CTA).
 cudaError_t launch_pack_signal(const Unit* units, const Slice* slices, int64_t total, float scale,
                                BucketFlags* flags, const PeerArgs& pa, cudaStream_t s);

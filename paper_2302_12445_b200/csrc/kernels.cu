@@ -332,6 +332,49 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) update_kernel(const Unit
   });
 }
 
+// ------------------------------------------------------- direct (P = 1) ---
+// One rank: the reduce-scatter and all-gather are the identity, so the
+// parameters are updated straight from the gradients (and the bf16 copy
+// refreshed) — 14 B per element. Same per-element operations as update_kernel
+// (sum * 1/P with P = 1 is exact), so the result is bit-identical.
+template <bool kWd, bool kShadow>
+__global__ void __launch_bounds__(kThreads, kCtasPerSm) update_direct_kernel(
+    const Unit* __restrict__ units, const Slice* __restrict__ slices,
+    const HyperParams* __restrict__ hpp) {
+  const HyperParams hp = *hpp;
+  walk_slice(units, slices, kSlices, [&](const Unit& U, int64_t off, int64_t n) {
+    const float* g = U.a + off;
+    float* w = U.b + off;
+    __nv_bfloat16* sh = (kShadow && U.c) ? static_cast<__nv_bfloat16*>(U.c) + off : nullptr;
+    run_unit<Hint::kStream>(
+        g, w, n,
+        [&](int64_t i) {
+          float m = 0.f;
+          const float v = sgd_elem<false, kWd>(g[i], w[i], m, hp, false);
+          w[i] = v;
+          if (kShadow && sh) sh[i] = __float2bfloat16_rn(v);
+        },
+        [&](int64_t head, int64_t q, float4 gv) {
+          float4* w4 = reinterpret_cast<float4*>(w + head);
+          float4 v = w4[q];
+          float m = 0.f;
+          v.x = sgd_elem<false, kWd>(gv.x, v.x, m, hp, false);
+          v.y = sgd_elem<false, kWd>(gv.y, v.y, m, hp, false);
+          v.z = sgd_elem<false, kWd>(gv.z, v.z, m, hp, false);
+          v.w = sgd_elem<false, kWd>(gv.w, v.w, m, hp, false);
+          w4[q] = v;
+          if (kShadow && sh) {
+            __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y);
+            __nv_bfloat162 hi = __floats2bfloat162_rn(v.z, v.w);
+            uint2 packed;
+            packed.x = *reinterpret_cast<uint32_t*>(&lo);
+            packed.y = *reinterpret_cast<uint32_t*>(&hi);
+            reinterpret_cast<uint2*>(sh + head)[q] = packed;
+          }
+        });
+  });
+}
+
 // -------------------------------------------------------------- unpack ----
 template <bool kShadow>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm) unpack_kernel(const Unit* __restrict__ units,
@@ -709,6 +752,22 @@ cudaError_t launch_unpack(const Unit* units, const Slice* slices, int64_t total,
     unpack_kernel<true><<<ug, kThreads, 0, s>>>(units, slices);
   else
     unpack_kernel<false><<<ug, kThreads, 0, s>>>(units, slices);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_update_direct(const Unit* units, const Slice* slices, int64_t total,
+                                 const HyperParams* hp, int use_wd, int with_shadow,
+                                 cudaStream_t s) {
+  if (total <= 0) return cudaSuccess;
+  const int grid = bucket_grid(kSlices);
+  if (use_wd && with_shadow)
+    update_direct_kernel<true, true><<<grid, kThreads, 0, s>>>(units, slices, hp);
+  else if (use_wd)
+    update_direct_kernel<true, false><<<grid, kThreads, 0, s>>>(units, slices, hp);
+  else if (with_shadow)
+    update_direct_kernel<false, true><<<grid, kThreads, 0, s>>>(units, slices, hp);
+  else
+    update_direct_kernel<false, false><<<grid, kThreads, 0, s>>>(units, slices, hp);
   return cudaGetLastError();
 }
 

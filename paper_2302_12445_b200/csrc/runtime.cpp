@@ -21,6 +21,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <deque>
 #include <map>
@@ -101,6 +102,10 @@ struct Bucket {
   Slice *pack_s = nullptr, *upd_s = nullptr, *unpack_s = nullptr;  // kSlices each
   Slice *upd_ps = nullptr, *unpack_ps = nullptr;  // kPeerSlices each (peer kernels)
   Slice* pack_ps = nullptr;                        // kPackPeerSlices (peer pack)
+  Unit* dir_u = nullptr;                           // P = 1 direct update (grad -> param)
+  int n_dir = 0;
+  int64_t e_dir = 0;
+  Slice* dir_s = nullptr;                          // kSlices
   BucketFlags* flags = nullptr;  // peer backend completion counters (in the arena)
   bool any_shadow = false;
   bool mom_init = false;
@@ -156,6 +161,10 @@ struct dear_ctx {
   unsigned long long* hash_dev = nullptr;
   size_t arena_bytes = 0;
   bool peer = false;             // NVLink peer backend (fused RS+update, AG+unpack)
+  // P = 1 without momentum: the reduce-scatter / all-gather are the identity,
+  // so one kernel updates the parameters (and their bf16 copy) straight from
+  // the gradients — 14 B/element instead of pack + update + unpack's 30.
+  bool direct = false;
   PeerArgs pa{};
   std::vector<void*> peer_maps;  // cudaIpcOpenMemHandle mappings to close
   bool timing = false;
@@ -374,6 +383,7 @@ void dear_ctx::exec(const Op& op) {
       cuda_check(cudaStreamWaitEvent(comm_stream, step_ev, 0), "cudaStreamWaitEvent");
       break;
     case OP_PACK:
+      if (direct) break;  // P = 1: the update reads the gradients in place
       record_t(op.bucket, T_PACK0);
       if (peer) {
         // The kernel first waits (in-kernel) until every peer gathered from
@@ -415,6 +425,15 @@ void dear_ctx::exec(const Op& op) {
       break;
     case OP_UPDATE:
       if (peer) break;
+      if (direct) {
+        cuda_check(launch_update_direct(B->dir_u, B->dir_s, B->e_dir, hp_dev,
+                                        cfg.weight_decay != 0.0, B->any_shadow ? 1 : 0,
+                                        comm_stream),
+                   "direct update kernel");
+        cuda_check(cudaEventRecord(packed_ev, comm_stream), "cudaEventRecord");
+        record_t(op.bucket, T_UPD1);
+        break;
+      }
       cuda_check(launch_update(B->upd_u, B->upd_s, B->e_upd, hp_dev, B->mom_init ? 1 : 0,
                                cfg.momentum != 0.0, cfg.weight_decay != 0.0, 0, comm_stream),
                  "update kernel");
@@ -437,7 +456,7 @@ void dear_ctx::exec(const Op& op) {
       record_t(op.bucket, T_AG1);
       break;
     case OP_UNPACK:
-      if (peer) break;
+      if (peer || direct) break;
       cuda_check(launch_unpack(B->unpack_u, B->unpack_s, B->e_unpack, B->any_shadow ? 1 : 0, 0,
                                comm_stream),
                  "unpack kernel");
@@ -738,6 +757,10 @@ int dear_finalize(dear_ctx* ctx) {
     B.stride = slot_stride(B.d, c.P);
     floats += static_cast<size_t>(B.stride) * static_cast<size_t>(c.P) + (mom ? static_cast<size_t>(B.stride) : 0);
   }
+  // DEAR_DIRECT=0 keeps the pack/update/unpack kernels at P = 1 (tools that
+  // measure those kernels on one GPU).
+  const char* dir_env = std::getenv("DEAR_DIRECT");
+  c.direct = c.P == 1 && !c.peer && c.cfg.momentum == 0.0 && !(dir_env && dir_env[0] == '0');
   // Unit tables.
   std::vector<Unit> host_units;
   struct Span { size_t pack, upd, unpack; };
@@ -756,12 +779,12 @@ int dear_finalize(dear_ctx* ctx) {
     size_t nu = 0;
     for_each_piece(c, B, bg[static_cast<size_t>(own)], bg[static_cast<size_t>(own) + 1],
                    [&](int, int64_t, int64_t, int64_t) { ++nu; });
-    units += 2 * n + nu;
+    units += 2 * n + nu + (c.direct ? n : 0);
   }
   const size_t float_bytes = (floats * sizeof(float) + 255) / 256 * 256;
   const size_t unit_bytes = (units * sizeof(Unit) + 255) / 256 * 256;
-  const size_t per_bucket_slices =
-      3 * static_cast<size_t>(kSlices) + 2 * kPeerSlices + kPackPeerSlices;
+  const size_t per_bucket_slices = 3 * static_cast<size_t>(kSlices) + 2 * kPeerSlices +
+                                   kPackPeerSlices + (c.direct ? kSlices : 0);
   const size_t n_slices = plan.size() * per_bucket_slices;
   const size_t slice_bytes = (n_slices * sizeof(Slice) + 255) / 256 * 256;
   // Layout: [bucket buffers + momentum][flags] is identical on every rank (the
@@ -832,6 +855,17 @@ int dear_finalize(dear_ctx* ctx) {
     }
     B.n_unpack = static_cast<int>(host_units.size() - static_cast<size_t>(B.unpack_u - up));
     B.e_unpack = set_starts(host_units, static_cast<size_t>(B.unpack_u - up));
+    if (c.direct) {
+      // P = 1: gradient -> parameter (+ bf16 copy), layer by layer.
+      B.dir_u = up + host_units.size();
+      for_each_piece(c, B, bg[0], bg[1], [&](int l, int64_t j, int64_t len, int64_t) {
+        const LayerReg& R = c.layers[static_cast<size_t>(l - 1)];
+        void* sh = R.shadow ? static_cast<void*>(static_cast<uint16_t*>(R.shadow) + j) : nullptr;
+        host_units.push_back({R.grad + j, R.param + j, sh, len, 0, 0, 0});
+      });
+      B.n_dir = static_cast<int>(host_units.size() - static_cast<size_t>(B.dir_u - up));
+      B.e_dir = set_starts(host_units, static_cast<size_t>(B.dir_u - up));
+    }
     // Equal element slices per CTA for each op (one wave of kSlices CTAs).
     Slice* hs = host_slices.data() + g * per_bucket_slices;
     make_slices(host_units.data() + (B.pack_u - up), B.n_pack, B.e_pack, hs, kSlices, 0);
@@ -844,12 +878,16 @@ int dear_finalize(dear_ctx* ctx) {
                 hs + 3 * kSlices + kPeerSlices, kPeerSlices, 2);
     make_slices(host_units.data() + (B.pack_u - up), B.n_pack, B.e_pack,
                 hs + 3 * kSlices + 2 * kPeerSlices, kPackPeerSlices, 0);
+    if (c.direct)
+      make_slices(host_units.data() + (B.dir_u - up), B.n_dir, B.e_dir,
+                  hs + 3 * kSlices + 2 * kPeerSlices + kPackPeerSlices, kSlices, 2);
     B.pack_s = sp + g * per_bucket_slices;
     B.upd_s = B.pack_s + kSlices;
     B.unpack_s = B.upd_s + kSlices;
     B.upd_ps = B.unpack_s + kSlices;
     B.unpack_ps = B.upd_ps + kPeerSlices;
     B.pack_ps = B.unpack_ps + kPeerSlices;
+    B.dir_s = c.direct ? B.pack_ps + kPackPeerSlices : nullptr;
     B.ag_done = new_event(false);
     for (int k = 0; k < T_COUNT; ++k) B.t[k] = new_event(true);
     B.layers_left = B.high - B.low + 1;

@@ -28,6 +28,9 @@ def main():
     a = ap.parse_args()
     import torch
 
+    # keep the separate pack / update / unpack kernels at P = 1 (not the fused
+    # direct update), which is what every P > 1 bucket runs
+    os.environ.setdefault("DEAR_DIRECT", "0")
     import paper_2302_12445_b200 as dear
     from paper_2302_12445_b200.presets import preset_param_counts
 
