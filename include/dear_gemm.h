@@ -58,6 +58,9 @@ int dear_gemm_plan_cluster(dear_gemm_plan* plan, int32_t* cm, int32_t* cn, int32
  * single-CTA (pair = 0) or 2-CTA pair (pair = 1) tiles; multicast clusters
  * off. Used by the plan-time autotuner (paper_2302_12445_b200.gemm.autotune). */
 int dear_gemm_plan_set_tile(dear_gemm_plan* plan, int32_t bn, int32_t pair);
+/* Override the split-K count of an accumulating plan (>= 1; clipped to the
+ * number of 64-deep k-blocks). */
+int dear_gemm_plan_set_splits(dear_gemm_plan* plan, int32_t split_k);
 int dear_gemm_plan_set_flags(dear_gemm_plan* plan, int32_t flags);
 /* 1 when the plan runs as 2-CTA pairs (cta_group::2 MMAs on 256-row tiles;
  * reported by dear_gemm_plan_cluster as cm = 2, cn = 1), else 0. */

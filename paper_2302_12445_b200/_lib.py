@@ -116,7 +116,7 @@ def check(rc: int) -> None:
 
 GEMM_SYMBOLS = ["dear_gemm_plan_create", "dear_gemm_run", "dear_gemm_run_group",
                 "dear_gemm_plan_info", "dear_gemm_plan_cluster", "dear_gemm_plan_pair",
-                "dear_gemm_plan_set_flags", "dear_gemm_plan_set_tile",
+                "dear_gemm_plan_set_flags", "dear_gemm_plan_set_tile", "dear_gemm_plan_set_splits",
                 "dear_gemm_set_trace",
                 "dear_gemm_plan_destroy"]  # bound in gemm.py
 

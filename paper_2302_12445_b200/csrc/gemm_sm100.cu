@@ -1041,6 +1041,21 @@ int dear_gemm_plan_set_tile(dear_gemm_plan* plan, int32_t bn, int32_t pair) {
   DEAR_API_END
 }
 
+int dear_gemm_plan_set_splits(dear_gemm_plan* plan, int32_t split_k) {
+  DEAR_API_BEGIN
+  using namespace dear::gemm;
+  if (!plan) throw Error(DEAR_EINVAL, "null plan");
+  Problem& p = plan->p;
+  if (split_k < 1) throw Error(DEAR_EINVAL, "dear_gemm_plan_set_splits: split_k must be >= 1");
+  if (split_k > 1 && !p.accumulate)
+    throw Error(DEAR_EINVAL, "dear_gemm_plan_set_splits: split_k > 1 needs accumulate");
+  const int splits = std::min<int>(split_k, p.num_kb);
+  p.kb_per_split = (p.num_kb + splits - 1) / splits;
+  p.splits = (p.num_kb + p.kb_per_split - 1) / p.kb_per_split;
+  configure(plan, TileChoice{p.bn, p.pair ? 2 : p.cm, p.pair ? 1 : p.cn, p.pair});
+  DEAR_API_END
+}
+
 int dear_gemm_plan_set_flags(dear_gemm_plan* plan, int32_t flags) {
   DEAR_API_BEGIN
   if (!plan) throw Error(DEAR_EINVAL, "null plan");

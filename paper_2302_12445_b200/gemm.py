@@ -32,10 +32,12 @@ def _bind():
     L.dear_gemm_plan_pair.argtypes = [P, C.POINTER(C.c_int32)]
     L.dear_gemm_plan_set_flags.argtypes = [P, C.c_int32]
     L.dear_gemm_plan_set_tile.argtypes = [P, C.c_int32, C.c_int32]
+    L.dear_gemm_plan_set_splits.argtypes = [P, C.c_int32]
     L.dear_gemm_set_trace.argtypes = [P]
     for f in ("dear_gemm_plan_create", "dear_gemm_run", "dear_gemm_run_group",
               "dear_gemm_plan_info", "dear_gemm_plan_cluster", "dear_gemm_plan_pair",
-              "dear_gemm_plan_set_flags", "dear_gemm_plan_set_tile", "dear_gemm_set_trace",
+              "dear_gemm_plan_set_flags", "dear_gemm_plan_set_tile", "dear_gemm_plan_set_splits",
+              "dear_gemm_set_trace",
               "dear_gemm_plan_destroy"):
         getattr(L, f).restype = C.c_int
     _bound = True
@@ -105,6 +107,10 @@ class GemmPlan:
     def set_tile(self, bn: int, pair: bool) -> None:
         """Override the cost model's tile choice (dear_gemm_plan_set_tile)."""
         check(_bind().dear_gemm_plan_set_tile(self._plan, int(bn), int(bool(pair))))
+
+    def set_splits(self, split_k: int) -> None:
+        """Override the split-K count of an accumulating plan."""
+        check(_bind().dear_gemm_plan_set_splits(self._plan, int(split_k)))
 
     @staticmethod
     def run_group(plans: "list[GemmPlan]", stream: torch.cuda.Stream | None = None) -> None:

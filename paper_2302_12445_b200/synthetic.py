@@ -38,7 +38,7 @@ def _round_up(x: int, m: int) -> int:
 
 class SyntheticModel:
     def __init__(self, numels: list[int], hidden: int, tokens: int, device="cuda", seed: int = 0,
-                 tune: bool = True):
+                 tune: bool = True, wgrad_split: int = 0):
         self.numels = [int(n) for n in numels]
         self.L = len(self.numels)
         self.H = int(hidden)
@@ -77,6 +77,7 @@ class SyntheticModel:
         self.dyt = self.dy.t().contiguous()
         self.y = torch.empty(T, self.rpad, dtype=torch.bfloat16, device=dev)
         self.dx = torch.empty(T, H, dtype=torch.bfloat16, device=dev)
+        self.wgrad_split = int(wgrad_split)
         self._build_plans()
         self.tiles = self.tune_tiles() if tune else None
 
@@ -96,15 +97,16 @@ class SyntheticModel:
                                        lda=self.rpad, ldb=H, ldd=H, early_operands=True))
             self.wgrad.append(GemmPlan(self.dyt, self.xt, self.grads[l] if n > 0 else self.grads_flat,
                                        R, H, T, lda=T, ldb=T, ldd=H, d_limit=n,
-                                       accumulate=True, early_operands=True))
+                                       accumulate=True, early_operands=True,
+                                       split_k=self.wgrad_split))
 
     def tune_tiles(self, chain: int = 16) -> dict:
         """Plan-time tile autotuning (gemm.autotune): FF as a chain of FF
-        launches, backprop as a chain of grouped wgrad+dgrad launches (top-3 x
-        top-3 of the per-GEMM chains), on this model's own layer shapes. The
-        weight-gradient candidates run on a scratch output; FF / dgrad outputs
-        are synthetic scratch already. Runs once, outside any timed region."""
-        from .gemm import autotune, autotune_group, tile_candidates
+        launches; wgrad (scratch output) and dgrad as chains of their own to
+        rank tiles, then backprop on the real chain of grouped launches over
+        every layer (top-2 x top-2 tiles x split-K counts). Runs once, outside
+        any timed region; the gradients are zeroed afterwards."""
+        from .gemm import autotune, tile_candidates
 
         H, T = self.H, self.T
         k = min(self.L, 8)
@@ -115,21 +117,53 @@ class SyntheticModel:
         dg = autotune(self.dgrad[:k], tile_candidates(T, H, True), chain, s)
         scratch = torch.zeros(n + 64, device=self.x.device)
         wgs = [GemmPlan(self.dyt, self.xt, scratch, R, H, T, lda=T, ldb=T, ldd=H, d_limit=n,
-                        accumulate=True, early_operands=True)]
+                        accumulate=True, early_operands=True, split_k=self.wgrad_split)]
         wg = autotune(wgs, tile_candidates(R, H, False), chain, s)
-        grp = autotune_group(wgs, self.dgrad[:k], [c[1:] for c in wg[:3]],
-                             [c[1:] for c in dg[:3]], chain, s)
-        best_ff, (best_wg, best_dg) = ff[0][1:], grp[0][1:]
+        best_ff = ff[0][1:]
         for l in range(self.L):
             self.ff[l].set_tile(*best_ff)
-            self.dgrad[l].set_tile(*best_dg)
-            self.wgrad[l].set_tile(*best_wg)
         wgs[0].close()
+        # Backprop on the real chain: every layer's grouped wgrad+dgrad into
+        # the real (freshly zeroed, mostly cold) gradients, as in a step. The
+        # scratch chain above cannot see the split-K reductions' cost on cold
+        # lines, so tiles (top-2 x top-2) and the split count are chosen here.
+        from .gemm import time_chain
+
+        L = self.L
+        split0 = self.wgrad[0].info()["splits"]
+        num_kb = (T + 63) // 64
+        splits = ([self.wgrad_split] if self.wgrad_split > 0 else
+                  sorted({x for x in (split0, 4, 6, 8, 12) if 1 <= x <= num_kb}))
+
+        def bp_real(i):
+            if i == 0:
+                self.zero_grad()
+            l = L - 1 - (i % L)
+            GemmPlan.run_group([self.wgrad[l], self.dgrad[l]], s)
+
+        trials = []
+        for wc in [c[1:] for c in wg[:2]]:
+            for dc in [c[1:] for c in dg[:2]]:
+                for sp in splits:
+                    for l in range(L):
+                        self.wgrad[l].set_tile(*wc)
+                        self.wgrad[l].set_splits(sp)
+                        self.dgrad[l].set_tile(*dc)
+                    trials.append((time_chain(bp_real, L, s, reps=2), wc, dc, sp))
+        trials.sort(key=lambda t: t[0])
+        us, best_wg, best_dg, best_sp = trials[0]
+        for l in range(L):
+            self.wgrad[l].set_tile(*best_wg)
+            self.wgrad[l].set_splits(best_sp)
+            self.dgrad[l].set_tile(*best_dg)
+        self.zero_grad()
+        torch.cuda.synchronize()
         return {"ff": {"bn": best_ff[0], "pair": best_ff[1], "us": round(ff[0][0], 2)},
-                "wgrad": {"bn": best_wg[0], "pair": best_wg[1]},
+                "wgrad": {"bn": best_wg[0], "pair": best_wg[1], "splits": best_sp},
                 "dgrad": {"bn": best_dg[0], "pair": best_dg[1]},
-                "bp_group_us": round(grp[0][0], 2),
-                "candidates": {"ff": len(ff), "wgrad": len(wg), "dgrad": len(dg)}}
+                "bp_group_us": round(us, 2),
+                "candidates": {"ff": len(ff), "wgrad": len(wg), "dgrad": len(dg),
+                               "bp_real_chain": len(trials)}}
 
     def gemm_launches_per_step(self) -> int:
         bp = sum(1 if w.info()["pair"] == d.info()["pair"] else 2

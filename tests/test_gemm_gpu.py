@@ -77,6 +77,15 @@ def test_gemm_splitk_accumulate_flat_limit(M, N, K):
     ref = (a.float() @ b.float().t()).reshape(-1)[:limit] + base
     _check(flat[:limit], ref, K)
     assert torch.all(flat[limit:] == 12345.0)
+    # split-K override (plan-time tuner): accumulates once more, same result
+    plan.set_splits(3)
+    nkb = (K + 63) // 64
+    per = -(-nkb // min(3, nkb))
+    assert plan.info()["splits"] == -(-nkb // per)  # equal k-block ranges
+    plan.run()
+    torch.cuda.synchronize()
+    _check(flat[:limit], ref + (a.float() @ b.float().t()).reshape(-1)[:limit], K)
+    assert torch.all(flat[limit:] == 12345.0)
 
 
 @pytest.mark.parametrize("M,N,K", [(4096, 825, 1024), (200, 72, 128)])
