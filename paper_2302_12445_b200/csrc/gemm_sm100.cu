@@ -44,7 +44,11 @@ constexpr int kRingBytes = 4 * (kAStage + kBStage);  // 192 KB: 4..8 stages by B
 constexpr int kThreads = 192;
 constexpr int kAccCols = 256;
 constexpr int kTmemCols = 2 * kAccCols;
-constexpr int kSmemBytes = kRingBytes + 1024 + 256;
+// Epilogue staging for TMA stores: per epilogue warp two 32x32 bf16 buffers.
+constexpr int kEpiBufBytes = 32 * 32 * 2;
+constexpr int kEpiBytes = 4 * 2 * kEpiBufBytes;  // 16 KB
+constexpr int kEpiOffset = kRingBytes + 512;     // after the barriers, 512 B aligned
+constexpr int kSmemBytes = kEpiOffset + kEpiBytes + 1024;
 constexpr int kMaxProblems = 2;
 constexpr int kSms = 148;
 
@@ -85,6 +89,13 @@ struct alignas(64) Problem {
   // running when this GEMM starts (dear_gemm_plan_set_flags): the producer
   // then streams operands before griddepcontrol.wait; only stores wait.
   int32_t early_operands;
+  // bf16, non-accumulating D: the epilogue stages 32x32 chunks in smem and
+  // writes them with TMA bulk stores (full lines, asynchronous; TMA clips rows
+  // >= M and columns >= N). tmD: box 32x32, 64 B swizzle; tmD16: box 16x32 for
+  // the last 16 columns of a tile whose bn is an odd multiple of 16.
+  CUtensorMap tmD;
+  CUtensorMap tmD16;
+  int32_t d_tma;
 };
 
 struct Launch {
@@ -163,6 +174,27 @@ __device__ __forceinline__ void tma_load_2d_mc(const CUtensorMap* map, uint64_t*
       ".multicast::cluster [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
       : "memory");
+}
+
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int32_t c0,
+                                             int32_t c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
 __device__ __forceinline__ uint64_t globaltimer() {
@@ -440,6 +472,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
                    : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&L.p[i].tmB))
                    : "memory");
+      if (L.p[i].d_tma)
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&L.p[i].tmD))
+                     : "memory");
     }
   }
   if (warp == 1) {
@@ -593,6 +628,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   } else {
     const int q = warp & 3;
     uint32_t j = 0;
+    uint32_t epi_chunk = 0;  // TMA-store staging buffer parity
     for (int t = cid; t < L.total_tiles; t += ncl, ++j) {
       const TileCoord tc = decode(L, t, ci, cj);
       const Problem& P = L.p[tc.prob];
@@ -602,10 +638,63 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       const int64_t row = tc.m0 + 32 * q + lane;
       const int64_t col_end = min(P.N, tc.n0 + P.bn);
       const uint32_t base = tmem + acc * kAccCols + (static_cast<uint32_t>(32 * q) << 16);
-      for (int c = 0; c < P.bn; c += 32) {
-        uint32_t v[32];
-        tmem_ld32(base + static_cast<uint32_t>(c), v);
-        store_row_chunk(P, row, tc.n0 + c, col_end, v);
+      if (P.d_tma) {
+        // 32 rows x 32 columns per chunk: lane = row; bf16 row of 64 B in four
+        // 16 B pieces, piece j stored at j ^ ((row >> 1) & 3) (TMA 64 B swizzle;
+        // conflict-free smem writes). Double-buffered per warp.
+        uint8_t* epi = smem + kEpiOffset + q * 2 * kEpiBufBytes;
+        for (int c = 0; c < P.bn; c += 32, ++epi_chunk) {
+          uint32_t v[32];
+          tmem_ld32(base + static_cast<uint32_t>(c), v);
+          uint8_t* buf = epi + (epi_chunk & 1) * kEpiBufBytes;
+          if (lane == 0) bulk_wait_read<1>();  // this buffer's previous store read it
+          __syncwarp();
+          const bool half = P.bn - c == 16;  // a tile's odd last 16 columns
+          if (!half) {
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+              uint4 w;
+              __nv_bfloat162 h0 = __floats2bfloat162_rn(__uint_as_float(v[8 * jj]), __uint_as_float(v[8 * jj + 1]));
+              __nv_bfloat162 h1 = __floats2bfloat162_rn(__uint_as_float(v[8 * jj + 2]), __uint_as_float(v[8 * jj + 3]));
+              __nv_bfloat162 h2 = __floats2bfloat162_rn(__uint_as_float(v[8 * jj + 4]), __uint_as_float(v[8 * jj + 5]));
+              __nv_bfloat162 h3 = __floats2bfloat162_rn(__uint_as_float(v[8 * jj + 6]), __uint_as_float(v[8 * jj + 7]));
+              w.x = *reinterpret_cast<uint32_t*>(&h0);
+              w.y = *reinterpret_cast<uint32_t*>(&h1);
+              w.z = *reinterpret_cast<uint32_t*>(&h2);
+              w.w = *reinterpret_cast<uint32_t*>(&h3);
+              const int phys = jj ^ ((lane >> 1) & 3);
+              *reinterpret_cast<uint4*>(buf + lane * 64 + phys * 16) = w;
+            }
+          } else {
+#pragma unroll
+            for (int jj = 0; jj < 2; ++jj) {
+              uint4 w;
+              __nv_bfloat162 h0 = __floats2bfloat162_rn(__uint_as_float(v[8 * jj]), __uint_as_float(v[8 * jj + 1]));
+              __nv_bfloat162 h1 = __floats2bfloat162_rn(__uint_as_float(v[8 * jj + 2]), __uint_as_float(v[8 * jj + 3]));
+              __nv_bfloat162 h2 = __floats2bfloat162_rn(__uint_as_float(v[8 * jj + 4]), __uint_as_float(v[8 * jj + 5]));
+              __nv_bfloat162 h3 = __floats2bfloat162_rn(__uint_as_float(v[8 * jj + 6]), __uint_as_float(v[8 * jj + 7]));
+              w.x = *reinterpret_cast<uint32_t*>(&h0);
+              w.y = *reinterpret_cast<uint32_t*>(&h1);
+              w.z = *reinterpret_cast<uint32_t*>(&h2);
+              w.w = *reinterpret_cast<uint32_t*>(&h3);
+              *reinterpret_cast<uint4*>(buf + lane * 32 + jj * 16) = w;  // no swizzle
+            }
+          }
+          fence_proxy_async_smem();  // generic-proxy writes -> TMA (async proxy)
+          __syncwarp();
+          if (lane == 0) {
+            const int32_t c0 = static_cast<int32_t>(tc.n0 + c);
+            const int32_t c1 = static_cast<int32_t>(tc.m0 + 32 * q);
+            tma_store_2d(half ? &P.tmD16 : &P.tmD, buf, c0, c1);
+            bulk_commit();
+          }
+        }
+      } else {
+        for (int c = 0; c < P.bn; c += 32) {
+          uint32_t v[32];
+          tmem_ld32(base + static_cast<uint32_t>(c), v);
+          store_row_chunk(P, row, tc.n0 + c, col_end, v);
+        }
       }
       tc_fence_before();
       __syncwarp();
@@ -616,6 +705,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           mbar_arrive(&tmem_empty[acc]);
       }
     }
+    if (lane == 0) bulk_wait_all();  // TMA stores complete before the CTA retires
 #ifndef DEAR_GEMM_WAITPROF
     if (tr && warp == 2 && lane == 0) tr[5] = globaltimer();  // epilogue done
 #endif
@@ -658,14 +748,15 @@ EncodeTiledFn encode_fn() {
 }
 
 void make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
-              uint64_t ld_elems, uint32_t box_inner, uint32_t box_outer) {
+              uint64_t ld_elems, uint32_t box_inner, uint32_t box_outer,
+              CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   const cuuint64_t dims[2] = {inner, outer};
   const cuuint64_t strides[1] = {ld_elems * 2};
   const cuuint32_t box[2] = {box_inner, box_outer};
   const cuuint32_t estr[2] = {1, 1};
   const CUresult r = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base),
                                  dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     throw Error(DEAR_EINTERNAL, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
@@ -951,7 +1042,19 @@ int dear_gemm_plan_create(const void* A, int64_t lda, const void* B, int64_t ldb
   plan->lda = lda;
   plan->ldb = ldb;
   plan->K = K;
+  // TMA-store epilogue for bf16, non-accumulating D (16 B aligned rows).
+  const char* tenv = std::getenv("DEAR_GEMM_TMA_STORE");
+  p.d_tma = (!d_fp32 && !accumulate && ldd % 8 == 0 &&
+             (reinterpret_cast<uintptr_t>(D) & 15) == 0 && !(tenv && tenv[0] == '0'))
+                ? 1
+                : 0;
   try {
+    if (p.d_tma) {
+      make_map(&p.tmD, D, static_cast<uint64_t>(N), static_cast<uint64_t>(M),
+               static_cast<uint64_t>(ldd), 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+      make_map(&p.tmD16, D, static_cast<uint64_t>(N), static_cast<uint64_t>(M),
+               static_cast<uint64_t>(ldd), 16, 32, CU_TENSOR_MAP_SWIZZLE_NONE);
+    }
     configure(plan, tch);
   } catch (...) {
     delete plan;

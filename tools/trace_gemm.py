@@ -23,6 +23,10 @@ def main():
     ap.add_argument("--workload", default="bert_large")
     ap.add_argument("--kind", default="ff", choices=["ff", "bp", "dgrad", "wgrad"])
     ap.add_argument("--launches", type=int, default=6)
+    ap.add_argument("--transposed", action="store_true", help="FF as Y^T = W X^T")
+    ap.add_argument("--early", action="store_true", help="early-operand plans")
+    ap.add_argument("--bn", type=int, default=0)
+    ap.add_argument("--pair", type=int, default=0)
     a = ap.parse_args()
     import torch
 
@@ -40,9 +44,17 @@ def main():
     G = torch.zeros(n, device="cuda")
     y = torch.empty(T, rpad, device="cuda", dtype=torch.bfloat16)
     dx = torch.empty(T, H, device="cuda", dtype=torch.bfloat16)
-    ff = GemmPlan(x, W, y, T, R, H, lda=H, ldb=H, ldd=rpad)
-    dg = GemmPlan(dy, W, dx, T, H, R, b_mn_major=True, lda=rpad, ldb=H, ldd=H)
-    wg = GemmPlan(dyt, xt, G, R, H, T, lda=T, ldb=T, ldd=H, d_limit=n, accumulate=True)
+    e = a.early
+    if a.transposed:
+        yt = torch.empty(rpad, T, device="cuda", dtype=torch.bfloat16)
+        ff = GemmPlan(W, x, yt, R, T, H, lda=H, ldb=H, ldd=T, early_operands=e)
+    else:
+        ff = GemmPlan(x, W, y, T, R, H, lda=H, ldb=H, ldd=rpad, early_operands=e)
+    dg = GemmPlan(dy, W, dx, T, H, R, b_mn_major=True, lda=rpad, ldb=H, ldd=H, early_operands=e)
+    wg = GemmPlan(dyt, xt, G, R, H, T, lda=T, ldb=T, ldd=H, d_limit=n, accumulate=True,
+                  early_operands=e)
+    if a.bn:
+        {"ff": ff, "dgrad": dg, "wgrad": wg, "bp": wg}[a.kind].set_tile(a.bn, a.pair)
     run = {"ff": lambda: ff.run(), "dgrad": lambda: dg.run(), "wgrad": lambda: wg.run(),
            "bp": lambda: GemmPlan.run_group([wg, dg])}[a.kind]
     for _ in range(3):
