@@ -54,6 +54,10 @@ int dear_gemm_plan_cluster(dear_gemm_plan* plan, int32_t* cm, int32_t* cn, int32
  * GEMM then streams its operands while the preceding kernel drains under
  * programmatic dependent launch; D is still touched only after it completes. */
 #define DEAR_GEMM_EARLY_OPERANDS 1
+/* DEAR_GEMM_RED_ADD: accumulate fp32 D with per-thread red.global.add instead
+ * of staged TMA reduce-add (a tuning choice; the sums are the same up to
+ * fp32 addition order, as with any split-K). */
+#define DEAR_GEMM_RED_ADD 2
 /* Override the cost model's tile choice: bn (multiple of 16, <= 256) and
  * single-CTA (pair = 0) or 2-CTA pair (pair = 1) tiles; multicast clusters
  * off. Used by the plan-time autotuner (paper_2302_12445_b200.gemm.autotune). */

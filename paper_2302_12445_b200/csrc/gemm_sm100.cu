@@ -95,7 +95,12 @@ struct alignas(64) Problem {
   // the last 16 columns of a tile whose bn is an odd multiple of 16.
   CUtensorMap tmD;
   CUtensorMap tmD16;
-  int32_t d_tma;
+  int32_t d_tma;      // 1: bf16 TMA stores; 2: fp32 TMA reduce-add (accumulate)
+  // d_tma == 2: tmD is fp32 with box 16x32 over the r_full complete rows of
+  // D (flat limit); a partial last row (row r_full) goes through red.add.
+  int64_t r_full;      // row added by red.add (partial under d_limit), or INT64_MAX
+  int64_t d_lim_rows;  // rows covered by the TMA map
+  int32_t tma_reduce_ok;  // fp32 TMA reduce-add possible (flag DEAR_GEMM_RED_ADD turns it off)
 };
 
 struct Launch {
@@ -182,6 +187,14 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
                    reinterpret_cast<uint64_t>(map)),
                "r"(smem_u32(src)), "r"(c0), "r"(c1)
                : "memory");
+}
+__device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, const void* src,
+                                                  int32_t c0, int32_t c1) {
+  asm volatile(
+      "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(smem_u32(src)), "r"(c0), "r"(c1)
+      : "memory");
 }
 __device__ __forceinline__ void bulk_commit() {
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
@@ -638,7 +651,40 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       const int64_t row = tc.m0 + 32 * q + lane;
       const int64_t col_end = min(P.N, tc.n0 + P.bn);
       const uint32_t base = tmem + acc * kAccCols + (static_cast<uint32_t>(32 * q) << 16);
-      if (P.d_tma) {
+      if (P.d_tma == 2) {
+        // fp32 accumulate: two 16-column sub-chunks per TMEM load, each staged
+        // (64 B per row, 64 B swizzle) and added into D by a TMA reduce; L2
+        // performs the adds on full lines. Row r_full (partial under the flat
+        // limit) is added by its lane directly.
+        uint8_t* epi = smem + kEpiOffset + q * 2 * kEpiBufBytes;
+        for (int c = 0; c < P.bn; c += 32) {
+          uint32_t v[32];
+          tmem_ld32(base + static_cast<uint32_t>(c), v);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            if (c + 16 * h >= P.bn) break;
+            uint8_t* buf = epi + (epi_chunk & 1) * kEpiBufBytes;
+            ++epi_chunk;
+            if (lane == 0) bulk_wait_read<1>();
+            __syncwarp();
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+              const uint4 w = make_uint4(v[16 * h + 4 * jj], v[16 * h + 4 * jj + 1],
+                                         v[16 * h + 4 * jj + 2], v[16 * h + 4 * jj + 3]);
+              const int phys = jj ^ ((lane >> 1) & 3);
+              *reinterpret_cast<uint4*>(buf + lane * 64 + phys * 16) = w;
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_reduce_add_2d(&P.tmD, buf, static_cast<int32_t>(tc.n0 + c + 16 * h),
+                                static_cast<int32_t>(tc.m0 + 32 * q));
+              bulk_commit();
+            }
+          }
+          if (row == P.r_full) store_row_chunk(P, row, tc.n0 + c, col_end, v);
+        }
+      } else if (P.d_tma) {
         // 32 rows x 32 columns per chunk: lane = row; bf16 row of 64 B in four
         // 16 B pieces, piece j stored at j ^ ((row >> 1) & 3) (TMA 64 B swizzle;
         // conflict-free smem writes). Double-buffered per warp.
@@ -749,12 +795,14 @@ EncodeTiledFn encode_fn() {
 
 void make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
               uint64_t ld_elems, uint32_t box_inner, uint32_t box_outer,
-              CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
+              CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B,
+              CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16) {
   const cuuint64_t dims[2] = {inner, outer};
-  const cuuint64_t strides[1] = {ld_elems * 2};
+  const cuuint64_t esize = dt == CU_TENSOR_MAP_DATA_TYPE_FLOAT32 ? 4 : 2;
+  const cuuint64_t strides[1] = {ld_elems * esize};
   const cuuint32_t box[2] = {box_inner, box_outer};
   const cuuint32_t estr[2] = {1, 1};
-  const CUresult r = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base),
+  const CUresult r = encode_fn()(map, dt, 2, const_cast<void*>(base),
                                  dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                  swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -1048,8 +1096,30 @@ int dear_gemm_plan_create(const void* A, int64_t lda, const void* B, int64_t ldb
              (reinterpret_cast<uintptr_t>(D) & 15) == 0 && !(tenv && tenv[0] == '0'))
                 ? 1
                 : 0;
+  // fp32 accumulate: TMA reduce-add over the complete rows under the flat
+  // limit (rows r with r*ldd + N <= d_limit); a partial row after them is
+  // added by red.add in the epilogue.
+  p.r_full = INT64_MAX;
+  p.d_lim_rows = M;
+  const char* renv = std::getenv("DEAR_GEMM_TMA_REDUCE");
+  if (!p.d_tma && d_fp32 && accumulate && ldd % 4 == 0 &&
+      (reinterpret_cast<uintptr_t>(D) & 15) == 0 && !(tenv && tenv[0] == '0') &&
+      !(renv && renv[0] == '0')) {
+    int64_t full = M;
+    if (d_limit >= 0) full = d_limit >= N ? std::min<int64_t>(M, (d_limit - N) / ldd + 1) : 0;
+    if (full > 0) {
+      p.d_tma = 2;
+      p.tma_reduce_ok = 1;
+      p.d_lim_rows = full;
+      if (d_limit >= 0 && full < M && full * ldd < d_limit) p.r_full = full;
+    }
+  }
   try {
-    if (p.d_tma) {
+    if (p.d_tma == 2) {
+      make_map(&p.tmD, D, static_cast<uint64_t>(N), static_cast<uint64_t>(p.d_lim_rows),
+               static_cast<uint64_t>(ldd), 16, 32, CU_TENSOR_MAP_SWIZZLE_64B,
+               CU_TENSOR_MAP_DATA_TYPE_FLOAT32);
+    } else if (p.d_tma) {
       make_map(&p.tmD, D, static_cast<uint64_t>(N), static_cast<uint64_t>(M),
                static_cast<uint64_t>(ldd), 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
       make_map(&p.tmD16, D, static_cast<uint64_t>(N), static_cast<uint64_t>(M),
@@ -1162,8 +1232,10 @@ int dear_gemm_plan_set_splits(dear_gemm_plan* plan, int32_t split_k) {
 int dear_gemm_plan_set_flags(dear_gemm_plan* plan, int32_t flags) {
   DEAR_API_BEGIN
   if (!plan) throw Error(DEAR_EINVAL, "null plan");
-  if (flags & ~DEAR_GEMM_EARLY_OPERANDS) throw Error(DEAR_EINVAL, "dear_gemm_plan_set_flags: unknown flag");
+  if (flags & ~(DEAR_GEMM_EARLY_OPERANDS | DEAR_GEMM_RED_ADD))
+    throw Error(DEAR_EINVAL, "dear_gemm_plan_set_flags: unknown flag");
   plan->p.early_operands = (flags & DEAR_GEMM_EARLY_OPERANDS) ? 1 : 0;
+  if (plan->p.tma_reduce_ok) plan->p.d_tma = (flags & DEAR_GEMM_RED_ADD) ? 0 : 2;
   DEAR_API_END
 }
 

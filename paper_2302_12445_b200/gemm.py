@@ -80,8 +80,9 @@ class GemmPlan:
                                       d.data_ptr(), ldd, int(d.dtype == torch.float32), M, N,
                                       K, d_limit, int(accumulate), split_k,
                                       C.byref(self._plan)))
-        if early_operands:
-            check(L.dear_gemm_plan_set_flags(self._plan, 1))
+        self._flags = 1 if early_operands else 0
+        if self._flags:
+            check(L.dear_gemm_plan_set_flags(self._plan, self._flags))
         self.M, self.N, self.K = M, N, K
 
     def run(self, stream: torch.cuda.Stream | None = None) -> None:
@@ -107,6 +108,11 @@ class GemmPlan:
     def set_tile(self, bn: int, pair: bool) -> None:
         """Override the cost model's tile choice (dear_gemm_plan_set_tile)."""
         check(_bind().dear_gemm_plan_set_tile(self._plan, int(bn), int(bool(pair))))
+
+    def set_red_add(self, on: bool) -> None:
+        """fp32 accumulate via per-thread red.add (True) or TMA reduce (False)."""
+        self._flags = (self._flags & ~2) | (2 if on else 0)
+        check(_bind().dear_gemm_plan_set_flags(self._plan, self._flags))
 
     def set_splits(self, split_k: int) -> None:
         """Override the split-K count of an accumulating plan."""

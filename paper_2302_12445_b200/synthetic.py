@@ -138,14 +138,15 @@ class SyntheticModel:
         # Backprop on the real chain: every layer's grouped wgrad+dgrad into
         # the real (freshly zeroed, mostly cold) gradients, as in a step. The
         # scratch chain above cannot see the split-K reductions' cost on cold
-        # lines, so tiles (top-2 x top-2) and the split count are chosen here.
+        # lines, so the weight-gradient tile, split count and reduction path,
+        # then the dgrad tile, are chosen here.
         from .gemm import time_chain
 
         L = self.L
         split0 = self.wgrad[0].info()["splits"]
         num_kb = (T + 63) // 64
         splits = ([self.wgrad_split] if self.wgrad_split > 0 else
-                  sorted({x for x in (split0, 4, 6, 8, 12) if 1 <= x <= num_kb}))
+                  sorted({x for x in (split0, 4, 6, 10) if 1 <= x <= num_kb}))
 
         def bp_real(i):
             if i == 0:
@@ -153,26 +154,37 @@ class SyntheticModel:
             l = L - 1 - (i % L)
             GemmPlan.run_group([self.wgrad[l], self.dgrad[l]], s)
 
+        def set_bp(wc, sp, red, dc):
+            for l in range(L):
+                self.wgrad[l].set_tile(*wc)
+                self.wgrad[l].set_splits(sp)
+                self.wgrad[l].set_red_add(red)
+                self.dgrad[l].set_tile(*dc)
+
+        # stage 1: weight-gradient tile x split-K x reduction path (TMA reduce
+        # or red.add), dgrad at its best chain tile
+        wtiles = list(dict.fromkeys([c[1:] for c in wg[:2]] + [(128, 0), (176, 0), (256, 0)]))
         trials = []
-        for wc in [c[1:] for c in wg[:2]]:
-            for dc in [c[1:] for c in dg[:2]]:
-                for sp in splits:
-                    for l in range(L):
-                        self.wgrad[l].set_tile(*wc)
-                        self.wgrad[l].set_splits(sp)
-                        self.dgrad[l].set_tile(*dc)
-                    trials.append((time_chain(bp_real, L, s, reps=2), wc, dc, sp))
+        for wc in wtiles:
+            for sp in splits:
+                for red in (False, True):
+                    set_bp(wc, sp, red, dg[0][1:])
+                    trials.append((time_chain(bp_real, L, s, reps=2), wc, sp, red, dg[0][1:]))
         trials.sort(key=lambda t: t[0])
-        us, best_wg, best_dg, best_sp = trials[0]
-        for l in range(L):
-            self.wgrad[l].set_tile(*best_wg)
-            self.wgrad[l].set_splits(best_sp)
-            self.dgrad[l].set_tile(*best_dg)
+        _, wc, sp, red, _ = trials[0]
+        # stage 2: dgrad tile with that weight-gradient configuration
+        for dc in [c[1:] for c in dg[1:3]]:
+            set_bp(wc, sp, red, dc)
+            trials.append((time_chain(bp_real, L, s, reps=2), wc, sp, red, dc))
+        trials.sort(key=lambda t: t[0])
+        us, best_wg, best_sp, best_red, best_dg = trials[0]
+        set_bp(best_wg, best_sp, best_red, best_dg)
         self.zero_grad()
         torch.cuda.synchronize()
         return {"ff": {"bn": best_ff[0], "pair": best_ff[1], "us": round(ff[0][0], 2),
                        "transposed": self.ff_transposed},
-                "wgrad": {"bn": best_wg[0], "pair": best_wg[1], "splits": best_sp},
+                "wgrad": {"bn": best_wg[0], "pair": best_wg[1], "splits": best_sp,
+                          "reduce": "red.add" if best_red else "tma"},
                 "dgrad": {"bn": best_dg[0], "pair": best_dg[1]},
                 "bp_group_us": round(us, 2),
                 "candidates": {"ff": len(ff), "wgrad": len(wg), "dgrad": len(dg),

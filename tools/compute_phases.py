@@ -26,9 +26,12 @@ def main():
     from paper_2302_12445_b200.synthetic import SyntheticModel
 
     wl = bench.WORKLOADS[a.workload]
+    import time
+    t0 = time.time()
     m = SyntheticModel(preset_param_counts(wl["preset"]), wl["hidden"],
                        wl["batch"] * wl["tokens_per_sample"], seed=1234,
                        wgrad_split=a.wgrad_split)
+    t_build = time.time() - t0
     s = torch.cuda.Stream()
     names = ("base", "input", "ff", "zero", "bp")
     ev = {k: torch.cuda.Event(enable_timing=True, external=True) for k in names}
@@ -62,6 +65,7 @@ def main():
     ms = {k: sorted(v)[len(v) // 2] for k, v in res.items()}
     t = m.tiles or {}
     print(json.dumps({"workload": a.workload, "L": m.L, "wgrad_split": a.wgrad_split,
+                      "build_and_tune_s": round(t_build, 1),
                       "splits_used": m.wgrad[0].info()["splits"], "phases_ms": ms,
                       "ff_us_per_layer": ms["ff"] * 1e3 / m.L,
                       "bp_us_per_layer": ms["bp"] * 1e3 / m.L,
