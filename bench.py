@@ -73,6 +73,8 @@ def parse():
                          "group-dependency dispatch order")
     ap.add_argument("--no-ablation", action="store_true", help="skip WFBP / compute-only runs")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-calibrate", action="store_true",
+                    help="north star: skip the t_ag = 1.25 t_ff batch comparison (N > 1)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--extra-workload", default="bert_large",
                     help="also measure DeAR vs WFBP on this workload (north-star "
@@ -345,9 +347,10 @@ def make_runtime(a, model, comm, rank, world, stream, policy, defer):
             ms = time_loop(run, 6, 3, stream, world > 1)
             del run
             rt.synchronize()
-        trials.append({"contention": ct, "ags_during_backprop": nb, "ms": ms,
+        trials.append({"contention": ct, "ags_during_backprop": nb,
+                       "ms": ms if ms == ms else None,
                        "predicted_ms": pred * 1e3, "order": order})
-    best = min(trials, key=lambda t: (t["ms"] if t["ms"] == t["ms"] else 0.0))
+    best = min(trials, key=lambda t: (t["ms"] if t["ms"] is not None else 0.0))
     rt.set_comm_order(best["order"])
     rt.comm_order_info = {"source": "reference scheduler simulated on measured stage times; "
                                     "fastest of the candidate orders",
@@ -391,6 +394,7 @@ def gpu_arm(a, wl, world, rank, local_rank):
     # --- headline: DeAR, inputs resident ---------------------------------
     rt = runtime(a.policy)
     backend_used = rt.backend
+    zero_copy = bool(getattr(rt, "zero_copy", False))
     rt_order_info = rt.comm_order_info
     buckets = rt.buckets()
     run = make_runner(Step(model, rt, stream), use_graph, stream)
@@ -462,15 +466,20 @@ def gpu_arm(a, wl, world, rank, local_rank):
     # Bucket-stage rooflines (isolated): algorithmic bytes per element.
     D = sum(counts)
     shard = sum(b["slot_stride"] for b in buckets)
+    # isolated stages run at P = 1 when N = 1 (update over whole buckets)
     elem_bytes = {"pack": 8 * D, "update": (20 if a.momentum else 12) * shard,
-                  "unpack": 10 * D}
+                  "unpack": 10 * D, "direct": 14 * D}
     roof = {}
     for k, nbytes in elem_bytes.items():
-        t = iso.get(k)
-        if t:
-            roof[k] = {"bound": "hbm", "achieved": nbytes / (t / 1e3) / 1e9, "peak": hbm,
-                       "unit": "GB/s", "frac": nbytes / (t / 1e3) / 1e9 / hbm,
-                       "bytes_per_step": nbytes, "ms_per_step": t}
+        if k not in iso:
+            continue
+        t, launches = iso[k]
+        roof[k] = {"bound": "hbm", "achieved": nbytes / (t / 1e3) / 1e9, "peak": hbm,
+                   "unit": "GB/s", "frac": nbytes / (t / 1e3) / 1e9 / hbm,
+                   "bytes_per_step": nbytes, "ms_per_step": t,
+                   "launches_per_step": launches, "us_per_launch": 1e3 * t / launches,
+                   "timing": "graph-replayed chain of launches (dear_bench_stage), "
+                             "CUDA events, no GEMMs"}
     busbw = {}
     if world > 1:
         for k in ("rs", "ag"):
@@ -491,6 +500,7 @@ def gpu_arm(a, wl, world, rank, local_rank):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic",
         "config": {"workload": wl["config"], "policy": a.policy, "collectives": backend_used,
+                   "zero_copy": zero_copy,
                    "dear_group_dependency": bool(a.group_dependency),
                    "comm_order": rt_order_info,
                    "fusion_buffer_bytes": a.buffer, "buckets": len(buckets),
@@ -573,91 +583,156 @@ def _time_gemms(model, rt, stream):
     return ms, sum(f for _, _, f in evs)
 
 
-def _isolated_stage_times(model, runtime, stream, policy):
-    """pack / update / unpack per step with no GEMMs running: grads reported
-    back to back, so the comm stream runs the bucket kernels alone."""
+def _isolated_stage_times(model, runtime, stream, policy, reps=20):
+    """pack / update / unpack (and the P = 1 direct update) per step with no
+    GEMMs running: each stage's kernel over every bucket, `reps` rounds
+    captured as one CUDA graph (dear_bench_stage) and timed with CUDA events
+    on `stream`, so a launch's average duration carries no host launch gap.
+    Returns {stage: (ms per step, launches per step)}."""
     import torch
 
+    import paper_2302_12445_b200 as dear
+
     # DEAR_DIRECT=0: at P = 1 keep the separate pack / update / unpack kernels
-    # (what every P > 1 bucket runs) instead of the fused direct update.
+    # (what every P > 1 NCCL bucket runs) next to the fused direct update.
     os.environ["DEAR_DIRECT"] = "0"
     try:
         rt = runtime(policy)
     finally:
         os.environ.pop("DEAR_DIRECT", None)
-    rt.set_timing(True)
-    for it in range(3):
-        with torch.cuda.stream(stream):
-            for l in range(1, model.L + 1):
-                rt.param_wait(l, stream)
-            for l in range(model.L, 0, -1):
-                rt.grad_ready(l, stream)
-            rt.step(stream)
-        rt.synchronize()
-    torch.cuda.synchronize()
-    st = rt.timings()
-    rt.close()
+    rt_dir = runtime(policy) if rt.world_size == 1 else None
+    nb = len(rt.buckets())
     out = {}
-    for k in ("pack", "update", "unpack"):
-        v = [s[k] for s in st if s[k] is not None]
-        out[k] = sum(v) if v else None
+    for k, r in (("pack", rt), ("update", rt), ("unpack", rt), ("direct", rt_dir)):
+        if r is None:
+            continue
+        try:
+            with torch.cuda.stream(stream):
+                r.bench_stage(k, 2, stream)
+        except dear.InvalidArgument:  # no direct-update tables (momentum)
+            continue
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            r.bench_stage(k, reps, stream)
+        with torch.cuda.stream(stream):
+            g.replay()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            g.replay()
+            e1.record(stream)
+        torch.cuda.synchronize()
+        out[k] = (e0.elapsed_time(e1) / reps, nb)
+        del g
+    rt.close()
+    if rt_dir is not None:
+        rt_dir.close()
+    # the stages rewrote parameters with synthetic values: restore sane ones
+    model.params_flat.uniform_(-0.02, 0.02)
+    model.grads_flat.zero_()
     return out
+
+
+def _policy_pair(a, model, comm, world, rank, stream, batch, steps, warm, backend=None):
+    """DeAR vs WFBP on `model` (same kernels, same fusion buffer), graph-replayed
+    steps, max over ranks. Also the measured per-step comm-stream times of the
+    DeAR runtime's comm-only iterations (t_rs = pack + RS + update side,
+    t_ag = AG + unpack side; make_runtime measures them for its dispatch order)."""
+    import argparse
+
+    ab = argparse.Namespace(**vars(a))
+    if backend is not None:
+        ab.backend = backend
+    res = {}
+    for policy in (a.policy, a.baseline_policy):
+        rt = make_runtime(ab, model, comm, rank, world, stream, policy, True)
+        res["collectives"] = rt.backend
+        res["zero_copy"] = bool(getattr(rt, "zero_copy", False))
+        if rt.comm_order_info:
+            info = rt.comm_order_info
+            res["comm_order"] = {k: v for k, v in info.items()
+                                 if k in ("ags_during_backprop", "contention")}
+            st, nb = info["stage_us_mean"], info["buckets"]
+            res["t_rs_ms"] = nb * (st["pack"] + st["rs"] + st["update"]) / 1e3
+            res["t_ag_ms"] = nb * (st["ag"] + st["unpack"]) / 1e3
+        run = make_runner(Step(model, rt, stream), True, stream)
+        ms = time_loop(run, steps, warm, stream, world > 1)
+        rt.synchronize()
+        rt.close()
+        res[policy] = {"ms_per_step": ms, "samples_per_s": batch * world / (ms / 1e3)}
+    return res
 
 
 def compare_policies(a, wl_name, comm, world, rank, stream):
     """DeAR vs WFBP (same kernels, same fusion buffer) and compute-only on a
-    second workload: the north-star comparison (BERT-Large-shaped layers)."""
+    second workload: the north-star comparison (BERT-Large-shaped layers).
+
+    Next to the measured step times: the measured t_ff / t_bp (tile tuner's
+    per-layer chain times x L) and t_rs / t_ag (comm-only iterations) with the
+    reference's Eq. 7 (DeAR) / Eq. 8 (all-reduce) predictions
+    (analysis.cpp:50-60). DeAR's edge over WFBP exists only where t_rs + t_ag
+    exceeds t_bp (SURVEY §7 "hard parts"); with N > 1 the comparison is
+    repeated at the batch that puts the measured t_ag at 1.25 t_ff, the band
+    SURVEY §7 names (t_ag = 1.2-1.33 t_ff), when that batch differs from the
+    paper's."""
     import torch
 
-    import paper_2302_12445_b200 as dear
+    from paper_2302_12445_b200 import costmodel
     from paper_2302_12445_b200.presets import preset_param_counts
     from paper_2302_12445_b200.synthetic import SyntheticModel
 
     wl = WORKLOADS[wl_name]
-    batch = wl["batch"]
-    model = SyntheticModel(preset_param_counts(wl["preset"]), wl["hidden"],
-                           batch * wl["tokens_per_sample"], seed=4321)
     dist_on = world > 1
     steps, warm = max(5, a.steps // 2), max(3, a.warmup)
-    out = {"workload": wl["config"], "batch_per_gpu": batch, "fusion_buffer_bytes": a.buffer,
-           "steps": steps, "warmup": warm}
-    run = make_runner(Step(model, None, stream), True, stream)
-    comp = time_loop(run, steps, warm, stream, dist_on)
-    out["compute_only_ms"] = comp
-    # The resolved default backend first; with N > 1 also NCCL, the north
-    # star's named transport (DeAR's edge over WFBP grows with comm cost).
-    backends = [None]
-    if world > 1 and a.backend != "nccl":
-        backends.append("nccl")
-    import argparse
-    for be in backends:
-        ab = argparse.Namespace(**vars(a))
-        if be is not None:
-            ab.backend = be
-        res = {}
-        for policy in (a.policy, a.baseline_policy):
-            rt = make_runtime(ab, model, comm, rank, world, stream, policy, True)
-            used = rt.backend
-            if rt.comm_order_info:
-                res["comm_order"] = {k: v for k, v in rt.comm_order_info.items()
-                                     if k in ("ags_during_backprop", "contention")}
-            run = make_runner(Step(model, rt, stream), True, stream)
-            ms = time_loop(run, steps, warm, stream, dist_on)
-            rt.synchronize()
-            rt.close()
-            res[policy] = {"ms_per_step": ms, "samples_per_s": batch * world / (ms / 1e3)}
-        d, w = res[a.policy]["ms_per_step"], res[a.baseline_policy]["ms_per_step"]
-        res.update({"dear_over_wfbp": w / d,
-                    "exposed_comm_pct": max(0.0, 100 * (d - comp) / d),
-                    "wfbp_exposed_comm_pct": max(0.0, 100 * (w - comp) / w)})
-        if be is None:
-            res["collectives"] = used
-            out.update(res)
-        else:
-            out["nccl"] = res
-    model.close()
-    del model
-    torch.cuda.empty_cache()
+
+    def one(batch, with_nccl):
+        model = SyntheticModel(preset_param_counts(wl["preset"]), wl["hidden"],
+                               batch * wl["tokens_per_sample"], seed=4321)
+        out = {"batch_per_gpu": batch}
+        run = make_runner(Step(model, None, stream), True, stream)
+        comp = time_loop(run, steps, warm, stream, dist_on)
+        out["compute_only_ms"] = comp
+        tiles = model.tiles or {}
+        t_ff = tiles.get("ff", {}).get("us", 0.0) * model.L / 1e3
+        t_bp = tiles.get("bp_group_us", 0.0) * model.L / 1e3
+        # The resolved default backend first; with N > 1 also NCCL, the north
+        # star's named transport (DeAR's edge over WFBP grows with comm cost).
+        for be in [None] + (["nccl"] if with_nccl and world > 1 and a.backend != "nccl" else []):
+            res = _policy_pair(a, model, comm, world, rank, stream, batch, steps, warm, be)
+            d, w = res[a.policy]["ms_per_step"], res[a.baseline_policy]["ms_per_step"]
+            res.update({"dear_over_wfbp": w / d,
+                        "exposed_comm_pct": max(0.0, 100 * (d - comp) / d),
+                        "wfbp_exposed_comm_pct": max(0.0, 100 * (w - comp) / w)})
+            if "t_rs_ms" in res:
+                t_rs, t_ag = res["t_rs_ms"], res["t_ag_ms"]
+                eq = costmodel.theoretical_times(t_ff, t_bp, t_rs, t_ag)
+                res["eq78"] = {"t_ff_ms": t_ff, "t_bp_ms": t_bp, "t_rs_ms": t_rs,
+                               "t_ag_ms": t_ag, "eq7_dear_ms": eq["dear"],
+                               "eq8_allreduce_ms": eq["baseline"],
+                               "eq_ratio": eq["baseline"] / eq["dear"] if eq["dear"] else None,
+                               "t_ag_over_t_ff": t_ag / t_ff if t_ff else None}
+            if be is None:
+                out.update(res)
+            else:
+                out["nccl"] = res
+        model.close()
+        del model
+        torch.cuda.empty_cache()
+        return out
+
+    base = wl["batch"]
+    out = {"workload": wl["config"], "fusion_buffer_bytes": a.buffer, "steps": steps,
+           "warmup": warm}
+    out.update(one(base, True))
+    eq = out.get("eq78")
+    if world > 1 and eq and eq["t_ag_ms"] > 0 and eq["t_ff_ms"] > 0 and not a.no_calibrate:
+        # t_ff scales with the batch, t_ag does not: the batch with t_ag = 1.25 t_ff
+        b = int(round(base * eq["t_ag_ms"] / (1.25 * eq["t_ff_ms"])))
+        b = max(4, min(b, 4 * base))
+        if abs(b - base) >= max(2, base // 8):
+            cal = one(b, False)
+            cal["rule"] = "batch with measured t_ag = 1.25 t_ff (SURVEY §7: 1.2-1.33)"
+            out["calibrated_batch"] = cal
     return out
 
 

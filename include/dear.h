@@ -178,10 +178,22 @@ int dear_set_lr(dear_ctx* ctx, double lr);
  * (graph-safe). The NCCL communicator is still used for dear_finalize's and
  * dear_check_replicas' cross-rank checks.
  * ------------------------------------------------------------------------ */
-#define DEAR_PEER_HANDLE_BYTES 128
+#define DEAR_PEER_HANDLE_BYTES 256
 int dear_peer_handle(dear_ctx* ctx, uint8_t out[DEAR_PEER_HANDLE_BYTES]);
-/* handles: n = P records of DEAR_PEER_HANDLE_BYTES, in rank order. */
+/* handles: n = P records of DEAR_PEER_HANDLE_BYTES, in rank order.
+ * Zero-copy: when every rank's registered gradients lie in one device
+ * allocation and its parameters in another (e.g. flat buffers viewed per
+ * layer), with the same relative layout on every rank, those allocations are
+ * IPC-mapped as well. The reduce-scatter kernel then reads the owned chunk of
+ * every rank's gradients in place (no pack, no bucket buffer) and writes the
+ * updated shard into the owner's parameters, and the all-gather kernel reads
+ * the owners' parameters: 14 B of HBM traffic per element and rank instead of
+ * 24 (P = 4). Same sums in the same order, so results are unchanged. The
+ * environment variable DEAR_ZERO_COPY=0 disables it. Gradients are then
+ * "consumed" (dear_step's fence) once every rank's reduce-scatters finished. */
 int dear_peer_connect(dear_ctx* ctx, const uint8_t* handles, int32_t n);
+/* *on = 1 when dear_peer_connect enabled the zero-copy path. */
+int dear_peer_zero_copy(dear_ctx* ctx, int32_t* on);
 
 /* ---------------------------------------------------------------------------
  * Introspection, timing and checks.
@@ -210,6 +222,13 @@ int dear_get_timeline(dear_ctx* ctx, void* base_event, float* out, int32_t n_buc
  * rejection (collective.cpp:172-181): hashes every registered parameter
  * and compares across ranks. *identical = 1 when all ranks agree. */
 int dear_check_replicas(dear_ctx* ctx, int32_t* identical);
+/* Measurement hook (bench.py's kernel rooflines): enqueue `reps` rounds of
+ * one bucket-kernel stage over every bucket on `stream`, outside the schedule
+ * — stage 0 pack, 1 update, 2 unpack, 3 direct update (P = 1). Capturable in
+ * a CUDA graph, so a chain of launches is timed without host launch gaps.
+ * It rewrites the bucket buffers / parameters like the real stages do
+ * (values are not meaningful afterwards: re-register or re-seed). */
+int dear_bench_stage(dear_ctx* ctx, int32_t stage, int32_t reps, void* stream);
 
 #ifdef __cplusplus
 }

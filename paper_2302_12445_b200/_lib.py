@@ -76,7 +76,10 @@ _SIGNATURES = {
     "dear_peer_handle": [_P, C.c_char_p],
     "dear_get_timeline": [_P, _P, C.POINTER(C.c_float), C.c_int32],
     "dear_peer_connect": [_P, C.c_char_p, C.c_int32],
+    "dear_peer_zero_copy": [_P, C.POINTER(C.c_int32)],
+    "dear_bench_stage": [_P, C.c_int32, C.c_int32, _P],
 }
+DEAR_PEER_HANDLE_BYTES = 256
 
 _lib = None
 

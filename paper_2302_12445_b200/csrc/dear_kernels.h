@@ -43,6 +43,13 @@ constexpr int kSlices = 148 * DEAR_SLICES_PER_SM;
 #define DEAR_PEER_SLICES 64
 #endif
 constexpr int kPeerSlices = DEAR_PEER_SLICES;
+// Zero-copy peer kernels: one CTA per SM (the reduce-scatter is bound by
+// NVLink round trips, so more requests in flight shorten it — and the time it
+// shares the SMs with the backprop GEMMs; profiles/r01e_zc_n2_sweep.log).
+#ifndef DEAR_ZC_SLICES
+#define DEAR_ZC_SLICES 148
+#endif
+constexpr int kZcSlices = DEAR_ZC_SLICES;
 // Peer-backend pack: one CTA per SM, one contiguous slice per CTA.
 constexpr int kPackPeerSlices = 148;
 
@@ -133,9 +140,21 @@ cudaError_t launch_rs_update_peer(const Unit* units, const Slice* slices, int64_
 // Fused all-gather + unpack: every element read from its owner's slot (remote
 // over NVLink unless owned), written to the params (+ bf16 copy); then
 // flags->gathered += 1.
+// `sa`: where unit sources live on each rank (the arena deltas for bucket
+// slots; the parameter-allocation deltas for zero-copy).
+// `n_slices`: entries of `slices` (kPeerSlices, or kZcSlices for zero-copy),
+// one CTA each.
 cudaError_t launch_ag_unpack_peer(const Unit* units, const Slice* slices, int64_t total,
-                                  int with_shadow, const PeerArgs& pa, BucketFlags* flags,
-                                  cudaStream_t s);
+                                  int with_shadow, const PeerArgs& pa, const PeerArgs& sa,
+                                  BucketFlags* flags, int n_slices, cudaStream_t s);
+// Zero-copy fused reduce-scatter + update: the owned chunk of every rank's
+// gradients (at ga.delta[k]) summed in ring order, 1/P, SGD, written into
+// the own parameters (+ bf16 copy); announces / waits on flags->packed and
+// bumps flags->updated. mom_base: the bucket's momentum shard (or null).
+cudaError_t launch_rs_update_zc(const Unit* units, const Slice* slices, const HyperParams* hp,
+                                int has_momentum_buf, float* mom_base, int use_momentum,
+                                int use_wd, int with_shadow, const PeerArgs& pa,
+                                const PeerArgs& ga, BucketFlags* flags, cudaStream_t s);
 
 // Order-independent 64-bit hash of float bit patterns (sum of mixed words),
 // accumulated into *acc with atomics. Used by dear_check_replicas.

@@ -566,14 +566,352 @@ __global__ void __launch_bounds__(kThreads, 1)
   signal_done(&flags->done[1], &flags->updated);
 }
 
+// ------------------------------------- zero-copy peer RS+update ----------
+// The gradients and parameters themselves are IPC-mapped (one allocation
+// each per rank, identical relative layout): no pack, no bucket buffer. The
+// owner of chunk (rank+1)%P reads that chunk of every rank's GRADIENTS over
+// NVLink, sums in the ring order of collective.cpp:70-90, applies 1/P and
+// the SGD update (sgd_elem, same operation sequence as update_kernel with
+// prescaled = 0) and writes w' straight into its own parameters and their
+// bf16 copy. Peers then gather the owner's parameters (ag_unpack_peer_kernel
+// with parameter deltas). Per element this moves 4 B of local gradient reads
+// served to the ring + 10/P B of update traffic, where pack + slot RS moved
+// 8 + 4 + 8/P.
+//
+// Cross-GPU protocol on the arena's per-bucket counters (graph-safe, no host
+// epoch): the first CTA announces "my gradients of this bucket are complete"
+// (packed += 1, release, system scope; the comm stream already waited on the
+// producing streams' events); every CTA then waits until each peer's
+// `packed` reached our `updated` + 1 — `updated` only moves when this kernel's
+// last CTA finishes, after every CTA passed its wait, so it is this
+// iteration's epoch on every rank.
+__device__ __forceinline__ void cta_announce_and_wait(BucketFlags* flags, const PeerArgs& pa) {
+  if (threadIdx.x < 32) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      __threadfence_system();
+      atomicAdd_system(&flags->packed, 1u);
+    }
+    const uint32_t target = ld_acquire_sys(&flags->updated) + 1u;
+    const int k = threadIdx.x;
+    if (k < pa.P && k != pa.rank) {
+      const uint32_t* f = at_peer(&flags->packed, pa.delta[k]);
+      const long long t0 = clock64();
+      while (static_cast<int32_t>(ld_acquire_sys(f) - target) < 0) {
+        __nanosleep(128);
+        if (clock64() - t0 > 60ll * 2000000000ll) __trap();  // fail loudly, never hang
+      }
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void store_bf16x4(__nv_bfloat16* sh, int64_t q, float4 v) {
+  __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y);
+  __nv_bfloat162 hi = __floats2bfloat162_rn(v.z, v.w);
+  uint2 packed;
+  packed.x = *reinterpret_cast<uint32_t*>(&lo);
+  packed.y = *reinterpret_cast<uint32_t*>(&hi);
+  reinterpret_cast<uint2*>(sh)[q] = packed;
+}
+
+// Units: a = gradient (local address; rank k's copy at a + ga.delta[k]),
+// b = parameter (in/out), c = bf16 copy or null. Momentum shard element i of
+// the op lives at mom_base[i] (the op's elements are the owned chunk in
+// order, so Unit::start + offset is the chunk position). Parameters and
+// gradients share their 16 B phase (registration requires 16 B alignment),
+// so after a scalar head every stream is float4-aligned.
+// Vectors per lane per round (each with P gradient loads in flight).
+#ifndef DEAR_ZC_KU2
+#define DEAR_ZC_KU2 8
+#endif
+#ifndef DEAR_ZC_KU4
+#define DEAR_ZC_KU4 4
+#endif
+#ifndef DEAR_ZC_KU8
+#define DEAR_ZC_KU8 2
+#endif
+template <int PC, bool kMom, bool kWd, bool kShadow>
+__global__ void __launch_bounds__(kThreads, 1)
+    rs_update_zc_kernel(const Unit* __restrict__ units, const Slice* __restrict__ slices,
+                        const HyperParams* __restrict__ hpp, int has_buf, float* mom_base,
+                        PeerArgs pa, PeerArgs ga, BucketFlags* flags) {
+  cta_announce_and_wait(flags, pa);
+  const HyperParams hp = *hpp;
+  const int P = PC > 0 ? PC : pa.P;
+  const int k0 = (pa.rank + 1) % P;
+  walk_slice(units, slices, kZcSlices, [&](const Unit& U, int64_t off, int64_t n) {
+    const float* g = U.a + off;
+    float* w = U.b + off;
+    float* mom = kMom ? mom_base + U.start + off : nullptr;
+    __nv_bfloat16* sh = (kShadow && U.c) ? static_cast<__nv_bfloat16*>(U.c) + off : nullptr;
+    auto scalar = [&](int64_t i) {
+      int k = k0;
+      float acc = __ldcg(at_peer(g + i, ga.delta[k]));
+      for (int j = 1; j < P; ++j) {
+        k = k + 1 == P ? 0 : k + 1;
+        acc = __fadd_rn(acc, __ldcg(at_peer(g + i, ga.delta[k])));
+      }
+      float m = kMom ? mom[i] : 0.f;
+      const float v = sgd_elem<kMom, kWd>(acc, w[i], m, hp, has_buf);
+      w[i] = v;
+      if (kMom) mom[i] = m;
+      if (kShadow && sh) sh[i] = __float2bfloat16_rn(v);
+    };
+    int64_t head = ((16 - (reinterpret_cast<uintptr_t>(w) & 15)) & 15) >> 2;
+    if (head > n) head = n;
+    if (threadIdx.x < head) scalar(static_cast<int64_t>(threadIdx.x));
+    const int64_t n4 = (n - head) >> 2;
+    if constexpr (PC > 0) {
+      constexpr int KU = PC <= 2 ? DEAR_ZC_KU2 : (PC <= 4 ? DEAR_ZC_KU4 : DEAR_ZC_KU8);
+      const float4* pg[PC];
+#pragma unroll
+      for (int j = 0; j < PC; ++j)
+        pg[j] = at_peer(reinterpret_cast<const float4*>(g + head), ga.delta[(k0 + j) % PC]);
+      float4* w4 = reinterpret_cast<float4*>(w + head);
+      // The momentum shard is indexed by chunk position, which need not share
+      // the parameters' 16 B phase: scalar (still coalesced) access then.
+      float* mh = kMom ? mom + head : nullptr;
+      const bool mvec = kMom && (reinterpret_cast<uintptr_t>(mh) & 15) == 0;
+      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+      constexpr int kWarps = kThreads / 32;
+      const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int64_t base = static_cast<int64_t>(warp) * 32 * KU; base < n4;
+           base += static_cast<int64_t>(kWarps) * 32 * KU) {
+        float4 wv[KU];
+        float4 v[KU][PC];
+#pragma unroll
+        for (int k = 0; k < KU; ++k) {
+          const int64_t q = base + k * 32 + lane;
+          wv[k] = q < n4 ? w4[q] : zero;
+#pragma unroll
+          for (int j = 0; j < PC; ++j) v[k][j] = q < n4 ? __ldcg(pg[j] + q) : zero;
+        }
+#pragma unroll
+        for (int k = 0; k < KU; ++k) {
+          const int64_t q = base + k * 32 + lane;
+          if (q >= n4) continue;
+          float4 acc = v[k][0];
+#pragma unroll
+          for (int j = 1; j < PC; ++j) {
+            acc.x = __fadd_rn(acc.x, v[k][j].x);
+            acc.y = __fadd_rn(acc.y, v[k][j].y);
+            acc.z = __fadd_rn(acc.z, v[k][j].z);
+            acc.w = __fadd_rn(acc.w, v[k][j].w);
+          }
+          float4 mv = zero;
+          if (kMom && has_buf) {
+            if (mvec) {
+              mv = reinterpret_cast<const float4*>(mh)[q];
+            } else {
+              mv = make_float4(mh[4 * q], mh[4 * q + 1], mh[4 * q + 2], mh[4 * q + 3]);
+            }
+          }
+          float4 o;
+          o.x = sgd_elem<kMom, kWd>(acc.x, wv[k].x, mv.x, hp, has_buf);
+          o.y = sgd_elem<kMom, kWd>(acc.y, wv[k].y, mv.y, hp, has_buf);
+          o.z = sgd_elem<kMom, kWd>(acc.z, wv[k].z, mv.z, hp, has_buf);
+          o.w = sgd_elem<kMom, kWd>(acc.w, wv[k].w, mv.w, hp, has_buf);
+          w4[q] = o;
+          if (kMom) {
+            if (mvec) {
+              reinterpret_cast<float4*>(mh)[q] = mv;
+            } else {
+              mh[4 * q] = mv.x;
+              mh[4 * q + 1] = mv.y;
+              mh[4 * q + 2] = mv.z;
+              mh[4 * q + 3] = mv.w;
+            }
+          }
+          if (kShadow && sh) store_bf16x4(sh + head, q, o);
+        }
+      }
+    } else {
+      for (int64_t q = threadIdx.x; q < n4; q += kThreads)
+        for (int e = 0; e < 4; ++e) scalar(head + 4 * q + e);
+    }
+    for (int64_t i = head + n4 * 4 + threadIdx.x; i < n; i += kThreads) scalar(i);
+  });
+  signal_done(&flags->done[1], &flags->updated);
+}
+
+// ---------------------------- zero-copy RS+update, TMA-staged (opt-in) ----
+// Same arithmetic and protocol as rs_update_zc_kernel, but the P gradient
+// streams (and the parameters) move by 1-D bulk TMA (cp.async.bulk) into a
+// shared-memory ring instead of per-thread loads (hypothesis: a per-SM cap on
+// outstanding LSU misses bounds the register version, since 2 CTAs per SM did
+// not help); the bulk engine keeps a whole stage per source in flight
+// from one issuing thread while the other warps sum / update from shared
+// memory. One CTA per SM; thread 0 refills a stage as soon as every warp has
+// consumed it.
+#ifndef DEAR_ZC_TMA_STAGES
+#define DEAR_ZC_TMA_STAGES 4
+#endif
+constexpr int kZcStages = DEAR_ZC_TMA_STAGES;
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+
+// Stage layout: (PC + 1) slots of kChunk floats (PC gradient sources in ring
+// order, then the parameters). kChunk per source keeps the ring <= ~160 KB.
+template <int PC>
+struct ZcTma {
+  static constexpr int kChunk = PC <= 2 ? 4096 : (PC <= 4 ? 2048 : 1024);  // floats
+  static constexpr int kSlot = kChunk * 4;                                // bytes
+  static constexpr int kStageBytes = (PC + 1) * kSlot;
+  static constexpr int kSmem = kZcStages * kStageBytes + 64;
+};
+
+template <int PC, bool kMom, bool kWd, bool kShadow>
+__global__ void __launch_bounds__(kThreads, 1)
+    rs_update_zc_tma_kernel(const Unit* __restrict__ units, const Slice* __restrict__ slices,
+                            const HyperParams* __restrict__ hpp, int has_buf, float* mom_base,
+                            PeerArgs pa, PeerArgs ga, BucketFlags* flags) {
+  using T = ZcTma<PC>;
+  extern __shared__ __align__(128) unsigned char zsm[];
+  float* ring = reinterpret_cast<float*>(zsm);
+  uint64_t* full = reinterpret_cast<uint64_t*>(zsm + kZcStages * T::kStageBytes);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kZcStages; ++i) mbar_init(&full[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  cta_announce_and_wait(flags, pa);  // ends with __syncthreads
+  if (threadIdx.x == 0) asm volatile("fence.proxy.async;" ::: "memory");
+  const HyperParams hp = *hpp;
+  const int k0 = (pa.rank + 1) % PC;
+  uint32_t iter = 0;  // chunks consumed by this CTA so far (ring position / parity)
+  walk_slice(units, slices, kZcSlices, [&](const Unit& U, int64_t off, int64_t n) {
+    const float* g = U.a + off;
+    float* w = U.b + off;
+    float* mom = kMom ? mom_base + U.start + off : nullptr;
+    __nv_bfloat16* sh = (kShadow && U.c) ? static_cast<__nv_bfloat16*>(U.c) + off : nullptr;
+    auto scalar = [&](int64_t i) {
+      int k = k0;
+      float acc = __ldcg(at_peer(g + i, ga.delta[k]));
+      for (int j = 1; j < PC; ++j) {
+        k = k + 1 == PC ? 0 : k + 1;
+        acc = __fadd_rn(acc, __ldcg(at_peer(g + i, ga.delta[k])));
+      }
+      float m = kMom ? mom[i] : 0.f;
+      const float v = sgd_elem<kMom, kWd>(acc, w[i], m, hp, has_buf);
+      w[i] = v;
+      if (kMom) mom[i] = m;
+      if (kShadow && sh) sh[i] = __float2bfloat16_rn(v);
+    };
+    int64_t head = ((16 - (reinterpret_cast<uintptr_t>(w) & 15)) & 15) >> 2;
+    if (head > n) head = n;
+    if (threadIdx.x < head) scalar(static_cast<int64_t>(threadIdx.x));
+    const int64_t nv = (n - head) & ~int64_t{3};  // vector elements (16 B multiples)
+    const int64_t nchunks = (nv + T::kChunk - 1) / T::kChunk;
+    const float* gb = g + head;
+    float* wb = w + head;
+    auto issue = [&](int64_t c) {  // thread 0: chunk c into its ring stage
+      const uint32_t st = (iter + static_cast<uint32_t>(c)) % kZcStages;
+      const int64_t e0 = c * T::kChunk;
+      const uint32_t bytes = static_cast<uint32_t>((nv - e0 < T::kChunk ? nv - e0 : int64_t{T::kChunk}) * 4);
+      float* base = ring + static_cast<size_t>(st) * (PC + 1) * T::kChunk;
+      mbar_expect(&full[st], bytes * (PC + 1));
+#pragma unroll
+      for (int j = 0; j < PC; ++j)
+        bulk_g2s(base + j * T::kChunk, at_peer(gb + e0, ga.delta[(k0 + j) % PC]), bytes, &full[st]);
+      bulk_g2s(base + PC * T::kChunk, wb + e0, bytes, &full[st]);
+    };
+    if (threadIdx.x == 0)
+      for (int64_t c = 0; c < nchunks && c < kZcStages; ++c) issue(c);
+    for (int64_t c = 0; c < nchunks; ++c) {
+      const uint32_t pos = iter + static_cast<uint32_t>(c);
+      const uint32_t st = pos % kZcStages;
+      mbar_wait(&full[st], (pos / kZcStages) & 1u);
+      const float* base = ring + static_cast<size_t>(st) * (PC + 1) * T::kChunk;
+      const int64_t e0 = c * T::kChunk;
+      const int n4 = static_cast<int>((nv - e0 < T::kChunk ? nv - e0 : int64_t{T::kChunk}) >> 2);
+      float4* w4 = reinterpret_cast<float4*>(wb + e0);
+      float* mh = kMom ? mom + head + e0 : nullptr;
+      const bool mvec = kMom && (reinterpret_cast<uintptr_t>(mh) & 15) == 0;
+      for (int q = threadIdx.x; q < n4; q += kThreads) {
+        float4 acc = reinterpret_cast<const float4*>(base)[q];
+#pragma unroll
+        for (int j = 1; j < PC; ++j) {
+          const float4 v = reinterpret_cast<const float4*>(base + j * T::kChunk)[q];
+          acc.x = __fadd_rn(acc.x, v.x);
+          acc.y = __fadd_rn(acc.y, v.y);
+          acc.z = __fadd_rn(acc.z, v.z);
+          acc.w = __fadd_rn(acc.w, v.w);
+        }
+        const float4 wv = reinterpret_cast<const float4*>(base + PC * T::kChunk)[q];
+        float4 mv = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (kMom && has_buf) {
+          if (mvec)
+            mv = reinterpret_cast<const float4*>(mh)[q];
+          else
+            mv = make_float4(mh[4 * q], mh[4 * q + 1], mh[4 * q + 2], mh[4 * q + 3]);
+        }
+        float4 o;
+        o.x = sgd_elem<kMom, kWd>(acc.x, wv.x, mv.x, hp, has_buf);
+        o.y = sgd_elem<kMom, kWd>(acc.y, wv.y, mv.y, hp, has_buf);
+        o.z = sgd_elem<kMom, kWd>(acc.z, wv.z, mv.z, hp, has_buf);
+        o.w = sgd_elem<kMom, kWd>(acc.w, wv.w, mv.w, hp, has_buf);
+        w4[q] = o;
+        if (kMom) {
+          if (mvec) {
+            reinterpret_cast<float4*>(mh)[q] = mv;
+          } else {
+            mh[4 * q] = mv.x;
+            mh[4 * q + 1] = mv.y;
+            mh[4 * q + 2] = mv.z;
+            mh[4 * q + 3] = mv.w;
+          }
+        }
+        if (kShadow && sh) store_bf16x4(sh + head + e0, q, o);
+      }
+      __syncthreads();  // every warp is done with this stage
+      if (threadIdx.x == 0 && c + kZcStages < nchunks) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(c + kZcStages);
+      }
+    }
+    iter += static_cast<uint32_t>(nchunks);
+    for (int64_t i = head + nv + threadIdx.x; i < n; i += kThreads) scalar(i);
+  });
+  signal_done(&flags->done[1], &flags->updated);
+}
+
 // ------------------------------------------- fused peer AG+unpack ---------
+// Source element of a unit: U.a + off on rank U.peer, i.e. at sa.delta[U.peer]
+// (sa = arena deltas for bucket slots, parameter deltas for zero-copy).
 template <bool kShadow>
 __global__ void __launch_bounds__(kThreads, 1)
     ag_unpack_peer_kernel(const Unit* __restrict__ units, const Slice* __restrict__ slices,
-                          PeerArgs pa, BucketFlags* flags) {
+                          PeerArgs pa, PeerArgs sa, BucketFlags* flags, int n_slices) {
   cta_wait_peers(&flags->updated, &flags->updated, pa);  // every owner updated its shard
-  walk_slice(units, slices, kPeerSlices, [&](const Unit& U, int64_t off, int64_t n) {
-    const float* src = at_peer(U.a + off, pa.delta[U.peer]);
+  walk_slice(units, slices, n_slices, [&](const Unit& U, int64_t off, int64_t n) {
+    const float* src = at_peer(U.a + off, sa.delta[U.peer]);
     float* dst = U.b + off;
     __nv_bfloat16* sh = (kShadow && U.c) ? static_cast<__nv_bfloat16*>(U.c) + off : nullptr;
     run_unit<Hint::kStream, kPeerUnroll>(
@@ -718,13 +1056,102 @@ cudaError_t launch_rs_update_peer(const Unit* units, const Slice* slices, int64_
 }
 
 cudaError_t launch_ag_unpack_peer(const Unit* units, const Slice* slices, int64_t total,
-                                  int with_shadow, const PeerArgs& pa, BucketFlags* flags,
-                                  cudaStream_t s) {
+                                  int with_shadow, const PeerArgs& pa, const PeerArgs& sa,
+                                  BucketFlags* flags, int n_slices, cudaStream_t s) {
   (void)total;
+  size_t smem = 0;
+#ifdef DEAR_ZC_SMEM_RESERVE
+  if (n_slices == kZcSlices) {
+    smem = DEAR_ZC_SMEM_RESERVE;
+    cudaFuncSetAttribute(ag_unpack_peer_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+    cudaFuncSetAttribute(ag_unpack_peer_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+  }
+#endif
   if (with_shadow)
-    ag_unpack_peer_kernel<true><<<bucket_grid(kPeerSlices), kThreads, 0, s>>>(units, slices, pa, flags);
+    ag_unpack_peer_kernel<true><<<bucket_grid(n_slices), kThreads, smem, s>>>(units, slices, pa, sa, flags, n_slices);
   else
-    ag_unpack_peer_kernel<false><<<bucket_grid(kPeerSlices), kThreads, 0, s>>>(units, slices, pa, flags);
+    ag_unpack_peer_kernel<false><<<bucket_grid(n_slices), kThreads, smem, s>>>(units, slices, pa, sa, flags, n_slices);
+  return cudaGetLastError();
+}
+
+template <int PC, bool kMom, bool kWd>
+void launch_rs_zc_p(const Unit* units, const Slice* slices, const HyperParams* hp, int has_buf,
+                    float* mom_base, int with_shadow, const PeerArgs& pa, const PeerArgs& ga,
+                    BucketFlags* flags, cudaStream_t s) {
+  const int grid = bucket_grid(kZcSlices);
+  // DEAR_ZC_SMEM_RESERVE (experiment builds): unused dynamic shared memory that
+  // keeps the zero-copy CTAs off SMs holding a GEMM CTA (soft SM partition,
+  // with DEAR_GEMM_MAX_CTAS leaving SMs free).
+  size_t smem = 0;
+#ifdef DEAR_ZC_SMEM_RESERVE
+  smem = DEAR_ZC_SMEM_RESERVE;
+  cudaFuncSetAttribute(rs_update_zc_kernel<PC, kMom, kWd, true>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  cudaFuncSetAttribute(rs_update_zc_kernel<PC, kMom, kWd, false>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+#endif
+  // Bulk-TMA staging for P in {2, 4, 8} with DEAR_ZC_TMA=1. Off by default:
+  // same isolated time as the register kernel at P = 4 (53 us per 25 MB
+  // bucket, so the per-SM LSU limit was not the bound), and its 160-192 KB
+  // ring cannot share an SM with a GEMM CTA (profiles/r01e_zc_experiments.md).
+  static const bool tma = [] {
+    const char* e = std::getenv("DEAR_ZC_TMA");
+    return e && e[0] == '1';
+  }();
+  if constexpr (PC > 0) {
+    if (tma) {
+      const int sm = ZcTma<PC>::kSmem;
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(rs_update_zc_tma_kernel<PC, kMom, kWd, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+        cudaFuncSetAttribute(rs_update_zc_tma_kernel<PC, kMom, kWd, false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+        attr = true;
+      }
+      if (with_shadow)
+        rs_update_zc_tma_kernel<PC, kMom, kWd, true><<<grid, kThreads, sm, s>>>(
+            units, slices, hp, has_buf, mom_base, pa, ga, flags);
+      else
+        rs_update_zc_tma_kernel<PC, kMom, kWd, false><<<grid, kThreads, sm, s>>>(
+            units, slices, hp, has_buf, mom_base, pa, ga, flags);
+      return;
+    }
+  }
+  if (with_shadow)
+    rs_update_zc_kernel<PC, kMom, kWd, true><<<grid, kThreads, smem, s>>>(units, slices, hp, has_buf,
+                                                                        mom_base, pa, ga, flags);
+  else
+    rs_update_zc_kernel<PC, kMom, kWd, false><<<grid, kThreads, smem, s>>>(units, slices, hp, has_buf,
+                                                                         mom_base, pa, ga, flags);
+}
+
+template <int PC>
+void launch_rs_zc_pc(const Unit* units, const Slice* slices, const HyperParams* hp, int has_buf,
+                     float* mom_base, int use_momentum, int use_wd, int with_shadow,
+                     const PeerArgs& pa, const PeerArgs& ga, BucketFlags* flags, cudaStream_t s) {
+  if (use_momentum && use_wd)
+    launch_rs_zc_p<PC, true, true>(units, slices, hp, has_buf, mom_base, with_shadow, pa, ga, flags, s);
+  else if (use_momentum)
+    launch_rs_zc_p<PC, true, false>(units, slices, hp, has_buf, mom_base, with_shadow, pa, ga, flags, s);
+  else if (use_wd)
+    launch_rs_zc_p<PC, false, true>(units, slices, hp, has_buf, mom_base, with_shadow, pa, ga, flags, s);
+  else
+    launch_rs_zc_p<PC, false, false>(units, slices, hp, has_buf, mom_base, with_shadow, pa, ga, flags, s);
+}
+
+cudaError_t launch_rs_update_zc(const Unit* units, const Slice* slices, const HyperParams* hp,
+                                int has_momentum_buf, float* mom_base, int use_momentum,
+                                int use_wd, int with_shadow, const PeerArgs& pa,
+                                const PeerArgs& ga, BucketFlags* flags, cudaStream_t s) {
+  switch (pa.P) {
+    case 2: launch_rs_zc_pc<2>(units, slices, hp, has_momentum_buf, mom_base, use_momentum, use_wd, with_shadow, pa, ga, flags, s); break;
+    case 4: launch_rs_zc_pc<4>(units, slices, hp, has_momentum_buf, mom_base, use_momentum, use_wd, with_shadow, pa, ga, flags, s); break;
+    case 8: launch_rs_zc_pc<8>(units, slices, hp, has_momentum_buf, mom_base, use_momentum, use_wd, with_shadow, pa, ga, flags, s); break;
+    default: launch_rs_zc_pc<0>(units, slices, hp, has_momentum_buf, mom_base, use_momentum, use_wd, with_shadow, pa, ga, flags, s); break;
+  }
   return cudaGetLastError();
 }
 

@@ -102,6 +102,13 @@ struct Bucket {
   Slice *pack_s = nullptr, *upd_s = nullptr, *unpack_s = nullptr;  // kSlices each
   Slice *upd_ps = nullptr, *unpack_ps = nullptr;  // kPeerSlices each (peer kernels)
   Slice* pack_ps = nullptr;                        // kPackPeerSlices (peer pack)
+  // Zero-copy peer path: RS units over the owned chunk (a = grad, b = param,
+  // c = bf16 copy) and AG units over the other chunks (a = b = param on the
+  // owner `peer`, c = bf16 copy); kPeerSlices slices each.
+  Unit *zrs_u = nullptr, *zag_u = nullptr;
+  int n_zrs = 0, n_zag = 0;
+  int64_t e_zrs = 0, e_zag = 0;
+  Slice *zrs_ps = nullptr, *zag_ps = nullptr;
   Unit* dir_u = nullptr;                           // P = 1 direct update (grad -> param)
   int n_dir = 0;
   int64_t e_dir = 0;
@@ -166,6 +173,11 @@ struct dear_ctx {
   // the gradients — 14 B/element instead of pack + update + unpack's 30.
   bool direct = false;
   PeerArgs pa{};
+  // Zero-copy (peer backend): every rank's gradient and parameter allocations
+  // are IPC-mapped too; ga / qa hold the per-rank deltas of those tensors.
+  bool zc = false;
+  bool zc_tables = false;  // finalize built the zero-copy unit tables
+  PeerArgs ga{}, qa{};
   std::vector<void*> peer_maps;  // cudaIpcOpenMemHandle mappings to close
   bool timing = false;
   std::vector<std::string> trace;
@@ -385,6 +397,10 @@ void dear_ctx::exec(const Op& op) {
     case OP_PACK:
       if (direct) break;  // P = 1: the update reads the gradients in place
       record_t(op.bucket, T_PACK0);
+      if (zc) {  // zero-copy: the reduce-scatter reads the gradients in place
+        record_t(op.bucket, T_PACK1);
+        break;
+      }
       if (peer) {
         // The kernel first waits (in-kernel) until every peer gathered from
         // our buffer, which it then rewrites. One CTA per SM, one contiguous
@@ -407,7 +423,16 @@ void dear_ctx::exec(const Op& op) {
       record_t(op.bucket, T_PACK1);
       break;
     case OP_RS:
-      if (peer) {
+      if (zc) {
+#ifdef DEAR_EXP_SKIP_ALL
+        break;  // attribution experiment only (variant build): no reduce-scatter
+#endif
+        cuda_check(launch_rs_update_zc(B->zrs_u, B->zrs_ps, hp_dev, B->mom_init ? 1 : 0, B->mom,
+                                       cfg.momentum != 0.0, cfg.weight_decay != 0.0,
+                                       B->any_shadow ? 1 : 0, pa, ga, B->flags, comm_stream),
+                   "zero-copy rs+update kernel");
+        if (cfg.momentum != 0.0) B->mom_init = true;
+      } else if (peer) {
         // Fused reduce-scatter + update over NVLink (OP_UPDATE becomes a no-op);
         // it waits in-kernel for every rank's pack of this bucket.
         cuda_check(launch_rs_update_peer(B->upd_u, B->upd_ps, B->e_upd, hp_dev, B->mom_init ? 1 : 0,
@@ -442,11 +467,20 @@ void dear_ctx::exec(const Op& op) {
       break;
     case OP_AG:
       if (!local) record_t(op.bucket, T_AG0);
-      if (peer) {
+      if (zc) {
+#if defined(DEAR_EXP_SKIP_AG) || defined(DEAR_EXP_SKIP_ALL)
+        break;  // attribution experiment only (variant build): no all-gather
+#endif
+        // Each owner's updated parameters, read over NVLink into ours.
+        cuda_check(launch_ag_unpack_peer(B->zag_u, B->zag_ps, B->e_zag, B->any_shadow ? 1 : 0,
+                                         pa, qa, B->flags, kZcSlices, comm_stream),
+                   "zero-copy ag kernel");
+      } else if (peer) {
         // Fused all-gather + unpack over NVLink (OP_UNPACK becomes a no-op);
         // it waits in-kernel for every owner's update of this bucket.
         cuda_check(launch_ag_unpack_peer(B->unpack_u, B->unpack_ps, B->e_unpack,
-                                         B->any_shadow ? 1 : 0, pa, B->flags, comm_stream),
+                                         B->any_shadow ? 1 : 0, pa, pa, B->flags, kPeerSlices,
+                                         comm_stream),
                    "ag+unpack kernel");
       } else if (!local && P > 1 && B->stride > 0) {
         nccl_check(ncclAllGather(B->buf + static_cast<int64_t>(rank) * B->stride, B->buf,
@@ -467,6 +501,13 @@ void dear_ctx::exec(const Op& op) {
       B->ag_capture = capture_id(comm_stream);
       break;
     case OP_CALLER_WAIT_PACKED:
+      if (zc && !buckets.empty()) {
+        // Zero-copy: peers read our gradients in their reduce-scatters, so
+        // "consumed" means every rank's last (plan-order) RS has finished.
+        const BucketFlags* f = buckets.back().flags;
+        cuda_check(launch_wait_peers(&f->updated, &f->updated, pa, comm_stream), "wait kernel");
+        cuda_check(cudaEventRecord(packed_ev, comm_stream), "cudaEventRecord");
+      }
       cuda_check(cudaStreamWaitEvent(op.stream, packed_ev, 0), "cudaStreamWaitEvent");
       break;
   }
@@ -761,6 +802,8 @@ int dear_finalize(dear_ctx* ctx) {
   // measure those kernels on one GPU).
   const char* dir_env = std::getenv("DEAR_DIRECT");
   c.direct = c.P == 1 && !c.peer && c.cfg.momentum == 0.0 && !(dir_env && dir_env[0] == '0');
+  // Zero-copy tables for a later dear_peer_connect (multi-process only).
+  c.zc_tables = !c.local && c.P > 1;
   // Unit tables.
   std::vector<Unit> host_units;
   struct Span { size_t pack, upd, unpack; };
@@ -779,12 +822,13 @@ int dear_finalize(dear_ctx* ctx) {
     size_t nu = 0;
     for_each_piece(c, B, bg[static_cast<size_t>(own)], bg[static_cast<size_t>(own) + 1],
                    [&](int, int64_t, int64_t, int64_t) { ++nu; });
-    units += 2 * n + nu + (c.direct ? n : 0);
+    units += 2 * n + nu + (c.direct ? n : 0) + (c.zc_tables ? n : 0);
   }
   const size_t float_bytes = (floats * sizeof(float) + 255) / 256 * 256;
   const size_t unit_bytes = (units * sizeof(Unit) + 255) / 256 * 256;
   const size_t per_bucket_slices = 3 * static_cast<size_t>(kSlices) + 2 * kPeerSlices +
-                                   kPackPeerSlices + (c.direct ? kSlices : 0);
+                                   kPackPeerSlices + (c.direct ? kSlices : 0) +
+                                   (c.zc_tables ? 2 * kZcSlices : 0);
   const size_t n_slices = plan.size() * per_bucket_slices;
   const size_t slice_bytes = (n_slices * sizeof(Slice) + 255) / 256 * 256;
   // Layout: [bucket buffers + momentum][flags] is identical on every rank (the
@@ -866,6 +910,32 @@ int dear_finalize(dear_ctx* ctx) {
       B.n_dir = static_cast<int>(host_units.size() - static_cast<size_t>(B.dir_u - up));
       B.e_dir = set_starts(host_units, static_cast<size_t>(B.dir_u - up));
     }
+    if (c.zc_tables) {
+      // Zero-copy RS: the owned chunk, gradient -> parameter (+ bf16 copy).
+      B.zrs_u = up + host_units.size();
+      for_each_piece(c, B, bg[static_cast<size_t>(own)], bg[static_cast<size_t>(own) + 1],
+                     [&](int l, int64_t j, int64_t len, int64_t) {
+                       const LayerReg& R = c.layers[static_cast<size_t>(l - 1)];
+                       void* sh = R.shadow ? static_cast<void*>(static_cast<uint16_t*>(R.shadow) + j) : nullptr;
+                       host_units.push_back({R.grad + j, R.param + j, sh, len, 0, 0, 0});
+                     });
+      B.n_zrs = static_cast<int>(host_units.size() - static_cast<size_t>(B.zrs_u - up));
+      B.e_zrs = set_starts(host_units, static_cast<size_t>(B.zrs_u - up));
+      // Zero-copy AG: every other chunk from its owner's parameters.
+      B.zag_u = up + host_units.size();
+      for (int ch = 0; ch < c.P; ++ch) {
+        if (ch == own) continue;
+        const int owner = (ch - 1 + c.P) % c.P;
+        for_each_piece(c, B, bg[static_cast<size_t>(ch)], bg[static_cast<size_t>(ch) + 1],
+                       [&](int l, int64_t j, int64_t len, int64_t) {
+                         const LayerReg& R = c.layers[static_cast<size_t>(l - 1)];
+                         void* sh = R.shadow ? static_cast<void*>(static_cast<uint16_t*>(R.shadow) + j) : nullptr;
+                         host_units.push_back({R.param + j, R.param + j, sh, len, 0, owner, 0});
+                       });
+      }
+      B.n_zag = static_cast<int>(host_units.size() - static_cast<size_t>(B.zag_u - up));
+      B.e_zag = set_starts(host_units, static_cast<size_t>(B.zag_u - up));
+    }
     // Equal element slices per CTA for each op (one wave of kSlices CTAs).
     Slice* hs = host_slices.data() + g * per_bucket_slices;
     make_slices(host_units.data() + (B.pack_u - up), B.n_pack, B.e_pack, hs, kSlices, 0);
@@ -888,6 +958,14 @@ int dear_finalize(dear_ctx* ctx) {
     B.unpack_ps = B.upd_ps + kPeerSlices;
     B.pack_ps = B.unpack_ps + kPeerSlices;
     B.dir_s = c.direct ? B.pack_ps + kPackPeerSlices : nullptr;
+    if (c.zc_tables) {
+      const size_t z0 = 3 * kSlices + 2 * kPeerSlices + kPackPeerSlices + (c.direct ? kSlices : 0);
+      make_slices(host_units.data() + (B.zrs_u - up), B.n_zrs, B.e_zrs, hs + z0, kZcSlices, 2);
+      make_slices(host_units.data() + (B.zag_u - up), B.n_zag, B.e_zag, hs + z0 + kZcSlices,
+                  kZcSlices, 2);
+      B.zrs_ps = B.pack_s + z0;
+      B.zag_ps = B.zrs_ps + kZcSlices;
+    }
     B.ag_done = new_event(false);
     for (int k = 0; k < T_COUNT; ++k) B.t[k] = new_event(true);
     B.layers_left = B.high - B.low + 1;
@@ -1139,6 +1217,60 @@ int dear_set_lr(dear_ctx* ctx, double lr) {
   DEAR_API_END
 }
 
+// ---- zero-copy span: one allocation holding every layer's tensor ----------
+namespace {
+struct TensorSpan {
+  bool ok = false;
+  char* lo = nullptr;    // lowest tensor address
+  char* base = nullptr;  // allocation base
+  uint64_t layout = 0;   // hash of every tensor's offset from `lo`
+};
+
+using MemGetAddressRange = int (*)(uintptr_t*, size_t*, uintptr_t);
+
+TensorSpan tensor_span(const dear_ctx& c, bool grads) {
+  TensorSpan sp;
+  static MemGetAddressRange range = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess)
+      return static_cast<MemGetAddressRange>(nullptr);
+    return reinterpret_cast<MemGetAddressRange>(fn);
+  }();
+  if (!range) return sp;
+  char *lo = nullptr, *hi = nullptr;
+  for (const LayerReg& R : c.layers) {
+    char* p = reinterpret_cast<char*>(grads ? R.grad : R.param);
+    if (!p || R.numel <= 0) continue;
+    if (!lo || p < lo) lo = p;
+    if (!hi || p + R.numel * 4 > hi) hi = p + R.numel * 4;
+  }
+  if (!lo) return sp;
+  uintptr_t base = 0;
+  size_t size = 0;
+  if (range(&base, &size, reinterpret_cast<uintptr_t>(lo)) != 0) return sp;
+  if (reinterpret_cast<uintptr_t>(hi) > base + size) return sp;  // several allocations
+  uint64_t h = 1469598103934665603ULL;
+  for (const LayerReg& R : c.layers) {
+    const char* p = reinterpret_cast<const char*>(grads ? R.grad : R.param);
+    h = fnv(h, p && R.numel > 0 ? static_cast<uint64_t>(p - lo) : ~0ULL);
+  }
+  sp.ok = true;
+  sp.lo = lo;
+  sp.base = reinterpret_cast<char*>(base);
+  sp.layout = h;
+  return sp;
+}
+
+// Handle record (DEAR_PEER_HANDLE_BYTES):
+//   [0,64) arena IPC handle  [64,72) arena bytes  [72,76) rank  [76,80) zero-copy ok
+//   [80,144) gradient allocation handle  [144,208) parameter allocation handle
+//   [208,216) grad lo - base  [216,224) param lo - base
+//   [224,232) gradient layout hash  [232,240) parameter layout hash
+constexpr size_t kH_ZC = 76, kH_G = 80, kH_Q = 144, kH_GOFF = 208, kH_QOFF = 216,
+                 kH_GLAY = 224, kH_QLAY = 232;
+}  // namespace
+
 int dear_peer_handle(dear_ctx* ctx, uint8_t out[DEAR_PEER_HANDLE_BYTES]) {
   DEAR_API_BEGIN
   need(ctx, true);
@@ -1153,6 +1285,28 @@ int dear_peer_handle(dear_ctx* ctx, uint8_t out[DEAR_PEER_HANDLE_BYTES]) {
   memcpy(out + 64, &sz, 8);
   const int32_t r = ctx->rank;
   memcpy(out + 72, &r, 4);
+  // Zero-copy: the gradients and parameters each in one exportable allocation.
+  const char* env = std::getenv("DEAR_ZERO_COPY");
+  int32_t zc = ctx->zc_tables && !(env && env[0] == '0');
+  TensorSpan gs, qs;
+  cudaIpcMemHandle_t gh{}, qh{};
+  if (zc) {
+    gs = tensor_span(*ctx, true);
+    qs = tensor_span(*ctx, false);
+    zc = gs.ok && qs.ok && cudaIpcGetMemHandle(&gh, gs.base) == cudaSuccess &&
+         cudaIpcGetMemHandle(&qh, qs.base) == cudaSuccess;
+    cudaGetLastError();  // a non-exportable allocation only disables zero-copy
+  }
+  memcpy(out + kH_ZC, &zc, 4);
+  if (zc) {
+    memcpy(out + kH_G, &gh, 64);
+    memcpy(out + kH_Q, &qh, 64);
+    const uint64_t goff = static_cast<uint64_t>(gs.lo - gs.base), qoff = static_cast<uint64_t>(qs.lo - qs.base);
+    memcpy(out + kH_GOFF, &goff, 8);
+    memcpy(out + kH_QOFF, &qoff, 8);
+    memcpy(out + kH_GLAY, &gs.layout, 8);
+    memcpy(out + kH_QLAY, &qs.layout, 8);
+  }
   DEAR_API_END
 }
 
@@ -1164,9 +1318,31 @@ int dear_peer_connect(dear_ctx* ctx, const uint8_t* handles, int32_t n) {
   if (c.peer) invalid("dear_peer_connect: already connected");
   if (!handles || n != c.P) invalid("dear_peer_connect: need one handle per rank");
   if (c.P > kMaxPeers) invalid("dear_peer_connect: at most 16 ranks");
-  PeerArgs pa{};
-  pa.P = c.P;
-  pa.rank = c.rank;
+  PeerArgs pa{}, ga{}, qa{};
+  pa.P = ga.P = qa.P = c.P;
+  pa.rank = ga.rank = qa.rank = c.rank;
+  // Zero-copy only when every rank offers it with the same tensor layouts
+  // (and the same 16 B phase, so the kernels' float4 streams line up).
+  bool zc = true;
+  uint64_t glay = 0, qlay = 0, goff0 = 0, qoff0 = 0;
+  for (int k = 0; k < c.P; ++k) {
+    const uint8_t* h = handles + static_cast<size_t>(k) * DEAR_PEER_HANDLE_BYTES;
+    int32_t z = 0;
+    uint64_t gl = 0, ql = 0, go = 0, qo = 0;
+    memcpy(&z, h + kH_ZC, 4);
+    memcpy(&gl, h + kH_GLAY, 8);
+    memcpy(&ql, h + kH_QLAY, 8);
+    memcpy(&go, h + kH_GOFF, 8);
+    memcpy(&qo, h + kH_QOFF, 8);
+    if (k == 0) {
+      glay = gl, qlay = ql, goff0 = go, qoff0 = qo;
+    }
+    zc = zc && z && gl == glay && ql == qlay && (go & 15) == (goff0 & 15) &&
+         (qo & 15) == (qoff0 & 15);
+  }
+  const TensorSpan gs = zc ? tensor_span(c, true) : TensorSpan{};
+  const TensorSpan qs = zc ? tensor_span(c, false) : TensorSpan{};
+  zc = zc && gs.ok && qs.ok;
   std::vector<void*> maps;
   try {
     for (int k = 0; k < c.P; ++k) {
@@ -1177,24 +1353,78 @@ int dear_peer_connect(dear_ctx* ctx, const uint8_t* handles, int32_t n) {
       memcpy(&r, h + 72, 4);
       if (r != k) invalid("dear_peer_connect: handles must be in rank order");
       if (sz != c.arena_bytes) invalid("dear_peer_connect: ranks registered different models");
-      if (k == c.rank) {
-        pa.delta[k] = 0;
-        continue;
+      if (k == c.rank) continue;
+      auto open = [&](size_t at) {
+        cudaIpcMemHandle_t ih;
+        memcpy(&ih, h + at, 64);
+        void* p = nullptr;
+        cuda_check(cudaIpcOpenMemHandle(&p, ih, cudaIpcMemLazyEnablePeerAccess),
+                   "cudaIpcOpenMemHandle");
+        maps.push_back(p);
+        return static_cast<char*>(p);
+      };
+      pa.delta[k] = static_cast<int64_t>(open(0) - c.arena);
+      if (zc) {
+        uint64_t go = 0, qo = 0;
+        memcpy(&go, h + kH_GOFF, 8);
+        memcpy(&qo, h + kH_QOFF, 8);
+        char* gbase = open(kH_G);
+        // Gradients and parameters in one allocation: map it once.
+        char* qbase = memcmp(h + kH_G, h + kH_Q, 64) == 0 ? gbase : open(kH_Q);
+        ga.delta[k] = static_cast<int64_t>(gbase + go - gs.lo);
+        qa.delta[k] = static_cast<int64_t>(qbase + qo - qs.lo);
       }
-      cudaIpcMemHandle_t ih;
-      memcpy(&ih, h, 64);
-      void* p = nullptr;
-      cuda_check(cudaIpcOpenMemHandle(&p, ih, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
-      maps.push_back(p);
-      pa.delta[k] = static_cast<int64_t>(static_cast<char*>(p) - c.arena);
     }
   } catch (...) {
     for (void* m : maps) cudaIpcCloseMemHandle(m);
     throw;
   }
   c.pa = pa;
+  c.ga = ga;
+  c.qa = qa;
   c.peer_maps = std::move(maps);
   c.peer = true;
+  if (zc) {
+    // No pack, so no pre-scaling: the update applies 1/P after the ring sum
+    // (collective.cpp:159-164's order; for P = 2^k the same bits either way).
+    c.zc = true;
+    c.hp_host.prescaled = 0;
+    cuda_check(cudaMemcpy(c.hp_dev, &c.hp_host, sizeof(HyperParams), cudaMemcpyHostToDevice),
+               "cudaMemcpy(hp)");
+  }
+  DEAR_API_END
+}
+
+int dear_peer_zero_copy(dear_ctx* ctx, int32_t* on) {
+  DEAR_API_BEGIN
+  need(ctx, true);
+  if (!on) invalid("dear_peer_zero_copy: null output");
+  *on = ctx->zc ? 1 : 0;
+  DEAR_API_END
+}
+
+int dear_bench_stage(dear_ctx* ctx, int32_t stage, int32_t reps, void* stream) {
+  DEAR_API_BEGIN
+  need(ctx, true);
+  dear_ctx& c = *ctx;
+  if (stage < 0 || stage > 3 || reps < 0) invalid("dear_bench_stage: stage in 0..3, reps >= 0");
+  if (stage == 3 && !c.direct) invalid("dear_bench_stage: no direct-update tables (P > 1 or DEAR_DIRECT=0)");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const bool wd = c.cfg.weight_decay != 0.0, mom = c.cfg.momentum != 0.0;
+  for (int r = 0; r < reps; ++r) {
+    for (Bucket& B : c.buckets) {
+      cudaError_t e = cudaSuccess;
+      switch (stage) {
+        case 0: e = launch_pack(B.pack_u, B.pack_s, B.e_pack, c.pack_scale, 0, s); break;
+        // has_buf = 0: momentum (if any) is re-seeded each launch, the same traffic
+        case 1: e = launch_update(B.upd_u, B.upd_s, B.e_upd, c.hp_dev, 0, mom, wd, 0, s); break;
+        case 2: e = launch_unpack(B.unpack_u, B.unpack_s, B.e_unpack, B.any_shadow ? 1 : 0, 0, s); break;
+        default: e = launch_update_direct(B.dir_u, B.dir_s, B.e_dir, c.hp_dev, wd,
+                                          B.any_shadow ? 1 : 0, s); break;
+      }
+      cuda_check(e, "dear_bench_stage");
+    }
+  }
   DEAR_API_END
 }
 

@@ -20,7 +20,7 @@ from typing import Optional
 
 import torch
 
-from ._lib import POLICIES, DearCfg, check, lib
+from ._lib import DEAR_PEER_HANDLE_BYTES, POLICIES, DearCfg, check, lib
 
 
 def _dist_ready() -> bool:
@@ -118,6 +118,7 @@ class Runtime:
             raise ValueError("the peer backend needs one process per GPU (not a LocalGroup)")
         self.policy = policy
         self.backend = backend
+        self.zero_copy = False  # set by the peer handshake (dear_peer_zero_copy)
         cfg = DearCfg(POLICIES[policy], int(fusion_buffer_bytes) if "FUSED" in policy else 0,
                       int(dear_group_dependency), float(lr),
                       float(momentum), float(dampening), float(weight_decay), int(nesterov),
@@ -164,12 +165,15 @@ class Runtime:
         """Exchange arena IPC handles over torch.distributed and map the peers."""
         import torch.distributed as dist
 
-        buf = C.create_string_buffer(128)
+        buf = C.create_string_buffer(DEAR_PEER_HANDLE_BYTES)
         check(lib().dear_peer_handle(self._ctx, buf))
         handles = [None] * self.world_size
         dist.all_gather_object(handles, buf.raw)
         check(lib().dear_peer_connect(self._ctx, b"".join(handles), self.world_size))
         dist.barrier()
+        on = C.c_int32()
+        check(lib().dear_peer_zero_copy(self._ctx, C.byref(on)))
+        self.zero_copy = bool(on.value)
 
     # -- schedule hooks ----------------------------------------------------
     def grad_ready(self, layer: int, stream=None) -> None:
@@ -217,6 +221,12 @@ class Runtime:
         buf = C.create_string_buffer(int(need.value))
         check(lib().dear_trace(self._ctx, buf, need.value, C.byref(need)))
         return [x for x in buf.value.decode().split("\n") if x]
+
+    def bench_stage(self, stage: str, reps: int = 1, stream=None) -> None:
+        """Measurement hook (dear_bench_stage): `reps` rounds of one bucket
+        kernel over every bucket, outside the schedule (graph-capturable)."""
+        k = {"pack": 0, "update": 1, "unpack": 2, "direct": 3}[stage]
+        check(lib().dear_bench_stage(self._ctx, k, int(reps), _stream_ptr(stream)))
 
     def set_timing(self, enable: bool) -> None:
         check(lib().dear_set_timing(self._ctx, int(enable)))

@@ -34,7 +34,10 @@ def close(a, b, tol=1e-5):
 
 
 def run_runtime(comm, rank, P, policy, buf, steps, lr, backend="nccl", comm_order=None,
-                **kw):  # explicit backend
+                flat=False, **kw):  # explicit backend
+    """flat=True: every layer's parameters (and gradients) are views of ONE flat
+    tensor at 64-element aligned offsets, which lets the peer backend map them
+    directly (zero-copy); the runtime must then report zero_copy."""
     o = Restated()
     numels = RAGGED
     offs = np.concatenate([[0], np.cumsum(numels)]).astype(np.int64)
@@ -43,13 +46,26 @@ def run_runtime(comm, rank, P, policy, buf, steps, lr, backend="nccl", comm_orde
     rt = dear.Runtime(comm, rank, P, policy=policy, fusion_buffer_bytes=buf, lr=lr, stream=s,
                       backend=backend, dear_group_dependency=comm_order is not None, **kw)
     params, grads = [], []
+    if flat:
+        aoffs = [0]
+        for n in numels:
+            aoffs.append(aoffs[-1] + (n + 63) // 64 * 64)
+        pflat = torch.zeros(aoffs[-1] + 64, device="cuda")
+        gflat = torch.zeros_like(pflat)
     for l in range(1, len(numels) + 1):
-        p = torch.from_numpy(w0[offs[l - 1]:offs[l]].copy()).cuda()
-        g = torch.zeros_like(p)
+        src = torch.from_numpy(w0[offs[l - 1]:offs[l]].copy()).cuda()
+        if flat:
+            p = pflat[aoffs[l - 1]:aoffs[l - 1] + numels[l - 1]]
+            p.copy_(src)
+            g = gflat[aoffs[l - 1]:aoffs[l - 1] + numels[l - 1]]
+        else:
+            p, g = src, torch.zeros_like(src)
         rt.register(l, p, g)
         params.append(p)
         grads.append(g)
     rt.finalize()
+    if flat and backend == "peer" and os.environ.get("DEAR_ZERO_COPY", "1") != "0":
+        assert rt.zero_copy, "flat parameters/gradients must enable the zero-copy peer path"
     if comm_order is not None:
         rt.set_comm_order(comm_order)
     with torch.cuda.stream(s):
@@ -126,24 +142,29 @@ def case_peer(rank, P):
     comm = dear.init()
     o = Restated()
     ok = True
-    for policy, buf in (("DEAR_FUSED", 100_000), ("DEAR", 0), ("WFBP_FUSED", 400_000),
-                        ("WFBP", 0), ("DEAR_FUSED", 25_000_000)):
-        w, same, _ = run_runtime(comm, rank, P, policy, buf, 3, 0.05, backend="peer")
-        exp32 = oracle_run(o, RAGGED, P, 3, policy, buf, 0.05, f32=True)
-        exp64 = oracle_run(o, RAGGED, P, 3, policy, buf, 0.05, f32=False)
-        good = same and np.array_equal(w, exp32) and close(w.astype(np.float64), exp64)
+    for flat in (False, True):
+        for policy, buf in (("DEAR_FUSED", 100_000), ("DEAR", 0), ("WFBP_FUSED", 400_000),
+                            ("WFBP", 0), ("DEAR_FUSED", 25_000_000)):
+            w, same, _ = run_runtime(comm, rank, P, policy, buf, 3, 0.05, backend="peer",
+                                     flat=flat)
+            exp32 = oracle_run(o, RAGGED, P, 3, policy, buf, 0.05, f32=True)
+            exp64 = oracle_run(o, RAGGED, P, 3, policy, buf, 0.05, f32=False)
+            good = same and np.array_equal(w, exp32) and close(w.astype(np.float64), exp64)
+            if rank == 0:
+                print(f"[peer P={P} {'zero-copy' if flat else 'slots'}] {policy:11s} "
+                      f"buf={buf:>9} replicas={same} "
+                      f"bit_exact_fp32_ring={np.array_equal(w, exp32)} "
+                      f"oracle_1e-5={close(w.astype(np.float64), exp64)}", flush=True)
+            ok &= good
+        kw = dict(momentum=0.9, weight_decay=1e-3, nesterov=True)
+        w, same, _ = run_runtime(comm, rank, P, "DEAR_FUSED", 200_000, 4, 0.02, backend="peer",
+                                 flat=flat, **kw)
+        exp32 = oracle_run(o, RAGGED, P, 4, "DEAR_FUSED", 200_000, 0.02, f32=True, **kw)
+        good = same and np.array_equal(w, exp32)
         if rank == 0:
-            print(f"[peer P={P}] {policy:11s} buf={buf:>9} replicas={same} "
-                  f"bit_exact_fp32_ring={np.array_equal(w, exp32)} "
-                  f"oracle_1e-5={close(w.astype(np.float64), exp64)}", flush=True)
+            print(f"[peer P={P} {'zero-copy' if flat else 'slots'}] momentum/wd/nesterov "
+                  f"bit_exact={good}", flush=True)
         ok &= good
-    kw = dict(momentum=0.9, weight_decay=1e-3, nesterov=True)
-    w, same, _ = run_runtime(comm, rank, P, "DEAR_FUSED", 200_000, 4, 0.02, backend="peer", **kw)
-    exp32 = oracle_run(o, RAGGED, P, 4, "DEAR_FUSED", 200_000, 0.02, f32=True, **kw)
-    good = same and np.array_equal(w, exp32)
-    if rank == 0:
-        print(f"[peer P={P}] momentum/wd/nesterov bit_exact={good}", flush=True)
-    ok &= good
     # dear_group_dependency: all-gathers back-filled between reduce-scatters
     from paper_2302_12445_b200 import costmodel as cm
     L = len(RAGGED)
@@ -153,7 +174,7 @@ def case_peer(rank, P):
                                  100_000, P, 0.0, 0.0, group_dependency=True,
                                  rs_times=[1.5] * G, ag_times=[1.0] * G)["comm_order"]
     w, same, trace = run_runtime(comm, rank, P, "DEAR_FUSED", 100_000, 3, 0.05, "peer",
-                                 comm_order=order)
+                                 comm_order=order, flat=True)
     exp32 = oracle_run(o, RAGGED, P, 3, "DEAR_FUSED", 100_000, 0.05, f32=True)
     exp64 = oracle_run(o, RAGGED, P, 3, "DEAR_FUSED", 100_000, 0.05, f32=False)
     want = [("RS g%d" % v) if v > 0 else ("AG g%d" % -v) for v in order]

@@ -51,7 +51,18 @@ def main():
     ns = argparse.Namespace(group_dependency=a.group_dependency, buffer=a.buffer, lr=0.05,
                             momentum=0.0, backend=a.backend, contention=a.contention,
                             order_search=1)
-    rt = bench.make_runtime(ns, model, comm, rank, world, stream, a.policy, True)
+    if a.policy == "NONE":  # compute only: the same marks without the runtime
+        class _NoRt:
+            comm_order_info = None
+
+            def __getattr__(self, name):
+                return lambda *args, **kw: None
+
+            def timeline(self, base):
+                return []
+        rt = _NoRt()
+    else:
+        rt = bench.make_runtime(ns, model, comm, rank, world, stream, a.policy, True)
     # external: recorded inside the graph capture, timed after a replay
     ev = {k: torch.cuda.Event(enable_timing=True, external=True)
           for k in ("base", "ff", "bp", "end")}

@@ -1,0 +1,23 @@
+set -u
+mkdir -p gpurun_out
+N=${N:-4}
+export DEAR_TEST_NPROC=$N
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node=$N --master-addr 127.0.0.1 --master-port 29511 tests/dist_worker.py peer > gpurun_out/zc4_peer.log 2>&1; echo "peer rc=$?"
+grep "^\[peer" gpurun_out/zc4_peer.log
+tl() {  # tag env... args
+  tag=$1; shift
+  env "$@" timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node=$N --master-addr 127.0.0.1 --master-port 29520 tools/graph_timeline.py $TLARGS > gpurun_out/tl4_$tag.log 2>&1; echo "tl $tag rc=$?"
+  grep '"rank"' gpurun_out/tl4_$tag.log | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); c=d['comm_order'] or {}
+print(d['marks_ms'], c.get('ags_during_backprop'), c.get('stage_us_mean'), d['rs_busy_ms'], d['ag_busy_ms'])"
+}
+TLARGS="--policy NONE" tl none X=1
+TLARGS="--policy DEAR_FUSED" tl dear_zc X=1
+TLARGS="--policy DEAR_FUSED" tl dear_zc_k4x8 DEAR_LIB=libdear_k4x8.so
+TLARGS="--policy DEAR_FUSED" tl dear_slots DEAR_ZERO_COPY=0
+TLARGS="--policy WFBP_FUSED" tl wfbp_zc X=1
+timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node=$N --master-addr 127.0.0.1 --master-port 29512 bench.py --gpus $N > gpurun_out/zc4_bench.log 2>&1; echo "bench rc=$?"
+grep '"metric"' gpurun_out/zc4_bench.log | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); ns=d.get('north_star',{})
+print(d['value'], d['ms_per_step'], d['config'].get('zero_copy'), d.get('exposed_comm_pct'), d.get('dear_over_wfbp'), d.get('busbw_gbs'))
+print(json.dumps(ns))"
