@@ -37,6 +37,19 @@ constexpr int64_t kUnitElems = 1 << 20;
 #define DEAR_SLICES_PER_SM 4
 #endif
 constexpr int kSlices = 148 * DEAR_SLICES_PER_SM;
+// The update kernels stream two inputs per round (run_unit_pre) and need more
+// registers: 3 CTAs per SM for the shard update, 2 for the P = 1 direct update
+// (graph-chained A/B, profiles/r01e_hbm_kernels_ab.log). Their slice tables use
+// the first kUpdSlices / kDirSlices entries of a kSlices-sized region.
+#ifndef DEAR_UPD_CTAS_PER_SM
+#define DEAR_UPD_CTAS_PER_SM 3
+#endif
+#ifndef DEAR_DIR_CTAS_PER_SM
+#define DEAR_DIR_CTAS_PER_SM 2
+#endif
+constexpr int kUpdSlices = 148 * DEAR_UPD_CTAS_PER_SM;
+constexpr int kDirSlices = 148 * DEAR_DIR_CTAS_PER_SM;
+static_assert(kUpdSlices <= kSlices && kDirSlices <= kSlices, "slice regions are kSlices long");
 // NVLink-bound peer kernels need far fewer CTAs to saturate the links
 // (~1.2 MB in flight); a small grid leaves the SMs to the concurrent GEMMs.
 #ifndef DEAR_PEER_SLICES

@@ -22,7 +22,17 @@
 namespace dear {
 namespace {
 
-constexpr int kThreads = 256;
+#ifndef DEAR_KTHREADS
+#define DEAR_KTHREADS 256
+#endif
+constexpr int kThreads = DEAR_KTHREADS;
+// Zero-copy / peer kernels: an optional register cap (experiments) so that one
+// comm CTA always fits next to a GEMM CTA but two never share an SM.
+#ifdef DEAR_ZC_MAXNREG
+#define DEAR_ZC_BOUNDS __maxnreg__(DEAR_ZC_MAXNREG)
+#else
+#define DEAR_ZC_BOUNDS __launch_bounds__(kThreads, 1)
+#endif
 #ifndef DEAR_HBM_UNROLL
 #define DEAR_HBM_UNROLL 4
 #endif
@@ -73,9 +83,13 @@ __device__ __forceinline__ float4 ld4(const float4* p) {
 // body(q, v) runs on every lane whose q < n4. All loads of one round (kUnroll
 // vectors per lane, plus the one vector past the round that lane 31 needs
 // when M != 0) are issued before any is consumed: no dependent second trip.
-template <int M, Hint H, int kUnroll, typename Body>
+// `pre` (optional, kPre): a second stream indexed like the destination
+// (pre[q] pairs with destination vector q), loaded in the same round as the
+// source so the body never starts a dependent second memory trip; the body
+// then receives it as its third argument.
+template <int M, Hint H, int kUnroll, bool kPre = false, typename Body>
 __device__ __forceinline__ void warp_stream(const float* src_floor, int64_t n4, int64_t qmax,
-                                            Body&& body) {
+                                            Body&& body, const float4* pre = nullptr) {
   const float4* s4 = reinterpret_cast<const float4*>(src_floor);
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -84,10 +98,12 @@ __device__ __forceinline__ void warp_stream(const float* src_floor, int64_t n4, 
   for (int64_t base = static_cast<int64_t>(warp) * 32 * kUnroll; base < n4;
        base += static_cast<int64_t>(kWarps) * 32 * kUnroll) {
     float4 a[kUnroll];
+    float4 p[kPre ? kUnroll : 1];
 #pragma unroll
     for (int k = 0; k < kUnroll; ++k) {
       const int64_t q = base + k * 32 + lane;
       a[k] = q <= qmax ? ld4<H>(s4 + q) : zero;
+      if constexpr (kPre) p[k] = q < n4 ? __ldcs(pre + q) : zero;
     }
     float4 extra = zero;
     if constexpr (M != 0) {
@@ -109,7 +125,11 @@ __device__ __forceinline__ void warp_stream(const float* src_floor, int64_t n4, 
         }
         if (lane == 31) b = nxt;
       }
-      if (q < n4) body(q, realign<M>(a[k], b));
+      if constexpr (kPre) {
+        if (q < n4) body(q, realign<M>(a[k], b), p[k]);
+      } else {
+        if (q < n4) body(q, realign<M>(a[k], b));
+      }
     }
   }
 }
@@ -142,6 +162,42 @@ __device__ __forceinline__ void run_unit(const float* src, const float* dst, int
       default:
         warp_stream<3, H, KU>(floor, n4, qmax, [&](int64_t q, float4 v) { vec_fn(head, q, v); });
         break;
+    }
+  }
+  for (int64_t i = head + n4 * 4 + threadIdx.x; i < len; i += kThreads) scalar_fn(i);
+}
+
+// run_unit with a second destination-aligned input stream `pre` (element i
+// of `pre` pairs with dst[i]); vec_fn(head, q, v_src, v_pre).
+template <Hint H, int KU = kUnroll, typename HeadFn, typename VecFn>
+__device__ __forceinline__ void run_unit_pre(const float* src, const float* dst, const float* pre,
+                                             int64_t len, HeadFn&& scalar_fn, VecFn&& vec_fn) {
+  int64_t head = ((16 - (reinterpret_cast<uintptr_t>(dst) & 15)) & 15) >> 2;
+  if (head > len) head = len;
+  if ((reinterpret_cast<uintptr_t>(pre + head) & 15) != 0) {
+    // `pre` out of phase with the destination (not produced by the runtime's
+    // layouts): per-lane scalar gathers of it inside the body.
+    run_unit<H, KU>(src, dst, len, scalar_fn, [&](int64_t h, int64_t q, float4 v) {
+      const float* pp = pre + h + 4 * q;
+      vec_fn(h, q, v, make_float4(pp[0], pp[1], pp[2], pp[3]));
+    });
+    return;
+  }
+  if (threadIdx.x < head) scalar_fn(static_cast<int64_t>(threadIdx.x));
+  const int64_t rest = len - head;
+  const int64_t n4 = rest >> 2;
+  if (n4 > 0) {
+    const float* s = src + head;
+    const int m = static_cast<int>((reinterpret_cast<uintptr_t>(s) & 15) >> 2);
+    const float* floor = s - m;
+    const int64_t qmax = (m + rest - 1) >> 2;
+    const float4* p4 = reinterpret_cast<const float4*>(pre + head);
+    auto body = [&](int64_t q, float4 v, float4 w) { vec_fn(head, q, v, w); };
+    switch (m) {
+      case 0: warp_stream<0, H, KU, true>(floor, n4, qmax, body, p4); break;
+      case 1: warp_stream<1, H, KU, true>(floor, n4, qmax, body, p4); break;
+      case 2: warp_stream<2, H, KU, true>(floor, n4, qmax, body, p4); break;
+      default: warp_stream<3, H, KU, true>(floor, n4, qmax, body, p4); break;
     }
   }
   for (int64_t i = head + n4 * 4 + threadIdx.x; i < len; i += kThreads) scalar_fn(i);
@@ -301,25 +357,24 @@ __device__ __forceinline__ float sgd_elem(float g, float w, float& m, const Hype
 }
 
 template <bool kMom, bool kWd>
-__global__ void __launch_bounds__(kThreads, kCtasPerSm) update_kernel(const Unit* __restrict__ units,
+__global__ void __launch_bounds__(kThreads, DEAR_UPD_CTAS_PER_SM) update_kernel(const Unit* __restrict__ units,
                                                              const Slice* __restrict__ slices,
                                                              const HyperParams* __restrict__ hpp,
                                                              int has_buf) {
   const HyperParams hp = *hpp;
-  walk_slice(units, slices, kSlices, [&](const Unit& U, int64_t off, int64_t n) {
+  walk_slice(units, slices, kUpdSlices, [&](const Unit& U, int64_t off, int64_t n) {
     const float* w = U.a + off;
     float* g = U.b + off;
     float* mom = kMom ? static_cast<float*>(U.c) + off : nullptr;
-    run_unit<Hint::kKeep>(
-        w, g, n,
+    run_unit_pre<Hint::kKeep>(
+        w, g, g, n,
         [&](int64_t i) {
           float m = kMom ? mom[i] : 0.f;
           g[i] = sgd_elem<kMom, kWd>(g[i], w[i], m, hp, has_buf);
           if (kMom) mom[i] = m;
         },
-        [&](int64_t head, int64_t q, float4 wv) {
+        [&](int64_t head, int64_t q, float4 wv, float4 gv) {
           float4* g4 = reinterpret_cast<float4*>(g + head);
-          float4 gv = __ldcs(g4 + q);
           float4 mv = make_float4(0.f, 0.f, 0.f, 0.f);
           if (kMom && has_buf) mv = reinterpret_cast<float4*>(mom + head)[q];
           gv.x = sgd_elem<kMom, kWd>(gv.x, wv.x, mv.x, hp, has_buf);
@@ -338,25 +393,24 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) update_kernel(const Unit
 // refreshed) — 14 B per element. Same per-element operations as update_kernel
 // (sum * 1/P with P = 1 is exact), so the result is bit-identical.
 template <bool kWd, bool kShadow>
-__global__ void __launch_bounds__(kThreads, kCtasPerSm) update_direct_kernel(
+__global__ void __launch_bounds__(kThreads, DEAR_DIR_CTAS_PER_SM) update_direct_kernel(
     const Unit* __restrict__ units, const Slice* __restrict__ slices,
     const HyperParams* __restrict__ hpp) {
   const HyperParams hp = *hpp;
-  walk_slice(units, slices, kSlices, [&](const Unit& U, int64_t off, int64_t n) {
+  walk_slice(units, slices, kDirSlices, [&](const Unit& U, int64_t off, int64_t n) {
     const float* g = U.a + off;
     float* w = U.b + off;
     __nv_bfloat16* sh = (kShadow && U.c) ? static_cast<__nv_bfloat16*>(U.c) + off : nullptr;
-    run_unit<Hint::kStream>(
-        g, w, n,
+    run_unit_pre<Hint::kStream>(
+        g, w, w, n,
         [&](int64_t i) {
           float m = 0.f;
           const float v = sgd_elem<false, kWd>(g[i], w[i], m, hp, false);
           w[i] = v;
           if (kShadow && sh) sh[i] = __float2bfloat16_rn(v);
         },
-        [&](int64_t head, int64_t q, float4 gv) {
+        [&](int64_t head, int64_t q, float4 gv, float4 v) {
           float4* w4 = reinterpret_cast<float4*>(w + head);
-          float4 v = w4[q];
           float m = 0.f;
           v.x = sgd_elem<false, kWd>(gv.x, v.x, m, hp, false);
           v.y = sgd_elem<false, kWd>(gv.y, v.y, m, hp, false);
@@ -632,7 +686,7 @@ __device__ __forceinline__ void store_bf16x4(__nv_bfloat16* sh, int64_t q, float
 #define DEAR_ZC_KU8 2
 #endif
 template <int PC, bool kMom, bool kWd, bool kShadow>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void DEAR_ZC_BOUNDS
     rs_update_zc_kernel(const Unit* __restrict__ units, const Slice* __restrict__ slices,
                         const HyperParams* __restrict__ hpp, int has_buf, float* mom_base,
                         PeerArgs pa, PeerArgs ga, BucketFlags* flags) {
@@ -906,7 +960,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 // Source element of a unit: U.a + off on rank U.peer, i.e. at sa.delta[U.peer]
 // (sa = arena deltas for bucket slots, parameter deltas for zero-copy).
 template <bool kShadow>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void DEAR_ZC_BOUNDS
     ag_unpack_peer_kernel(const Unit* __restrict__ units, const Slice* __restrict__ slices,
                           PeerArgs pa, PeerArgs sa, BucketFlags* flags, int n_slices) {
   cta_wait_peers(&flags->updated, &flags->updated, pa);  // every owner updated its shard
@@ -1159,7 +1213,7 @@ cudaError_t launch_update(const Unit* units, const Slice* slices, int64_t total,
                           const HyperParams* hp, int has_momentum_buf, int use_momentum,
                           int use_wd, int grid, cudaStream_t s) {
   if (total <= 0) return cudaSuccess;
-  const int ug = bucket_grid(kSlices, grid);
+  const int ug = bucket_grid(kUpdSlices, grid);
   if (use_momentum && use_wd)
     update_kernel<true, true><<<ug, kThreads, 0, s>>>(units, slices, hp, has_momentum_buf);
   else if (use_momentum)
@@ -1186,7 +1240,7 @@ cudaError_t launch_update_direct(const Unit* units, const Slice* slices, int64_t
                                  const HyperParams* hp, int use_wd, int with_shadow,
                                  cudaStream_t s) {
   if (total <= 0) return cudaSuccess;
-  const int grid = bucket_grid(kSlices);
+  const int grid = bucket_grid(kDirSlices);
   if (use_wd && with_shadow)
     update_direct_kernel<true, true><<<grid, kThreads, 0, s>>>(units, slices, hp);
   else if (use_wd)

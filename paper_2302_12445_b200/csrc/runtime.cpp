@@ -939,7 +939,7 @@ int dear_finalize(dear_ctx* ctx) {
     // Equal element slices per CTA for each op (one wave of kSlices CTAs).
     Slice* hs = host_slices.data() + g * per_bucket_slices;
     make_slices(host_units.data() + (B.pack_u - up), B.n_pack, B.e_pack, hs, kSlices, 0);
-    make_slices(host_units.data() + (B.upd_u - up), B.n_upd, B.e_upd, hs + kSlices, kSlices, 4);
+    make_slices(host_units.data() + (B.upd_u - up), B.n_upd, B.e_upd, hs + kSlices, kUpdSlices, 4);
     make_slices(host_units.data() + (B.unpack_u - up), B.n_unpack, B.e_unpack, hs + 2 * kSlices,
                 kSlices, 2);
     make_slices(host_units.data() + (B.upd_u - up), B.n_upd, B.e_upd, hs + 3 * kSlices,
@@ -950,7 +950,7 @@ int dear_finalize(dear_ctx* ctx) {
                 hs + 3 * kSlices + 2 * kPeerSlices, kPackPeerSlices, 0);
     if (c.direct)
       make_slices(host_units.data() + (B.dir_u - up), B.n_dir, B.e_dir,
-                  hs + 3 * kSlices + 2 * kPeerSlices + kPackPeerSlices, kSlices, 2);
+                  hs + 3 * kSlices + 2 * kPeerSlices + kPackPeerSlices, kDirSlices, 2);
     B.pack_s = sp + g * per_bucket_slices;
     B.upd_s = B.pack_s + kSlices;
     B.unpack_s = B.upd_s + kSlices;

@@ -36,7 +36,8 @@ class DistOptim:
     def __init__(self, optimizer: torch.optim.Optimizer, model: Optional[torch.nn.Module] = None,
                  *, comm=None, rank: int = 0, policy: str = "DEAR_FUSED",
                  fusion_buffer_bytes: int = 25_000_000, defer_allgather: bool = False,
-                 backend: str = "auto", stream: Optional[torch.cuda.Stream] = None):
+                 backend: str = "auto", stream: Optional[torch.cuda.Stream] = None,
+                 flatten: bool = True):
         if not isinstance(optimizer, torch.optim.SGD):
             raise TypeError("DistOptim supports torch.optim.SGD (the reference's update rule)")
         if len(optimizer.param_groups) != 1:
@@ -67,11 +68,31 @@ class DistOptim:
                                nesterov=bool(g.get("nesterov", False)),
                                defer_allgather=defer_allgather, backend=backend,
                                stream=stream)
+        for p in params:
+            if p.dtype != torch.float32 or not p.is_cuda or not p.is_contiguous():
+                raise ValueError("DistOptim needs contiguous fp32 CUDA parameters")
+        if flatten:
+            # One flat parameter buffer and one flat gradient buffer (64-element
+            # aligned views, layer order): the NVLink peer backend then maps
+            # them directly (zero-copy: no pack, no bucket buffer).
+            offs, n = [], 0
+            for p in params:
+                offs.append(n)
+                n += (p.numel() + 63) // 64 * 64
+            pflat = torch.zeros(max(n, 64), dtype=torch.float32, device=params[0].device)
+            gflat = torch.zeros_like(pflat)
+            for p, o in zip(params, offs):
+                view = pflat[o:o + p.numel()].view_as(p)
+                view.copy_(p.data)
+                p.data = view
+                g = gflat[o:o + p.numel()].view_as(p)
+                if p.grad is not None:
+                    g.copy_(p.grad)
+                p.grad = g
+            self._flat = (pflat, gflat)
         self._layer_of = {}
         self._grad_ptr = {}
         for layer, p in enumerate(params, start=1):
-            if p.dtype != torch.float32 or not p.is_cuda or not p.is_contiguous():
-                raise ValueError("DistOptim needs contiguous fp32 CUDA parameters")
             # Gradients live in fixed storage the runtime packs from; zero_grad
             # zeroes in place instead of dropping it.
             if p.grad is None:

@@ -221,8 +221,12 @@ def case_distoptim(rank, P):
     ok = opt.check_replicas()
     for p, q in zip(model.parameters(), ref.parameters()):
         ok &= close(p.detach().double().cpu().numpy(), q.detach().double().cpu().numpy(), 1e-5)
+    zc = opt.runtime.zero_copy
+    if opt.runtime.backend == "peer":
+        ok &= zc  # flat parameter / gradient buffers: the zero-copy path must engage
     if rank == 0:
-        print(f"[distoptim P={P}] match single-process SGD on averaged grads: {ok}", flush=True)
+        print(f"[distoptim P={P}] backend={opt.runtime.backend} zero_copy={zc} "
+              f"match single-process SGD on averaged grads: {ok}", flush=True)
     opt.close()
     comm.close()
     return ok

@@ -27,6 +27,8 @@ def main():
     ap.add_argument("--buffer", type=int, default=25_000_000)
     ap.add_argument("--backend", default="auto")
     ap.add_argument("--out", default="")
+    ap.add_argument("--clock-steps", type=int, default=0,
+                    help="also replay this many steps under the nvidia-smi clock sampler")
     a = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -95,8 +97,21 @@ def main():
     run()
     torch.cuda.synchronize()
     tl = rt.timeline(ev["base"])
+    clocks = None
+    if a.clock_steps:
+        import time as _t
+        with bench.ClockSampler(lr_) as clk:
+            t0 = _t.time()
+            for _ in range(a.clock_steps):
+                run()
+            torch.cuda.synchronize()
+            wall = _t.time() - t0
+        clocks = dict(clk.summary(), wall_ms_per_step=1e3 * wall / a.clock_steps)
+        pw = [float(r[2]) for r in clk.rows if len(r) >= 7 and r[2].replace(".", "").isdigit()]
+        clocks["power_w_median"] = sorted(pw)[len(pw) // 2] if pw else None
     marks = {k: ev["base"].elapsed_time(ev[k]) for k in ("ff", "bp", "end")}
     out = {"rank": rank, "policy": a.policy, "gd": a.group_dependency, "marks_ms": marks,
+           "clocks": clocks,
            "comm_order": rt.comm_order_info, "buckets": tl}
     # comm-stream busy time split by phase
     rs_spans = [(b["pack0"], b["update1"] if b["update1"] is not None else b["rs1"]) for b in tl
