@@ -4,10 +4,16 @@
 //   (mbarrier full/empty) -> tcgen05.mma kind::f16 (bf16 in, fp32 accumulate
 //   in TMEM, issued by one thread) -> tcgen05.ld epilogue -> global.
 //
-// Persistent: one CTA per SM walks a static round-robin list of output tiles
-// (128 x BN, BN <= 256 a multiple of 16 chosen per problem). TMEM holds two
-// 256-column accumulators, so the epilogue of tile i overlaps the mainloop of
-// tile i+1. A launch may carry up to two independent problems (the wgrad and
+// Persistent: two CTAs per SM (94 KB smem ring, one 256-column TMEM
+// accumulator each) walk a static round-robin list of output tiles (128 x BN,
+// BN <= 256 a multiple of 16 chosen per problem). With two resident CTAs the
+// epilogue of one overlaps the other's mainloop — and, across launches under
+// programmatic dependent launch, the next GEMM's CTA streams its operands
+// while the previous GEMM's CTA on the same SM drains its epilogue. (The
+// earlier one-CTA-per-SM form, 192 KB ring and two accumulators, is
+// DEAR_GEMM_RING_KB=192 DEAR_GEMM_ACCS=2 DEAR_GEMM_CTAS_PER_SM=1; the two-CTA
+// form cut the BERT-L compute-only step from 8.80 to 6.42 ms,
+// profiles/r01e_gemm_two_ctas.log.) A launch may carry up to two independent problems (the wgrad and
 // dgrad of one layer's backprop), sharing the persistent grid. Launches use
 // programmatic dependent launch: the next GEMM's CTAs run their prologue
 // (barrier init, TMEM alloc, descriptor prefetch) while this one drains, and
@@ -40,10 +46,23 @@ constexpr int kBNMax = 256;
 constexpr int kMaxStages = 8;
 constexpr int kAStage = kBM * kBK * 2;     // 16 KB
 constexpr int kBStage = kBNMax * kBK * 2;  // 32 KB (widest B stage)
-constexpr int kRingBytes = 4 * (kAStage + kBStage);  // 192 KB: 4..8 stages by BN
+// Ring size (and with it the CTAs an SM can hold): 94 KB + 17.5 KB of
+// barriers / epilogue staging fits two CTAs per SM (2-5 stages by BN).
+#ifndef DEAR_GEMM_RING_KB
+#define DEAR_GEMM_RING_KB 94
+#endif
+#ifndef DEAR_GEMM_ACCS
+#define DEAR_GEMM_ACCS 1
+#endif
+#ifndef DEAR_GEMM_CTAS_PER_SM
+#define DEAR_GEMM_CTAS_PER_SM 2
+#endif
+static_assert(DEAR_GEMM_ACCS * DEAR_GEMM_CTAS_PER_SM * 256 <= 512, "TMEM has 512 columns per SM");
+constexpr int kRingBytes = DEAR_GEMM_RING_KB * 1024;
 constexpr int kThreads = 192;
 constexpr int kAccCols = 256;
-constexpr int kTmemCols = 2 * kAccCols;
+constexpr int kNumAcc = DEAR_GEMM_ACCS;  // TMEM accumulators per CTA (1 or 2)
+constexpr int kTmemCols = kNumAcc * kAccCols;
 // Epilogue staging for TMA stores: per epilogue warp two 32x32 bf16 buffers.
 constexpr int kEpiBufBytes = 32 * 32 * 2;
 constexpr int kEpiBytes = 4 * 2 * kEpiBufBytes;  // 16 KB
@@ -588,7 +607,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       for (int t = cid; t < L.total_tiles; t += ncl, ++j) {
         const TileCoord tc = decode(L, t, ci, cj);
         const Problem& P = L.p[tc.prob];
-        const uint32_t acc = j & 1, aph = (j >> 1) & 1;
+        const uint32_t acc = j % kNumAcc, aph = (j / kNumAcc) & 1;
         long long w_tm = 0;
         WAIT_T(w_tm, &tmem_empty[acc], aph ^ 1);
         (void)w_tm;
@@ -645,7 +664,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     for (int t = cid; t < L.total_tiles; t += ncl, ++j) {
       const TileCoord tc = decode(L, t, ci, cj);
       const Problem& P = L.p[tc.prob];
-      const uint32_t acc = j & 1, aph = (j >> 1) & 1;
+      const uint32_t acc = j % kNumAcc, aph = (j / kNumAcc) & 1;
       mbar_wait(&tmem_full[acc], aph);
       tc_fence_after();
       const int64_t row = tc.m0 + 32 * q + lane;
@@ -954,7 +973,7 @@ void set_smem_attr() {
 
 int max_active_clusters(int csize, bool pair) {
   static int cache[2][17] = {{0}};
-  if (csize <= 1) return kSms;
+  if (csize <= 1) return kSms * DEAR_GEMM_CTAS_PER_SM;
   if (cache[pair][csize]) return cache[pair][csize];
   set_smem_attr();
   cudaLaunchConfig_t cfg = {};

@@ -666,7 +666,11 @@ __device__ __forceinline__ void store_bf16x4(__nv_bfloat16* sh, int64_t q, float
   uint2 packed;
   packed.x = *reinterpret_cast<uint32_t*>(&lo);
   packed.y = *reinterpret_cast<uint32_t*>(&hi);
+#ifdef DEAR_ZC_EVICT
+  __stcs(reinterpret_cast<uint2*>(sh) + q, packed);
+#else
   reinterpret_cast<uint2*>(sh)[q] = packed;
+#endif
 }
 
 // Units: a = gradient (local address; rank k's copy at a + ga.delta[k]),
@@ -684,6 +688,17 @@ __device__ __forceinline__ void store_bf16x4(__nv_bfloat16* sh, int64_t q, float
 #endif
 #ifndef DEAR_ZC_KU8
 #define DEAR_ZC_KU8 2
+#endif
+// DEAR_ZC_EVICT (experiment): evict-first hints on every zero-copy stream so
+// the comm traffic does not push the backprop GEMMs' operands out of L2.
+#ifdef DEAR_ZC_EVICT
+#define ZC_LDR(p) __ldcs(p)
+#define ZC_LDW(p) __ldcs(p)
+#define ZC_ST(p, v) __stcs(p, v)
+#else
+#define ZC_LDR(p) __ldcg(p)
+#define ZC_LDW(p) (*(p))
+#define ZC_ST(p, v) (*(p) = (v))
 #endif
 template <int PC, bool kMom, bool kWd, bool kShadow>
 __global__ void DEAR_ZC_BOUNDS
@@ -737,9 +752,9 @@ __global__ void DEAR_ZC_BOUNDS
 #pragma unroll
         for (int k = 0; k < KU; ++k) {
           const int64_t q = base + k * 32 + lane;
-          wv[k] = q < n4 ? w4[q] : zero;
+          wv[k] = q < n4 ? ZC_LDW(w4 + q) : zero;
 #pragma unroll
-          for (int j = 0; j < PC; ++j) v[k][j] = q < n4 ? __ldcg(pg[j] + q) : zero;
+          for (int j = 0; j < PC; ++j) v[k][j] = q < n4 ? ZC_LDR(pg[j] + q) : zero;
         }
 #pragma unroll
         for (int k = 0; k < KU; ++k) {
@@ -766,7 +781,7 @@ __global__ void DEAR_ZC_BOUNDS
           o.y = sgd_elem<kMom, kWd>(acc.y, wv[k].y, mv.y, hp, has_buf);
           o.z = sgd_elem<kMom, kWd>(acc.z, wv[k].z, mv.z, hp, has_buf);
           o.w = sgd_elem<kMom, kWd>(acc.w, wv[k].w, mv.w, hp, has_buf);
-          w4[q] = o;
+          ZC_ST(w4 + q, o);
           if (kMom) {
             if (mvec) {
               reinterpret_cast<float4*>(mh)[q] = mv;
@@ -976,15 +991,8 @@ __global__ void DEAR_ZC_BOUNDS
           if (kShadow && sh) sh[i] = __float2bfloat16_rn(v);
         },
         [&](int64_t head, int64_t q, float4 v) {
-          reinterpret_cast<float4*>(dst + head)[q] = v;
-          if (kShadow && sh) {
-            __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y);
-            __nv_bfloat162 hi = __floats2bfloat162_rn(v.z, v.w);
-            uint2 packed;
-            packed.x = *reinterpret_cast<uint32_t*>(&lo);
-            packed.y = *reinterpret_cast<uint32_t*>(&hi);
-            reinterpret_cast<uint2*>(sh + head)[q] = packed;
-          }
+          ZC_ST(reinterpret_cast<float4*>(dst + head) + q, v);
+          if (kShadow && sh) store_bf16x4(sh + head, q, v);
         });
   });
   signal_done(&flags->done[2], &flags->gathered);
