@@ -4,7 +4,7 @@
 //   (mbarrier full/empty) -> tcgen05.mma kind::f16 (bf16 in, fp32 accumulate
 //   in TMEM, issued by one thread) -> tcgen05.ld epilogue -> global.
 //
-// Persistent: two CTAs per SM (94 KB smem ring, one 256-column TMEM
+// Persistent: two CTAs per SM (102 KB smem ring, one 256-column TMEM
 // accumulator each) walk a static round-robin list of output tiles (128 x BN,
 // BN <= 256 a multiple of 16 chosen per problem). With two resident CTAs the
 // epilogue of one overlaps the other's mainloop — and, across launches under
@@ -46,10 +46,13 @@ constexpr int kBNMax = 256;
 constexpr int kMaxStages = 8;
 constexpr int kAStage = kBM * kBK * 2;     // 16 KB
 constexpr int kBStage = kBNMax * kBK * 2;  // 32 KB (widest B stage)
-// Ring size (and with it the CTAs an SM can hold): 94 KB + 17.5 KB of
-// barriers / epilogue staging fits two CTAs per SM (2-5 stages by BN).
+// Ring size (and with it the CTAs an SM can hold): 102 KB + 9.5 KB of
+// barriers / one epilogue staging buffer per warp fits two CTAs per SM
+// (2 stages at BN = 256, 3 at BN = 128, up to 4). Measured against 94 KB with
+// double-buffered staging (BN = 256 impossible there): ResNet-50 N = 1 16,621
+// -> 20,326 samples/s (profiles/r01e_gemm_ring_epi.log).
 #ifndef DEAR_GEMM_RING_KB
-#define DEAR_GEMM_RING_KB 94
+#define DEAR_GEMM_RING_KB 102
 #endif
 #ifndef DEAR_GEMM_ACCS
 #define DEAR_GEMM_ACCS 1
@@ -65,7 +68,11 @@ constexpr int kNumAcc = DEAR_GEMM_ACCS;  // TMEM accumulators per CTA (1 or 2)
 constexpr int kTmemCols = kNumAcc * kAccCols;
 // Epilogue staging for TMA stores: per epilogue warp two 32x32 bf16 buffers.
 constexpr int kEpiBufBytes = 32 * 32 * 2;
-constexpr int kEpiBytes = 4 * 2 * kEpiBufBytes;  // 16 KB
+#ifndef DEAR_GEMM_EPI_BUFS
+#define DEAR_GEMM_EPI_BUFS 1
+#endif
+constexpr int kEpiBufs = DEAR_GEMM_EPI_BUFS;  // staging buffers per epilogue warp
+constexpr int kEpiBytes = 4 * kEpiBufs * kEpiBufBytes;  // 8 KB with one
 constexpr int kEpiOffset = kRingBytes + 512;     // after the barriers, 512 B aligned
 constexpr int kSmemBytes = kEpiOffset + kEpiBytes + 1024;
 constexpr int kMaxProblems = 2;
@@ -675,16 +682,16 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         // (64 B per row, 64 B swizzle) and added into D by a TMA reduce; L2
         // performs the adds on full lines. Row r_full (partial under the flat
         // limit) is added by its lane directly.
-        uint8_t* epi = smem + kEpiOffset + q * 2 * kEpiBufBytes;
+        uint8_t* epi = smem + kEpiOffset + q * kEpiBufs * kEpiBufBytes;
         for (int c = 0; c < P.bn; c += 32) {
           uint32_t v[32];
           tmem_ld32(base + static_cast<uint32_t>(c), v);
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             if (c + 16 * h >= P.bn) break;
-            uint8_t* buf = epi + (epi_chunk & 1) * kEpiBufBytes;
+            uint8_t* buf = epi + (epi_chunk % kEpiBufs) * kEpiBufBytes;
             ++epi_chunk;
-            if (lane == 0) bulk_wait_read<1>();
+            if (lane == 0) bulk_wait_read<kEpiBufs - 1>();
             __syncwarp();
 #pragma unroll
             for (int jj = 0; jj < 4; ++jj) {
@@ -706,13 +713,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       } else if (P.d_tma) {
         // 32 rows x 32 columns per chunk: lane = row; bf16 row of 64 B in four
         // 16 B pieces, piece j stored at j ^ ((row >> 1) & 3) (TMA 64 B swizzle;
-        // conflict-free smem writes). Double-buffered per warp.
-        uint8_t* epi = smem + kEpiOffset + q * 2 * kEpiBufBytes;
+        // conflict-free smem writes). kEpiBufs staging buffers per warp.
+        uint8_t* epi = smem + kEpiOffset + q * kEpiBufs * kEpiBufBytes;
         for (int c = 0; c < P.bn; c += 32, ++epi_chunk) {
           uint32_t v[32];
           tmem_ld32(base + static_cast<uint32_t>(c), v);
-          uint8_t* buf = epi + (epi_chunk & 1) * kEpiBufBytes;
-          if (lane == 0) bulk_wait_read<1>();  // this buffer's previous store read it
+          uint8_t* buf = epi + (epi_chunk % kEpiBufs) * kEpiBufBytes;
+          if (lane == 0) bulk_wait_read<kEpiBufs - 1>();  // this buffer's previous store read it
           __syncwarp();
           const bool half = P.bn - c == 16;  // a tile's odd last 16 columns
           if (!half) {
