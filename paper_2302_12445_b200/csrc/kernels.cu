@@ -26,9 +26,14 @@ namespace {
 #define DEAR_KTHREADS 256
 #endif
 constexpr int kThreads = DEAR_KTHREADS;
-// Zero-copy / peer kernels: an optional register cap (experiments) so that one
-// comm CTA always fits next to a GEMM CTA but two never share an SM.
-#ifdef DEAR_ZC_MAXNREG
+// Zero-copy / peer kernels: a register cap so one comm CTA (256 threads x 96)
+// still fits on an SM next to the GEMM's two resident CTAs (2 x 6 warps x 88
+// registers); at P = 2 BERT-L this took the step from 8.64 to 8.40 ms
+// (profiles/r01e/tl4j_2_*.jsonl).
+#ifndef DEAR_ZC_MAXNREG
+#define DEAR_ZC_MAXNREG 96
+#endif
+#if DEAR_ZC_MAXNREG > 0
 #define DEAR_ZC_BOUNDS __maxnreg__(DEAR_ZC_MAXNREG)
 #else
 #define DEAR_ZC_BOUNDS __launch_bounds__(kThreads, 1)
@@ -681,13 +686,13 @@ __device__ __forceinline__ void store_bf16x4(__nv_bfloat16* sh, int64_t q, float
 // so after a scalar head every stream is float4-aligned.
 // Vectors per lane per round (each with P gradient loads in flight).
 #ifndef DEAR_ZC_KU2
-#define DEAR_ZC_KU2 8
+#define DEAR_ZC_KU2 4
 #endif
 #ifndef DEAR_ZC_KU4
-#define DEAR_ZC_KU4 4
+#define DEAR_ZC_KU4 2
 #endif
 #ifndef DEAR_ZC_KU8
-#define DEAR_ZC_KU8 2
+#define DEAR_ZC_KU8 1
 #endif
 // DEAR_ZC_EVICT (experiment): evict-first hints on every zero-copy stream so
 // the comm traffic does not push the backprop GEMMs' operands out of L2.

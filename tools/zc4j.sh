@@ -9,4 +9,6 @@ import json,sys; d=json.loads(sys.stdin.read()); c=d['comm_order'] or {}
 print(d['marks_ms'], c.get('stage_us_mean'), d['rs_busy_ms'], d['ag_busy_ms'])"
 }
 TLARGS="--policy DEAR_FUSED" tl dear X=1
-TLARGS="--policy DEAR_FUSED" tl dear_ev DEAR_LIB=libdear_ev.so
+TLARGS="--policy DEAR_FUSED" tl dear_r80 DEAR_LIB=libdear_r80.so
+TLARGS="--policy DEAR_FUSED" tl dear_r96 DEAR_LIB=libdear_r96.so
+TLARGS="--policy NONE" tl none X=1
