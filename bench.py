@@ -200,16 +200,34 @@ def reference_arm(a, wl, world: int, rank: int, emit: bool = True):
 class Step:
     """One DeAR iteration over the synthetic model through the public API."""
 
-    def __init__(self, model, rt, stream, x_host=None, out_host=None):
+    def __init__(self, model, rt, stream, x_host=None, out_host=None, prefetch=True):
+        import torch
+
         self.m, self.rt, self.s = model, rt, stream
         self.x_host, self.out_host = x_host, out_host
+        # e2e input pipeline (what a pinned-memory data loader does): every step
+        # copies one batch host -> device, the NEXT step's, on a copy stream
+        # overlapped with this step's compute; this step's batch (landed during
+        # the previous step) moves staging -> model input with a D2D copy.
+        self.prefetch = prefetch and x_host is not None
+        if self.prefetch:
+            self.x_stage = torch.empty_like(model.x)
+            self.x_stage.copy_(x_host)  # primes the first step (outside timing)
+            self.copy_stream = torch.cuda.Stream()
 
     def __call__(self):
         import torch
 
         m, rt, s = self.m, self.rt, self.s
         with torch.cuda.stream(s):
-            m.set_input(self.x_host)
+            if self.prefetch:
+                m.x.copy_(self.x_stage)
+                m.set_input(None)
+                self.copy_stream.wait_stream(s)  # staging buffer consumed
+                with torch.cuda.stream(self.copy_stream):
+                    self.x_stage.copy_(self.x_host, non_blocking=True)
+            else:
+                m.set_input(self.x_host)
             for l in range(1, m.L + 1):
                 if rt is not None:
                     rt.param_wait(l, s)
@@ -222,6 +240,8 @@ class Step:
             if rt is not None:
                 rt.step(s)
                 rt.join(s)
+            if self.prefetch:
+                s.wait_stream(self.copy_stream)  # next batch landed (joins the graph)
             if self.out_host is not None:
                 self.out_host.copy_(m.result_scalar(), non_blocking=True)
 
@@ -395,6 +415,9 @@ def gpu_arm(a, wl, world, rank, local_rank):
     rt = runtime(a.policy)
     backend_used = rt.backend
     zero_copy = bool(getattr(rt, "zero_copy", False))
+    nb = len(rt.buckets())
+    bucket_launches = (nb if world == 1 and a.momentum == 0 else
+                       2 * nb + 1 if zero_copy else 3 * nb)
     rt_order_info = rt.comm_order_info
     buckets = rt.buckets()
     run = make_runner(Step(model, rt, stream), use_graph, stream)
@@ -423,7 +446,7 @@ def gpu_arm(a, wl, world, rank, local_rank):
     rt.synchronize()
     run_e2e = make_runner(Step(model, rt, stream, x_host, out_host), use_graph, stream)
     res["e2e_ms"] = time_loop(run_e2e, a.steps, a.warmup, stream, dist_on)
-    h2d = x_host.numel() * x_host.element_size()
+    h2d = x_host.numel() * x_host.element_size()  # one batch per step (prefetched, Step)
     d2h = out_host.element_size()
 
     # --- per-stage timings (one instrumented eager step) ---------------------
@@ -508,13 +531,18 @@ def gpu_arm(a, wl, world, rank, local_rank):
                    "hidden": wl["hidden"], "params": D, "cuda_graph": use_graph,
                    "l2": "working set (params+grads+buckets) > 126 MB L2; no flush"},
         "e2e": {"value": e2e, "unit": "samples/s", "h2d_bytes_per_step": h2d,
+                "input_pipeline": "each step: D2D of its batch from staging, H2D of the next "
+                                  "batch (pinned) on a copy stream overlapped with compute, "
+                                  "D2H of the loss scalar",
                 "d2h_bytes_per_step": d2h},
         "clocks": clocks,
         # our kernels per step: FF + grouped BP GEMMs (two launches when the
-        # tuned wgrad / dgrad tiles differ in pair mode) and the bucket kernels
-        # (pack/update/unpack; peer: pack + fused RS-update + fused AG-unpack, waits in-kernel)
-        "gpu_launches": a.steps * (model.gemm_launches_per_step() +
-                                   3 * len(buckets)),
+        # tuned wgrad / dgrad tiles differ in pair mode) and the bucket kernels:
+        # P = 1 one direct update per bucket; zero-copy peer RS-update + AG per
+        # bucket + the one-warp "gradients consumed" wait at dear_step; slot
+        # peer pack + RS-update + AG-unpack; NCCL pack + update + unpack (the
+        # NCCL collectives themselves are not counted)
+        "gpu_launches": a.steps * (model.gemm_launches_per_step() + bucket_launches),
         "roofline": {"bound": "tensor", "kernel": "tcgen05 GEMM chain (FF + grouped wgrad/dgrad)",
                      "achieved": gemm_achieved, "peak": tf_sus, "unit": "TFLOP/s",
                      "frac": gemm_achieved / tf_sus, "traffic": _ncu_traffic(a.workload),
