@@ -1126,16 +1126,7 @@ cudaError_t launch_ag_unpack_peer(const Unit* units, const Slice* slices, int64_
                                   int with_shadow, const PeerArgs& pa, const PeerArgs& sa,
                                   BucketFlags* flags, int n_slices, cudaStream_t s) {
   (void)total;
-  size_t smem = 0;
-#ifdef DEAR_ZC_SMEM_RESERVE
-  if (n_slices == kZcSlices) {
-    smem = DEAR_ZC_SMEM_RESERVE;
-    cudaFuncSetAttribute(ag_unpack_peer_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-    cudaFuncSetAttribute(ag_unpack_peer_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-  }
-#endif
+  const size_t smem = 0;
   if (with_shadow)
     ag_unpack_peer_kernel<true><<<bucket_grid(n_slices), kThreads, smem, s>>>(units, slices, pa, sa, flags, n_slices);
   else
@@ -1148,17 +1139,7 @@ void launch_rs_zc_p(const Unit* units, const Slice* slices, const HyperParams* h
                     float* mom_base, int with_shadow, const PeerArgs& pa, const PeerArgs& ga,
                     BucketFlags* flags, cudaStream_t s) {
   const int grid = bucket_grid(kZcSlices);
-  // DEAR_ZC_SMEM_RESERVE (experiment builds): unused dynamic shared memory that
-  // keeps the zero-copy CTAs off SMs holding a GEMM CTA (soft SM partition,
-  // with DEAR_GEMM_MAX_CTAS leaving SMs free).
-  size_t smem = 0;
-#ifdef DEAR_ZC_SMEM_RESERVE
-  smem = DEAR_ZC_SMEM_RESERVE;
-  cudaFuncSetAttribute(rs_update_zc_kernel<PC, kMom, kWd, true>,
-                       cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  cudaFuncSetAttribute(rs_update_zc_kernel<PC, kMom, kWd, false>,
-                       cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-#endif
+  const size_t smem = 0;
   // Bulk-TMA staging for P in {2, 4, 8} with DEAR_ZC_TMA=1. Off by default:
   // same isolated time as the register kernel at P = 4 (53 us per 25 MB
   // bucket, so the per-SM LSU limit was not the bound), and its 160-192 KB

@@ -424,9 +424,6 @@ void dear_ctx::exec(const Op& op) {
       break;
     case OP_RS:
       if (zc) {
-#ifdef DEAR_EXP_SKIP_ALL
-        break;  // attribution experiment only (variant build): no reduce-scatter
-#endif
         cuda_check(launch_rs_update_zc(B->zrs_u, B->zrs_ps, hp_dev, B->mom_init ? 1 : 0, B->mom,
                                        cfg.momentum != 0.0, cfg.weight_decay != 0.0,
                                        B->any_shadow ? 1 : 0, pa, ga, B->flags, comm_stream),
@@ -468,9 +465,6 @@ void dear_ctx::exec(const Op& op) {
     case OP_AG:
       if (!local) record_t(op.bucket, T_AG0);
       if (zc) {
-#if defined(DEAR_EXP_SKIP_AG) || defined(DEAR_EXP_SKIP_ALL)
-        break;  // attribution experiment only (variant build): no all-gather
-#endif
         // Each owner's updated parameters, read over NVLink into ours.
         cuda_check(launch_ag_unpack_peer(B->zag_u, B->zag_ps, B->e_zag, B->any_shadow ? 1 : 0,
                                          pa, qa, B->flags, kZcSlices, comm_stream),
