@@ -42,7 +42,10 @@ namespace gemm {
 
 constexpr int kBM = 128;
 constexpr int kBK = 64;  // one 128-byte swizzle atom of bf16 along K
-constexpr int kBNMax = 256;
+#ifndef DEAR_GEMM_BN_MAX
+#define DEAR_GEMM_BN_MAX 256
+#endif
+constexpr int kBNMax = DEAR_GEMM_BN_MAX;  // widest tile = TMEM accumulator columns
 constexpr int kMaxStages = 8;
 constexpr int kAStage = kBM * kBK * 2;     // 16 KB
 constexpr int kBStage = kBNMax * kBK * 2;  // 32 KB (widest B stage)
@@ -60,10 +63,11 @@ constexpr int kBStage = kBNMax * kBK * 2;  // 32 KB (widest B stage)
 #ifndef DEAR_GEMM_CTAS_PER_SM
 #define DEAR_GEMM_CTAS_PER_SM 2
 #endif
-static_assert(DEAR_GEMM_ACCS * DEAR_GEMM_CTAS_PER_SM * 256 <= 512, "TMEM has 512 columns per SM");
+static_assert(DEAR_GEMM_ACCS * DEAR_GEMM_CTAS_PER_SM * DEAR_GEMM_BN_MAX <= 512,
+              "TMEM has 512 columns per SM");
 constexpr int kRingBytes = DEAR_GEMM_RING_KB * 1024;
 constexpr int kThreads = 192;
-constexpr int kAccCols = 256;
+constexpr int kAccCols = kBNMax;
 constexpr int kNumAcc = DEAR_GEMM_ACCS;  // TMEM accumulators per CTA (1 or 2)
 constexpr int kTmemCols = kNumAcc * kAccCols;
 // Epilogue staging for TMA stores: per epilogue warp two 32x32 bf16 buffers.

@@ -7,6 +7,7 @@ fallback: the plan calls the native kernel or raises.
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import torch
 
@@ -148,11 +149,14 @@ class GemmPlan:
 # outside any timed region.
 
 def tile_candidates(M: int, N: int, mn_major: bool) -> list[tuple[int, int]]:
+    # DEAR_GEMM_MAX_BN: for library builds with narrower TMEM accumulators
+    # (DEAR_GEMM_BN_MAX, e.g. three CTAs per SM at BN <= 128).
+    max_bn = int(os.environ.get("DEAR_GEMM_MAX_BN", "256"))
     out = []
     for pair in (0, 1):
         if pair and M <= 128:
             continue
-        for bn in range(64, 257, 16):
+        for bn in range(64, max_bn + 1, 16):
             if pair and mn_major and bn not in (128, 256):
                 continue
             nt = -(-N // bn)

@@ -26,6 +26,7 @@ G_l is the true weight gradient of Y_l = X W_l^T for upstream dY.
 from __future__ import annotations
 
 import math
+import os
 
 import torch
 
@@ -163,7 +164,9 @@ class SyntheticModel:
 
         # stage 1: weight-gradient tile x split-K x reduction path (TMA reduce
         # or red.add), dgrad at its best chain tile
-        wtiles = list(dict.fromkeys([c[1:] for c in wg[:2]] + [(128, 0), (176, 0), (256, 0)]))
+        max_bn = int(os.environ.get("DEAR_GEMM_MAX_BN", "256"))  # see gemm.tile_candidates
+        wtiles = list(dict.fromkeys([c[1:] for c in wg[:2]] +
+                                    [t for t in ((128, 0), (176, 0), (256, 0)) if t[0] <= max_bn]))
         trials = []
         for wc in wtiles:
             for sp in splits:
