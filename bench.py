@@ -661,7 +661,8 @@ def _isolated_stage_times(model, runtime, stream, policy, reps=20):
     return out
 
 
-def _policy_pair(a, model, comm, world, rank, stream, batch, steps, warm, backend=None):
+def _policy_pair(a, model, comm, world, rank, stream, batch, steps, warm, backend=None,
+                 buffer=None):
     """DeAR vs WFBP on `model` (same kernels, same fusion buffer), graph-replayed
     steps, max over ranks. Also the measured per-step comm-stream times of the
     DeAR runtime's comm-only iterations (t_rs = pack + RS + update side,
@@ -671,6 +672,8 @@ def _policy_pair(a, model, comm, world, rank, stream, batch, steps, warm, backen
     ab = argparse.Namespace(**vars(a))
     if backend is not None:
         ab.backend = backend
+    if buffer is not None:
+        ab.buffer = buffer
     res = {}
     for policy in (a.policy, a.baseline_policy):
         rt = make_runtime(ab, model, comm, rank, world, stream, policy, True)
@@ -743,6 +746,18 @@ def compare_policies(a, wl_name, comm, world, rank, stream):
                 out.update(res)
             else:
                 out["nccl"] = res
+        if with_nccl and world > 1:
+            # BASELINE configs 3/4 "fusion buffer sweep": the same comparison
+            # with 10 MB buckets on the default transport, where per-bucket
+            # costs make the step comm-bound and DeAR's reordering can matter.
+            sw = {}
+            for buf in (10_000_000,):
+                r = _policy_pair(a, model, comm, world, rank, stream, batch, steps, warm,
+                                 buffer=buf)
+                d, w = r[a.policy]["ms_per_step"], r[a.baseline_policy]["ms_per_step"]
+                sw[str(buf)] = {"DEAR_ms": d, "WFBP_ms": w, "dear_over_wfbp": w / d,
+                                "exposed_comm_pct": max(0.0, 100 * (d - comp) / d)}
+            out["buffer_sweep"] = sw
         model.close()
         del model
         torch.cuda.empty_cache()

@@ -83,6 +83,7 @@ class SyntheticModel:
         self.ff_transposed = False
         self.dx = torch.empty(T, H, dtype=torch.bfloat16, device=dev)
         self.wgrad_split = int(wgrad_split)
+        self.bp_split = os.environ.get("DEAR_BP_SPLIT", "0") == "1"
         self._build_plans()
         self.tiles = self.tune_tiles() if tune else None
 
@@ -153,7 +154,7 @@ class SyntheticModel:
             if i == 0:
                 self.zero_grad()
             l = L - 1 - (i % L)
-            GemmPlan.run_group([self.wgrad[l], self.dgrad[l]], s)
+            self._run_bp(l, s)
 
         def set_bp(wc, sp, red, dc):
             for l in range(L):
@@ -194,7 +195,7 @@ class SyntheticModel:
                                "bp_real_chain": len(trials)}}
 
     def gemm_launches_per_step(self) -> int:
-        bp = sum(1 if w.info()["pair"] == d.info()["pair"] else 2
+        bp = sum(2 if self.bp_split or w.info()["pair"] != d.info()["pair"] else 1
                  for w, d in zip(self.wgrad, self.dgrad))
         return self.L + bp
 
@@ -217,7 +218,14 @@ class SyntheticModel:
 
     def backward_layer(self, l: int, stream=None) -> None:
         # wgrad and dgrad are independent: one persistent launch computes both.
-        GemmPlan.run_group([self.wgrad[l - 1], self.dgrad[l - 1]], stream)
+        self._run_bp(l - 1, stream)
+
+    def _run_bp(self, i: int, stream) -> None:
+        if self.bp_split:  # two chained launches (DEAR_BP_SPLIT=1, A/B experiments)
+            self.wgrad[i].run(stream)
+            self.dgrad[i].run(stream)
+        else:
+            GemmPlan.run_group([self.wgrad[i], self.dgrad[i]], stream)
 
     def zero_grad(self) -> None:
         self.grads_flat.zero_()

@@ -15,4 +15,4 @@ timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node=2 --mas
 grep '"metric"' gpurun_out/${TAG}_bench_n2.log | python -c "
 import json,sys; d=json.loads(sys.stdin.read()); ns=d['north_star']
 print(d['value'], d['ms_per_step'], d['e2e']['value'], d['exposed_comm_pct'], d['config']['zero_copy'])
-print({k: ns.get(k) for k in ('DEAR_FUSED','WFBP_FUSED','dear_over_wfbp','exposed_comm_pct','compute_only_ms')}, (ns.get('calibrated_batch') or {}).get('dear_over_wfbp'), (ns.get('nccl') or {}).get('dear_over_wfbp'))"
+print({k: ns.get(k) for k in ('DEAR_FUSED','WFBP_FUSED','dear_over_wfbp','exposed_comm_pct','compute_only_ms','buffer_sweep')}, (ns.get('calibrated_batch') or {}).get('dear_over_wfbp'), (ns.get('nccl') or {}).get('dear_over_wfbp'))"
