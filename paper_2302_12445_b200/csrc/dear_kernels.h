@@ -47,6 +47,15 @@ constexpr int kSlices = 148 * DEAR_SLICES_PER_SM;
 #ifndef DEAR_DIR_CTAS_PER_SM
 #define DEAR_DIR_CTAS_PER_SM 2
 #endif
+#ifndef DEAR_PACK_CTAS_PER_SM
+#define DEAR_PACK_CTAS_PER_SM 4
+#endif
+#ifndef DEAR_UNPACK_CTAS_PER_SM
+#define DEAR_UNPACK_CTAS_PER_SM 4
+#endif
+constexpr int kPackSlices = 148 * DEAR_PACK_CTAS_PER_SM;
+constexpr int kUnpackSlices = 148 * DEAR_UNPACK_CTAS_PER_SM;
+static_assert(kPackSlices <= kSlices && kUnpackSlices <= kSlices, "slice regions are kSlices long");
 constexpr int kUpdSlices = 148 * DEAR_UPD_CTAS_PER_SM;
 constexpr int kDirSlices = 148 * DEAR_DIR_CTAS_PER_SM;
 static_assert(kUpdSlices <= kSlices && kDirSlices <= kSlices, "slice regions are kSlices long");

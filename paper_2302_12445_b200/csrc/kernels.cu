@@ -321,7 +321,13 @@ constexpr bool kPeerPackLight = false;  // experiment: peer pack on the full gri
 constexpr bool kPeerPackLight = true;
 #endif
 template <bool kSignal>
-__global__ void __launch_bounds__(kThreads, (kSignal && kPeerPackLight) ? 1 : kCtasPerSm) pack_kernel(const Unit* __restrict__ units,
+#ifndef DEAR_PACK_UNROLL
+#define DEAR_PACK_UNROLL kUnroll
+#endif
+#ifndef DEAR_UNPACK_UNROLL
+#define DEAR_UNPACK_UNROLL kUnroll
+#endif
+__global__ void __launch_bounds__(kThreads, (kSignal && kPeerPackLight) ? 1 : DEAR_PACK_CTAS_PER_SM) pack_kernel(const Unit* __restrict__ units,
                                                            const Slice* __restrict__ slices,
                                                            float scale, BucketFlags* flags,
                                                            PeerArgs pa, int n_slices) {
@@ -330,7 +336,7 @@ __global__ void __launch_bounds__(kThreads, (kSignal && kPeerPackLight) ? 1 : kC
   walk_slice(units, slices, n_slices, [&](const Unit& U, int64_t off, int64_t n) {
     const float* src = U.a + off;
     float* dst = U.b + off;
-    run_unit<Hint::kStream, (kSignal && kPeerPackLight) ? kPackPeerUnroll : kUnroll>(
+    run_unit<Hint::kStream, (kSignal && kPeerPackLight) ? kPackPeerUnroll : DEAR_PACK_UNROLL>(
         src, dst, n, [&](int64_t i) { dst[i] = __fmul_rn(src[i], scale); },
         [&](int64_t head, int64_t q, float4 v) {
           v.x = __fmul_rn(v.x, scale);
@@ -436,13 +442,13 @@ __global__ void __launch_bounds__(kThreads, DEAR_DIR_CTAS_PER_SM) update_direct_
 
 // -------------------------------------------------------------- unpack ----
 template <bool kShadow>
-__global__ void __launch_bounds__(kThreads, kCtasPerSm) unpack_kernel(const Unit* __restrict__ units,
+__global__ void __launch_bounds__(kThreads, DEAR_UNPACK_CTAS_PER_SM) unpack_kernel(const Unit* __restrict__ units,
                                                              const Slice* __restrict__ slices) {
-  walk_slice(units, slices, kSlices, [&](const Unit& U, int64_t off, int64_t n) {
+  walk_slice(units, slices, kUnpackSlices, [&](const Unit& U, int64_t off, int64_t n) {
     const float* src = U.a + off;
     float* dst = U.b + off;
     __nv_bfloat16* sh = (kShadow && U.c) ? static_cast<__nv_bfloat16*>(U.c) + off : nullptr;
-    run_unit<Hint::kStream>(
+    run_unit<Hint::kStream, DEAR_UNPACK_UNROLL>(
         src, dst, n,
         [&](int64_t i) {
           const float v = src[i];
@@ -1070,8 +1076,8 @@ int bucket_grid(int n_slices, int want = 0) {
 cudaError_t launch_pack(const Unit* units, const Slice* slices, int64_t total, float scale,
                         int grid, cudaStream_t s) {
   if (total <= 0) return cudaSuccess;
-  pack_kernel<false><<<bucket_grid(kSlices, grid), kThreads, 0, s>>>(units, slices, scale, nullptr,
-                                                                     PeerArgs{}, kSlices);
+  pack_kernel<false><<<bucket_grid(kPackSlices, grid), kThreads, 0, s>>>(units, slices, scale, nullptr,
+                                                                         PeerArgs{}, kPackSlices);
   return cudaGetLastError();
 }
 
@@ -1222,7 +1228,7 @@ cudaError_t launch_update(const Unit* units, const Slice* slices, int64_t total,
 cudaError_t launch_unpack(const Unit* units, const Slice* slices, int64_t total, int with_shadow,
                           int grid, cudaStream_t s) {
   if (total <= 0) return cudaSuccess;
-  const int ug = bucket_grid(kSlices, grid);
+  const int ug = bucket_grid(kUnpackSlices, grid);
   if (with_shadow)
     unpack_kernel<true><<<ug, kThreads, 0, s>>>(units, slices);
   else

@@ -932,10 +932,10 @@ int dear_finalize(dear_ctx* ctx) {
     }
     // Equal element slices per CTA for each op (one wave of kSlices CTAs).
     Slice* hs = host_slices.data() + g * per_bucket_slices;
-    make_slices(host_units.data() + (B.pack_u - up), B.n_pack, B.e_pack, hs, kSlices, 0);
+    make_slices(host_units.data() + (B.pack_u - up), B.n_pack, B.e_pack, hs, kPackSlices, 0);
     make_slices(host_units.data() + (B.upd_u - up), B.n_upd, B.e_upd, hs + kSlices, kUpdSlices, 4);
     make_slices(host_units.data() + (B.unpack_u - up), B.n_unpack, B.e_unpack, hs + 2 * kSlices,
-                kSlices, 2);
+                kUnpackSlices, 2);
     make_slices(host_units.data() + (B.upd_u - up), B.n_upd, B.e_upd, hs + 3 * kSlices,
                 kPeerSlices, 4);
     make_slices(host_units.data() + (B.unpack_u - up), B.n_unpack, B.e_unpack,
