@@ -667,7 +667,11 @@ static int create_common(dear_ctx* c, int32_t rank, int32_t P, void* compute_str
   cuda_check(cudaGetDevice(&c->device), "cudaGetDevice");
   int lo = 0, hi = 0;
   cuda_check(cudaDeviceGetStreamPriorityRange(&lo, &hi), "cudaDeviceGetStreamPriorityRange");
-  cuda_check(cudaStreamCreateWithPriority(&c->comm_stream, cudaStreamNonBlocking, hi),
+  // DEAR_COMM_PRIORITY=low|high (default high): block-scheduling priority of
+  // the comm stream's kernels against the compute stream's GEMMs.
+  const char* pe = std::getenv("DEAR_COMM_PRIORITY");
+  const int prio = (pe && pe[0] == 'l') ? lo : hi;
+  cuda_check(cudaStreamCreateWithPriority(&c->comm_stream, cudaStreamNonBlocking, prio),
              "cudaStreamCreateWithPriority");
   return DEAR_OK;
 }

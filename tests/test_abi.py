@@ -58,6 +58,11 @@ def test_invalid_arguments_without_gpu():
     cfg = _lib.DearCfg(3, 0, 0, 0.1, 0, 0, 0, 0, 0)
     assert L.dear_create(None, 0, 2, None, C.byref(cfg), C.byref(ctx)) == _lib.DEAR_EINVAL
     assert "NCCL communicator is required" in L.dear_last_error().decode()
+    # zero-copy query and the bench hook validate their context first
+    on = C.c_int32(7)
+    assert L.dear_peer_zero_copy(None, C.byref(on)) == _lib.DEAR_EINVAL
+    assert L.dear_bench_stage(None, 0, 1, None) == _lib.DEAR_EINVAL
+    assert L.dear_peer_connect(None, None, 0) == _lib.DEAR_EINVAL
 
 
 def test_runtime_rejects_unknown_policy():
