@@ -109,6 +109,7 @@ struct Bucket {
   int n_zrs = 0, n_zag = 0;
   int64_t e_zrs = 0, e_zag = 0;
   Slice *zrs_ps = nullptr, *zag_ps = nullptr;
+  std::vector<Unit> zag_host;  // host copy of the AG units (copy-engine all-gather)
   Unit* dir_u = nullptr;                           // P = 1 direct update (grad -> param)
   int n_dir = 0;
   int64_t e_dir = 0;
@@ -178,6 +179,14 @@ struct dear_ctx {
   bool zc = false;
   bool zc_tables = false;  // finalize built the zero-copy unit tables
   PeerArgs ga{}, qa{};
+  // DEAR_CE_AG=1 (zero-copy only): the all-gather's NVLink reads run on the
+  // copy engines (one cudaMemcpyAsync per AG unit from the owner's mapped
+  // parameters) and a local in-place pass writes the bf16 copies, so the
+  // SMs the forward GEMMs use are not held waiting on NVLink loads.
+  bool ce_ag = false;
+  static constexpr int kCeStreams = 4;  // copies spread over several copy engines
+  cudaStream_t ce_stream[kCeStreams] = {};
+  cudaEvent_t ce_fork = nullptr, ce_join[kCeStreams] = {};
   std::vector<void*> peer_maps;  // cudaIpcOpenMemHandle mappings to close
   bool timing = false;
   std::vector<std::string> trace;
@@ -355,6 +364,11 @@ dear_ctx::~dear_ctx() {
   for (void* m : peer_maps) cudaIpcCloseMemHandle(m);
   if (arena) cudaFree(arena);
   if (comm_stream) cudaStreamDestroy(comm_stream);
+  for (int k = 0; k < kCeStreams; ++k) {
+    if (ce_stream[k]) cudaStreamDestroy(ce_stream[k]);
+    if (ce_join[k]) cudaEventDestroy(ce_join[k]);
+  }
+  if (ce_fork) cudaEventDestroy(ce_fork);
   if (group) {
     for (auto& r : group->ranks)
       if (r == this) r = nullptr;
@@ -464,7 +478,45 @@ void dear_ctx::exec(const Op& op) {
       break;
     case OP_AG:
       if (!local) record_t(op.bucket, T_AG0);
-      if (zc) {
+      if (zc && ce_ag) {
+        // Copy engines: wait for every owner's update of this bucket, pull
+        // each owner's chunk pieces, then write the bf16 copies locally
+        // (the AG kernel with zero source deltas: in-place read + cast).
+        cuda_check(launch_wait_peers(&B->flags->updated, &B->flags->updated, pa, comm_stream),
+                   "wait kernel");
+        cuda_check(cudaEventRecord(ce_fork, comm_stream), "cudaEventRecord");
+        for (int k = 0; k < kCeStreams; ++k)
+          cuda_check(cudaStreamWaitEvent(ce_stream[k], ce_fork, 0), "cudaStreamWaitEvent");
+        {
+          // Equal element shares per copy stream, units split at share edges.
+          const int64_t share = (B->e_zag + kCeStreams - 1) / kCeStreams;
+          int64_t pos = 0;
+          for (const Unit& U : B->zag_host) {
+            int64_t o = 0;
+            while (o < U.len) {
+              const int k = static_cast<int>(pos / share);
+              const int64_t n = std::min(U.len - o, (k + 1) * share - pos);
+              const void* src = reinterpret_cast<const char*>(U.a + o) + qa.delta[U.peer];
+              cuda_check(cudaMemcpyAsync(U.b + o, src, static_cast<size_t>(n) * sizeof(float),
+                                         cudaMemcpyDefault, ce_stream[k]),
+                         "cudaMemcpyAsync(ce ag)");
+              o += n;
+              pos += n;
+            }
+          }
+        }
+        for (int k = 0; k < kCeStreams; ++k) {
+          cuda_check(cudaEventRecord(ce_join[k], ce_stream[k]), "cudaEventRecord");
+          cuda_check(cudaStreamWaitEvent(comm_stream, ce_join[k], 0), "cudaStreamWaitEvent");
+        }
+        if (B->any_shadow) {
+          PeerArgs za = qa;
+          for (int k = 0; k < kMaxPeers; ++k) za.delta[k] = 0;
+          cuda_check(launch_ag_unpack_peer(B->zag_u, B->zag_ps, B->e_zag, 1, pa, za, B->flags,
+                                           kZcSlices, comm_stream),
+                     "bf16 copy kernel");
+        }
+      } else if (zc) {
         // Each owner's updated parameters, read over NVLink into ours.
         cuda_check(launch_ag_unpack_peer(B->zag_u, B->zag_ps, B->e_zag, B->any_shadow ? 1 : 0,
                                          pa, qa, B->flags, kZcSlices, comm_stream),
@@ -802,6 +854,8 @@ int dear_finalize(dear_ctx* ctx) {
   c.direct = c.P == 1 && !c.peer && c.cfg.momentum == 0.0 && !(dir_env && dir_env[0] == '0');
   // Zero-copy tables for a later dear_peer_connect (multi-process only).
   c.zc_tables = !c.local && c.P > 1;
+  const char* ce_env = std::getenv("DEAR_CE_AG");
+  c.ce_ag = ce_env && ce_env[0] == '1';
   // Unit tables.
   std::vector<Unit> host_units;
   struct Span { size_t pack, upd, unpack; };
@@ -933,6 +987,7 @@ int dear_finalize(dear_ctx* ctx) {
       }
       B.n_zag = static_cast<int>(host_units.size() - static_cast<size_t>(B.zag_u - up));
       B.e_zag = set_starts(host_units, static_cast<size_t>(B.zag_u - up));
+      B.zag_host.assign(host_units.begin() + (B.zag_u - up), host_units.end());
     }
     // Equal element slices per CTA for each op (one wave of kSlices CTAs).
     Slice* hs = host_slices.data() + g * per_bucket_slices;
@@ -1389,6 +1444,14 @@ int dear_peer_connect(dear_ctx* ctx, const uint8_t* handles, int32_t n) {
     c.hp_host.prescaled = 0;
     cuda_check(cudaMemcpy(c.hp_dev, &c.hp_host, sizeof(HyperParams), cudaMemcpyHostToDevice),
                "cudaMemcpy(hp)");
+    if (c.ce_ag) {
+      c.ce_fork = new_event(false);
+      for (int k = 0; k < dear_ctx::kCeStreams; ++k) {
+        cuda_check(cudaStreamCreateWithFlags(&c.ce_stream[k], cudaStreamNonBlocking),
+                   "cudaStreamCreateWithFlags");
+        c.ce_join[k] = new_event(false);
+      }
+    }
   }
   DEAR_API_END
 }
