@@ -47,7 +47,6 @@ constexpr int kUnroll = DEAR_HBM_UNROLL;
 #define DEAR_PEER_UNROLL 8
 #endif
 constexpr int kPeerUnroll = DEAR_PEER_UNROLL;
-constexpr int kCtasPerSm = kSlices / 148;
 constexpr int kSms = 148;
 
 __device__ __forceinline__ float4 shfl_down4(float4 v) {
