@@ -110,6 +110,12 @@ struct Bucket {
   int64_t e_zrs = 0, e_zag = 0;
   Slice *zrs_ps = nullptr, *zag_ps = nullptr;
   std::vector<Unit> zag_host;  // host copy of the AG units (copy-engine all-gather)
+  // DEAR_CE_AG split: AG units [0, n_zcc) go to the copy engines (zcc_u: the
+  // same units for the bf16 pass), [n_zcc, n_zag) to the AG kernel (zsm_u).
+  Unit *zcc_u = nullptr, *zsm_u = nullptr;
+  int n_zcc = 0, n_zsm = 0;
+  int64_t e_zcc = 0, e_zsm = 0;
+  Slice *zcc_ps = nullptr, *zsm_ps = nullptr;
   Unit* dir_u = nullptr;                           // P = 1 direct update (grad -> param)
   int n_dir = 0;
   int64_t e_dir = 0;
@@ -184,7 +190,8 @@ struct dear_ctx {
   // parameters) and a local in-place pass writes the bf16 copies, so the
   // SMs the forward GEMMs use are not held waiting on NVLink loads.
   bool ce_ag = false;
-  static constexpr int kCeStreams = 4;  // copies spread over several copy engines
+  double ce_frac = 0.0;  // DEAR_CE_AG=<fraction of AG elements on the copy engines>
+  static constexpr int kCeStreams = 1;
   cudaStream_t ce_stream[kCeStreams] = {};
   cudaEvent_t ce_fork = nullptr, ce_join[kCeStreams] = {};
   std::vector<void*> peer_maps;  // cudaIpcOpenMemHandle mappings to close
@@ -479,40 +486,31 @@ void dear_ctx::exec(const Op& op) {
     case OP_AG:
       if (!local) record_t(op.bucket, T_AG0);
       if (zc && ce_ag) {
-        // Copy engines: wait for every owner's update of this bucket, pull
-        // each owner's chunk pieces, then write the bf16 copies locally
-        // (the AG kernel with zero source deltas: in-place read + cast).
+        // Split all-gather: the first `ce_frac` of the bucket's AG units are
+        // pulled by the copy engines on a side stream while the AG kernel
+        // pulls the rest; then a local in-place pass (the AG kernel with zero
+        // source deltas) writes the bf16 copies of the copy-engine part.
         cuda_check(launch_wait_peers(&B->flags->updated, &B->flags->updated, pa, comm_stream),
                    "wait kernel");
         cuda_check(cudaEventRecord(ce_fork, comm_stream), "cudaEventRecord");
-        for (int k = 0; k < kCeStreams; ++k)
-          cuda_check(cudaStreamWaitEvent(ce_stream[k], ce_fork, 0), "cudaStreamWaitEvent");
-        {
-          // Equal element shares per copy stream, units split at share edges.
-          const int64_t share = (B->e_zag + kCeStreams - 1) / kCeStreams;
-          int64_t pos = 0;
-          for (const Unit& U : B->zag_host) {
-            int64_t o = 0;
-            while (o < U.len) {
-              const int k = static_cast<int>(pos / share);
-              const int64_t n = std::min(U.len - o, (k + 1) * share - pos);
-              const void* src = reinterpret_cast<const char*>(U.a + o) + qa.delta[U.peer];
-              cuda_check(cudaMemcpyAsync(U.b + o, src, static_cast<size_t>(n) * sizeof(float),
-                                         cudaMemcpyDefault, ce_stream[k]),
-                         "cudaMemcpyAsync(ce ag)");
-              o += n;
-              pos += n;
-            }
-          }
+        cuda_check(cudaStreamWaitEvent(ce_stream[0], ce_fork, 0), "cudaStreamWaitEvent");
+        for (int i = 0; i < B->n_zcc; ++i) {
+          const Unit& U = B->zag_host[static_cast<size_t>(i)];
+          const void* src = reinterpret_cast<const char*>(U.a) + qa.delta[U.peer];
+          cuda_check(cudaMemcpyAsync(U.b, src, static_cast<size_t>(U.len) * sizeof(float),
+                                     cudaMemcpyDefault, ce_stream[0]),
+                     "cudaMemcpyAsync(ce ag)");
         }
-        for (int k = 0; k < kCeStreams; ++k) {
-          cuda_check(cudaEventRecord(ce_join[k], ce_stream[k]), "cudaEventRecord");
-          cuda_check(cudaStreamWaitEvent(comm_stream, ce_join[k], 0), "cudaStreamWaitEvent");
-        }
-        if (B->any_shadow) {
+        cuda_check(cudaEventRecord(ce_join[0], ce_stream[0]), "cudaEventRecord");
+        if (B->n_zsm > 0)
+          cuda_check(launch_ag_unpack_peer(B->zsm_u, B->zsm_ps, B->e_zsm, B->any_shadow ? 1 : 0,
+                                           pa, qa, B->flags, kZcSlices, comm_stream),
+                     "zero-copy ag kernel");
+        cuda_check(cudaStreamWaitEvent(comm_stream, ce_join[0], 0), "cudaStreamWaitEvent");
+        if (B->any_shadow && B->n_zcc > 0) {
           PeerArgs za = qa;
           for (int k = 0; k < kMaxPeers; ++k) za.delta[k] = 0;
-          cuda_check(launch_ag_unpack_peer(B->zag_u, B->zag_ps, B->e_zag, 1, pa, za, B->flags,
+          cuda_check(launch_ag_unpack_peer(B->zcc_u, B->zcc_ps, B->e_zcc, 1, pa, za, B->flags,
                                            kZcSlices, comm_stream),
                      "bf16 copy kernel");
         }
@@ -855,7 +853,8 @@ int dear_finalize(dear_ctx* ctx) {
   // Zero-copy tables for a later dear_peer_connect (multi-process only).
   c.zc_tables = !c.local && c.P > 1;
   const char* ce_env = std::getenv("DEAR_CE_AG");
-  c.ce_ag = ce_env && ce_env[0] == '1';
+  c.ce_frac = ce_env ? std::min(1.0, std::max(0.0, std::atof(ce_env))) : 0.0;
+  c.ce_ag = c.ce_frac > 0.0;
   // Unit tables.
   std::vector<Unit> host_units;
   struct Span { size_t pack, upd, unpack; };
@@ -874,13 +873,13 @@ int dear_finalize(dear_ctx* ctx) {
     size_t nu = 0;
     for_each_piece(c, B, bg[static_cast<size_t>(own)], bg[static_cast<size_t>(own) + 1],
                    [&](int, int64_t, int64_t, int64_t) { ++nu; });
-    units += 2 * n + nu + (c.direct ? n : 0) + (c.zc_tables ? n : 0);
+    units += 2 * n + nu + (c.direct ? n : 0) + (c.zc_tables ? 2 * n : 0);
   }
   const size_t float_bytes = (floats * sizeof(float) + 255) / 256 * 256;
   const size_t unit_bytes = (units * sizeof(Unit) + 255) / 256 * 256;
   const size_t per_bucket_slices = 3 * static_cast<size_t>(kSlices) + 2 * kPeerSlices +
                                    kPackPeerSlices + (c.direct ? kSlices : 0) +
-                                   (c.zc_tables ? 2 * kZcSlices : 0);
+                                   (c.zc_tables ? 4 * kZcSlices : 0);
   const size_t n_slices = plan.size() * per_bucket_slices;
   const size_t slice_bytes = (n_slices * sizeof(Slice) + 255) / 256 * 256;
   // Layout: [bucket buffers + momentum][flags] is identical on every rank (the
@@ -988,6 +987,20 @@ int dear_finalize(dear_ctx* ctx) {
       B.n_zag = static_cast<int>(host_units.size() - static_cast<size_t>(B.zag_u - up));
       B.e_zag = set_starts(host_units, static_cast<size_t>(B.zag_u - up));
       B.zag_host.assign(host_units.begin() + (B.zag_u - up), host_units.end());
+      {
+        const int64_t target = static_cast<int64_t>(c.ce_frac * static_cast<double>(B.e_zag));
+        int64_t acc = 0;
+        while (B.n_zcc < B.n_zag && acc + B.zag_host[static_cast<size_t>(B.n_zcc)].len <= target)
+          acc += B.zag_host[static_cast<size_t>(B.n_zcc++)].len;
+        if (c.ce_frac >= 1.0) B.n_zcc = B.n_zag;
+        B.n_zsm = B.n_zag - B.n_zcc;
+        B.zcc_u = up + host_units.size();
+        host_units.insert(host_units.end(), B.zag_host.begin(), B.zag_host.begin() + B.n_zcc);
+        B.e_zcc = set_starts(host_units, static_cast<size_t>(B.zcc_u - up));
+        B.zsm_u = up + host_units.size();
+        host_units.insert(host_units.end(), B.zag_host.begin() + B.n_zcc, B.zag_host.end());
+        B.e_zsm = set_starts(host_units, static_cast<size_t>(B.zsm_u - up));
+      }
     }
     // Equal element slices per CTA for each op (one wave of kSlices CTAs).
     Slice* hs = host_slices.data() + g * per_bucket_slices;
@@ -1018,6 +1031,14 @@ int dear_finalize(dear_ctx* ctx) {
                   kZcSlices, 2);
       B.zrs_ps = B.pack_s + z0;
       B.zag_ps = B.zrs_ps + kZcSlices;
+      B.zcc_ps = B.zag_ps + kZcSlices;
+      B.zsm_ps = B.zcc_ps + kZcSlices;
+      if (B.n_zcc > 0)
+        make_slices(host_units.data() + (B.zcc_u - up), B.n_zcc, B.e_zcc, hs + z0 + 2 * kZcSlices,
+                    kZcSlices, 2);
+      if (B.n_zsm > 0)
+        make_slices(host_units.data() + (B.zsm_u - up), B.n_zsm, B.e_zsm, hs + z0 + 3 * kZcSlices,
+                    kZcSlices, 2);
     }
     B.ag_done = new_event(false);
     for (int k = 0; k < T_COUNT; ++k) B.t[k] = new_event(true);
