@@ -94,6 +94,24 @@ int dear_comm_destroy(void* comm);
 int dear_local_group_create(int32_t P, dear_local_group** group);
 int dear_local_group_destroy(dear_local_group* group);
 
+/* Local-group transports. RING: the ranks' ops are queued and the group runs
+ * each collective once every rank reached it, as ring-order kernels over all
+ * ranks' buffers (collective.cpp:59-152). PEER: the contexts behave like one
+ * process per GPU on the NVLink peer backend — the SAME fused kernels
+ * (zero-copy or slot RS+update, AG), with the other ranks' memory addressed by
+ * in-process deltas instead of IPC mappings — so a one-GPU box runs the
+ * multi-GPU data path. Every rank's spinning peer kernel must be resident at
+ * once, so each takes at most SMs/P CTAs; ranks need distinct compute streams
+ * (a rank's dear_step fence waits on the other ranks' reduce-scatters). */
+#define DEAR_LOCAL_RING 0
+#define DEAR_LOCAL_PEER 1
+int dear_local_group_create_ex(int32_t P, int32_t transport, dear_local_group** group);
+/* PEER transport, after dear_finalize on every rank: connect the ranks.
+ * allow_zero_copy = 1 selects the zero-copy kernels when every rank's
+ * gradients and parameters share one relative layout (as dear_peer_connect);
+ * 0 forces the slot path. dear_peer_zero_copy reports the outcome. */
+int dear_local_group_connect(dear_local_group* group, int32_t allow_zero_copy);
+
 /* ---------------------------------------------------------------------------
  * Runtime context (the DistOptim of PAPER.md:183-188).
  * ------------------------------------------------------------------------ */

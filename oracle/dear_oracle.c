@@ -52,6 +52,14 @@ void or_random_vectors(int P, int64_t d, uint64_t seed, double* out) {
   for (int64_t i = 0; i < (int64_t)P * d; ++i) out[i] = or_uniform_pm1(&g);
 }
 
+/* The same draws rounded to fp32 (= or_random_vectors then a cast), without
+ * the fp64 array: bench-scale parity inputs (BERT-L: 336M per rank). */
+void or_random_vectors_f32(int P, int64_t d, uint64_t seed, float* out) {
+  or_mt64 g;
+  or_mt64_seed(&g, seed);
+  for (int64_t i = 0; i < (int64_t)P * d; ++i) out[i] = (float)or_uniform_pm1(&g);
+}
+
 /* -------------------------------------------------------------- presets --
  * model.cpp:80-86 (tensor counts and totals), :90-98 (spread_uniform: first
  * total%count shares get +1), :138-152 (imbalanced: 80% of the parameters in

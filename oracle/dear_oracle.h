@@ -33,6 +33,7 @@ uint64_t or_mt64_next(or_mt64* g);
 double or_uniform_pm1(or_mt64* g);
 /* P*d values, worker-major, one generator — random_vectors() of the tests. */
 void or_random_vectors(int P, int64_t d, uint64_t seed, double* out);
+void or_random_vectors_f32(int P, int64_t d, uint64_t seed, float* out);
 
 /* ---- Model presets (model.cpp:80-168). profile 0 = Uniform, 1 = Imbalanced.
  * Returns L (tensor count) or -1 on unknown name / cap too small. */

@@ -40,6 +40,7 @@ class Restated:
             build(ref=False)
         lib = C.CDLL(path)
         lib.or_random_vectors.argtypes = [C.c_int, C.c_int64, C.c_uint64, _f64p]
+        lib.or_random_vectors_f32.argtypes = [C.c_int, C.c_int64, C.c_uint64, _f32p]
         lib.or_preset_params.argtypes = [C.c_char_p, C.c_int, _i64p, C.c_int]
         lib.or_build_fusion_plan.argtypes = [_i64p, C.c_int, C.c_int64, _i32p, _i32p]
         lib.or_chunk_ranges.argtypes = [C.c_int64, C.c_int, _i64p]
@@ -59,6 +60,12 @@ class Restated:
     def random_vectors(self, P: int, d: int, seed: int) -> np.ndarray:
         out = np.empty(P * d, np.float64)
         self.lib.or_random_vectors(P, d, seed, out)
+        return out.reshape(P, d)
+
+    def random_vectors_f32(self, P: int, d: int, seed: int) -> np.ndarray:
+        """random_vectors(P, d, seed).astype(float32) without the fp64 array."""
+        out = np.empty(P * d, np.float32)
+        self.lib.or_random_vectors_f32(P, d, seed, out)
         return out.reshape(P, d)
 
     def preset_params(self, name: str, profile: int = 0) -> np.ndarray:

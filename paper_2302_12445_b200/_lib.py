@@ -53,6 +53,8 @@ _SIGNATURES = {
     "dear_comm_destroy": [_P],
     "dear_local_group_create": [C.c_int32, C.POINTER(_P)],
     "dear_local_group_destroy": [_P],
+    "dear_local_group_create_ex": [C.c_int32, C.c_int32, C.POINTER(_P)],
+    "dear_local_group_connect": [_P, C.c_int32],
     "dear_create": [_P, C.c_int32, C.c_int32, _P, C.POINTER(DearCfg), C.POINTER(_P)],
     "dear_create_local": [_P, C.c_int32, _P, C.POINTER(DearCfg), C.POINTER(_P)],
     "dear_register_tensor": [_P, C.c_int32, _P, _P, C.c_int64],

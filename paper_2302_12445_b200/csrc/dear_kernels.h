@@ -131,6 +131,9 @@ struct PeerArgs {
   int64_t delta[kMaxPeers];  // peer arena base - own arena base (bytes)
   int32_t P;
   int32_t rank;
+  long long spin_limit;  // clock64 cycles a cross-GPU wait may spin before __trap (0: forever)
+  int32_t grid;          // > 0: cap on the peer kernels' grid (same-device peer group)
+  int32_t pad;
 };
 struct BucketFlags {
   uint32_t packed;
@@ -177,6 +180,9 @@ cudaError_t launch_rs_update_zc(const Unit* units, const Slice* slices, const Hy
                                 int has_momentum_buf, float* mom_base, int use_momentum,
                                 int use_wd, int with_shadow, const PeerArgs& pa,
                                 const PeerArgs& ga, BucketFlags* flags, cudaStream_t s);
+
+// hp->lr = lr, stream-ordered (dear_set_lr; graph-capturable).
+cudaError_t launch_set_lr(HyperParams* hp, float lr, cudaStream_t s);
 
 // Order-independent 64-bit hash of float bit patterns (sum of mixed words),
 // accumulated into *acc with atomics. Used by dear_check_replicas.

@@ -276,8 +276,9 @@ __global__ void wait_peers_kernel(const uint32_t* mine, const uint32_t* watch, P
     const long long t0 = clock64();
     while (static_cast<int32_t>(ld_acquire_sys(f) - target) < 0) {
       __nanosleep(256);
-      // A peer that never arrives must fail loudly, not hang the GPU.
-      if (clock64() - t0 > 60ll * 2000000000ll) __trap();
+      // A peer that never arrives fails loudly after pa.spin_limit cycles
+      // (DEAR_PEER_TIMEOUT_S; 0 = wait forever, like NCCL).
+      if (pa.spin_limit > 0 && clock64() - t0 > pa.spin_limit) __trap();
     }
   }
 }
@@ -296,7 +297,7 @@ __device__ __forceinline__ void cta_wait_peers(const uint32_t* mine, const uint3
       const long long t0 = clock64();
       while (static_cast<int32_t>(ld_acquire_sys(f) - target) < 0) {
         __nanosleep(128);
-        if (clock64() - t0 > 60ll * 2000000000ll) __trap();  // fail loudly, never hang
+        if (pa.spin_limit > 0 && clock64() - t0 > pa.spin_limit) __trap();
       }
     }
     __syncwarp();
@@ -662,7 +663,7 @@ __device__ __forceinline__ void cta_announce_and_wait(BucketFlags* flags, const 
       const long long t0 = clock64();
       while (static_cast<int32_t>(ld_acquire_sys(f) - target) < 0) {
         __nanosleep(128);
-        if (clock64() - t0 > 60ll * 2000000000ll) __trap();  // fail loudly, never hang
+        if (pa.spin_limit > 0 && clock64() - t0 > pa.spin_limit) __trap();
       }
     }
     __syncwarp();
@@ -814,173 +815,6 @@ __global__ void DEAR_ZC_BOUNDS
   signal_done(&flags->done[1], &flags->updated);
 }
 
-// ---------------------------- zero-copy RS+update, TMA-staged (opt-in) ----
-// Same arithmetic and protocol as rs_update_zc_kernel, but the P gradient
-// streams (and the parameters) move by 1-D bulk TMA (cp.async.bulk) into a
-// shared-memory ring instead of per-thread loads (hypothesis: a per-SM cap on
-// outstanding LSU misses bounds the register version, since 2 CTAs per SM did
-// not help); the bulk engine keeps a whole stage per source in flight
-// from one issuing thread while the other warps sum / update from shared
-// memory. One CTA per SM; thread 0 refills a stage as soon as every warp has
-// consumed it.
-#ifndef DEAR_ZC_TMA_STAGES
-#define DEAR_ZC_TMA_STAGES 4
-#endif
-constexpr int kZcStages = DEAR_ZC_TMA_STAGES;
-
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_addr(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
-                                         uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-          "r"(smem_addr(dst)),
-      "l"(src), "r"(bytes), "r"(smem_addr(bar))
-      : "memory");
-}
-
-// Stage layout: (PC + 1) slots of kChunk floats (PC gradient sources in ring
-// order, then the parameters). kChunk per source keeps the ring <= ~160 KB.
-template <int PC>
-struct ZcTma {
-  static constexpr int kChunk = PC <= 2 ? 4096 : (PC <= 4 ? 2048 : 1024);  // floats
-  static constexpr int kSlot = kChunk * 4;                                // bytes
-  static constexpr int kStageBytes = (PC + 1) * kSlot;
-  static constexpr int kSmem = kZcStages * kStageBytes + 64;
-};
-
-template <int PC, bool kMom, bool kWd, bool kShadow>
-__global__ void __launch_bounds__(kThreads, 1)
-    rs_update_zc_tma_kernel(const Unit* __restrict__ units, const Slice* __restrict__ slices,
-                            const HyperParams* __restrict__ hpp, int has_buf, float* mom_base,
-                            PeerArgs pa, PeerArgs ga, BucketFlags* flags) {
-  using T = ZcTma<PC>;
-  extern __shared__ __align__(128) unsigned char zsm[];
-  float* ring = reinterpret_cast<float*>(zsm);
-  uint64_t* full = reinterpret_cast<uint64_t*>(zsm + kZcStages * T::kStageBytes);
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < kZcStages; ++i) mbar_init(&full[i], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  cta_announce_and_wait(flags, pa);  // ends with __syncthreads
-  if (threadIdx.x == 0) asm volatile("fence.proxy.async;" ::: "memory");
-  const HyperParams hp = *hpp;
-  const int k0 = (pa.rank + 1) % PC;
-  uint32_t iter = 0;  // chunks consumed by this CTA so far (ring position / parity)
-  walk_slice(units, slices, kZcSlices, [&](const Unit& U, int64_t off, int64_t n) {
-    const float* g = U.a + off;
-    float* w = U.b + off;
-    float* mom = kMom ? mom_base + U.start + off : nullptr;
-    __nv_bfloat16* sh = (kShadow && U.c) ? static_cast<__nv_bfloat16*>(U.c) + off : nullptr;
-    auto scalar = [&](int64_t i) {
-      int k = k0;
-      float acc = __ldcg(at_peer(g + i, ga.delta[k]));
-      for (int j = 1; j < PC; ++j) {
-        k = k + 1 == PC ? 0 : k + 1;
-        acc = __fadd_rn(acc, __ldcg(at_peer(g + i, ga.delta[k])));
-      }
-      float m = kMom ? mom[i] : 0.f;
-      const float v = sgd_elem<kMom, kWd>(acc, w[i], m, hp, has_buf);
-      w[i] = v;
-      if (kMom) mom[i] = m;
-      if (kShadow && sh) sh[i] = __float2bfloat16_rn(v);
-    };
-    int64_t head = ((16 - (reinterpret_cast<uintptr_t>(w) & 15)) & 15) >> 2;
-    if (head > n) head = n;
-    if (threadIdx.x < head) scalar(static_cast<int64_t>(threadIdx.x));
-    const int64_t nv = (n - head) & ~int64_t{3};  // vector elements (16 B multiples)
-    const int64_t nchunks = (nv + T::kChunk - 1) / T::kChunk;
-    const float* gb = g + head;
-    float* wb = w + head;
-    auto issue = [&](int64_t c) {  // thread 0: chunk c into its ring stage
-      const uint32_t st = (iter + static_cast<uint32_t>(c)) % kZcStages;
-      const int64_t e0 = c * T::kChunk;
-      const uint32_t bytes = static_cast<uint32_t>((nv - e0 < T::kChunk ? nv - e0 : int64_t{T::kChunk}) * 4);
-      float* base = ring + static_cast<size_t>(st) * (PC + 1) * T::kChunk;
-      mbar_expect(&full[st], bytes * (PC + 1));
-#pragma unroll
-      for (int j = 0; j < PC; ++j)
-        bulk_g2s(base + j * T::kChunk, at_peer(gb + e0, ga.delta[(k0 + j) % PC]), bytes, &full[st]);
-      bulk_g2s(base + PC * T::kChunk, wb + e0, bytes, &full[st]);
-    };
-    if (threadIdx.x == 0)
-      for (int64_t c = 0; c < nchunks && c < kZcStages; ++c) issue(c);
-    for (int64_t c = 0; c < nchunks; ++c) {
-      const uint32_t pos = iter + static_cast<uint32_t>(c);
-      const uint32_t st = pos % kZcStages;
-      mbar_wait(&full[st], (pos / kZcStages) & 1u);
-      const float* base = ring + static_cast<size_t>(st) * (PC + 1) * T::kChunk;
-      const int64_t e0 = c * T::kChunk;
-      const int n4 = static_cast<int>((nv - e0 < T::kChunk ? nv - e0 : int64_t{T::kChunk}) >> 2);
-      float4* w4 = reinterpret_cast<float4*>(wb + e0);
-      float* mh = kMom ? mom + head + e0 : nullptr;
-      const bool mvec = kMom && (reinterpret_cast<uintptr_t>(mh) & 15) == 0;
-      for (int q = threadIdx.x; q < n4; q += kThreads) {
-        float4 acc = reinterpret_cast<const float4*>(base)[q];
-#pragma unroll
-        for (int j = 1; j < PC; ++j) {
-          const float4 v = reinterpret_cast<const float4*>(base + j * T::kChunk)[q];
-          acc.x = __fadd_rn(acc.x, v.x);
-          acc.y = __fadd_rn(acc.y, v.y);
-          acc.z = __fadd_rn(acc.z, v.z);
-          acc.w = __fadd_rn(acc.w, v.w);
-        }
-        const float4 wv = reinterpret_cast<const float4*>(base + PC * T::kChunk)[q];
-        float4 mv = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (kMom && has_buf) {
-          if (mvec)
-            mv = reinterpret_cast<const float4*>(mh)[q];
-          else
-            mv = make_float4(mh[4 * q], mh[4 * q + 1], mh[4 * q + 2], mh[4 * q + 3]);
-        }
-        float4 o;
-        o.x = sgd_elem<kMom, kWd>(acc.x, wv.x, mv.x, hp, has_buf);
-        o.y = sgd_elem<kMom, kWd>(acc.y, wv.y, mv.y, hp, has_buf);
-        o.z = sgd_elem<kMom, kWd>(acc.z, wv.z, mv.z, hp, has_buf);
-        o.w = sgd_elem<kMom, kWd>(acc.w, wv.w, mv.w, hp, has_buf);
-        w4[q] = o;
-        if (kMom) {
-          if (mvec) {
-            reinterpret_cast<float4*>(mh)[q] = mv;
-          } else {
-            mh[4 * q] = mv.x;
-            mh[4 * q + 1] = mv.y;
-            mh[4 * q + 2] = mv.z;
-            mh[4 * q + 3] = mv.w;
-          }
-        }
-        if (kShadow && sh) store_bf16x4(sh + head + e0, q, o);
-      }
-      __syncthreads();  // every warp is done with this stage
-      if (threadIdx.x == 0 && c + kZcStages < nchunks) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue(c + kZcStages);
-      }
-    }
-    iter += static_cast<uint32_t>(nchunks);
-    for (int64_t i = head + nv + threadIdx.x; i < n; i += kThreads) scalar(i);
-  });
-  signal_done(&flags->done[1], &flags->updated);
-}
-
 // ------------------------------------------- fused peer AG+unpack ---------
 // Source element of a unit: U.a + off on rank U.peer, i.e. at sa.delta[U.peer]
 // (sa = arena deltas for bucket slots, parameter deltas for zero-copy).
@@ -1039,6 +873,8 @@ __global__ void local_ag_kernel(float* const* __restrict__ bufs, int P, int64_t 
   }
 }
 
+__global__ void set_lr_kernel(HyperParams* hp, float lr) { hp->lr = lr; }
+
 // ---------------------------------------------------------------- hash ----
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
@@ -1070,6 +906,13 @@ int bucket_grid(int n_slices, int want = 0) {
   return g > 0 && g < n_slices ? g : n_slices;
 }
 
+// Peer kernels: pa.grid (> 0) caps the grid — the same-device peer group runs
+// P ranks' spinning kernels on one GPU, which must all be resident at once.
+int peer_grid(int n_slices, const PeerArgs& pa) {
+  const int g = bucket_grid(n_slices);
+  return pa.grid > 0 && pa.grid < g ? pa.grid : g;
+}
+
 }  // namespace
 
 cudaError_t launch_pack(const Unit* units, const Slice* slices, int64_t total, float scale,
@@ -1084,10 +927,10 @@ cudaError_t launch_pack_signal(const Unit* units, const Slice* slices, int64_t t
                                BucketFlags* flags, const PeerArgs& pa, cudaStream_t s) {
   (void)total;  // the signal must fire even for an empty bucket
   if (kPeerPackLight)
-    pack_kernel<true><<<bucket_grid(kPackPeerSlices), kThreads, 0, s>>>(units, slices, scale, flags,
+    pack_kernel<true><<<peer_grid(kPackPeerSlices, pa), kThreads, 0, s>>>(units, slices, scale, flags,
                                                                        pa, kPackPeerSlices);
   else
-    pack_kernel<true><<<bucket_grid(kSlices), kThreads, 0, s>>>(units, slices, scale, flags, pa,
+    pack_kernel<true><<<peer_grid(kSlices, pa), kThreads, 0, s>>>(units, slices, scale, flags, pa,
                                                                 kSlices);
   return cudaGetLastError();
 }
@@ -1102,7 +945,7 @@ template <int PC>
 void launch_rs_update_peer_p(const Unit* units, const Slice* slices, const HyperParams* hp,
                              int has_momentum_buf, int use_momentum, int use_wd,
                              const PeerArgs& pa, BucketFlags* flags, cudaStream_t s) {
-  const int grid = bucket_grid(kPeerSlices);
+  const int grid = peer_grid(kPeerSlices, pa);
   if (use_momentum && use_wd)
     rs_update_peer_kernel<PC, true, true><<<grid, kThreads, 0, s>>>(units, slices, hp, has_momentum_buf, pa, flags);
   else if (use_momentum)
@@ -1133,9 +976,9 @@ cudaError_t launch_ag_unpack_peer(const Unit* units, const Slice* slices, int64_
   (void)total;
   const size_t smem = 0;
   if (with_shadow)
-    ag_unpack_peer_kernel<true><<<bucket_grid(n_slices), kThreads, smem, s>>>(units, slices, pa, sa, flags, n_slices);
+    ag_unpack_peer_kernel<true><<<peer_grid(n_slices, pa), kThreads, smem, s>>>(units, slices, pa, sa, flags, n_slices);
   else
-    ag_unpack_peer_kernel<false><<<bucket_grid(n_slices), kThreads, smem, s>>>(units, slices, pa, sa, flags, n_slices);
+    ag_unpack_peer_kernel<false><<<peer_grid(n_slices, pa), kThreads, smem, s>>>(units, slices, pa, sa, flags, n_slices);
   return cudaGetLastError();
 }
 
@@ -1143,36 +986,8 @@ template <int PC, bool kMom, bool kWd>
 void launch_rs_zc_p(const Unit* units, const Slice* slices, const HyperParams* hp, int has_buf,
                     float* mom_base, int with_shadow, const PeerArgs& pa, const PeerArgs& ga,
                     BucketFlags* flags, cudaStream_t s) {
-  const int grid = bucket_grid(kZcSlices);
+  const int grid = peer_grid(kZcSlices, pa);
   const size_t smem = 0;
-  // Bulk-TMA staging for P in {2, 4, 8} with DEAR_ZC_TMA=1. Off by default:
-  // same isolated time as the register kernel at P = 4 (53 us per 25 MB
-  // bucket, so the per-SM LSU limit was not the bound), and its 160-192 KB
-  // ring cannot share an SM with a GEMM CTA (profiles/r01e_zc_experiments.md).
-  static const bool tma = [] {
-    const char* e = std::getenv("DEAR_ZC_TMA");
-    return e && e[0] == '1';
-  }();
-  if constexpr (PC > 0) {
-    if (tma) {
-      const int sm = ZcTma<PC>::kSmem;
-      static bool attr = false;
-      if (!attr) {
-        cudaFuncSetAttribute(rs_update_zc_tma_kernel<PC, kMom, kWd, true>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-        cudaFuncSetAttribute(rs_update_zc_tma_kernel<PC, kMom, kWd, false>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-        attr = true;
-      }
-      if (with_shadow)
-        rs_update_zc_tma_kernel<PC, kMom, kWd, true><<<grid, kThreads, sm, s>>>(
-            units, slices, hp, has_buf, mom_base, pa, ga, flags);
-      else
-        rs_update_zc_tma_kernel<PC, kMom, kWd, false><<<grid, kThreads, sm, s>>>(
-            units, slices, hp, has_buf, mom_base, pa, ga, flags);
-      return;
-    }
-  }
   if (with_shadow)
     rs_update_zc_kernel<PC, kMom, kWd, true><<<grid, kThreads, smem, s>>>(units, slices, hp, has_buf,
                                                                         mom_base, pa, ga, flags);
@@ -1293,6 +1108,11 @@ cudaError_t launch_local_all_gather(float* const* bufs_dev, int P, int64_t strid
                                     int64_t count, cudaStream_t s) {
   if (count <= 0) return cudaSuccess;
   local_ag_kernel<<<kSms * 4, 256, 0, s>>>(bufs_dev, P, stride, count);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_set_lr(HyperParams* hp, float lr, cudaStream_t s) {
+  set_lr_kernel<<<1, 1, 0, s>>>(hp, lr);
   return cudaGetLastError();
 }
 

@@ -66,12 +66,13 @@ bool is_dear(int policy) {
 }
 
 enum OpKind { OP_FENCE_READY, OP_FENCE_STEP, OP_PACK, OP_RS, OP_UPDATE, OP_AG, OP_UNPACK,
-              OP_AG_DONE, OP_CALLER_WAIT_PACKED };
+              OP_AG_DONE, OP_CALLER_WAIT_PACKED, OP_SET_LR };
 
 struct Op {
   OpKind kind;
   int bucket;
   cudaStream_t stream;  // OP_CALLER_WAIT_PACKED
+  float value = 0.f;    // OP_SET_LR
   bool collective() const { return kind == OP_RS || kind == OP_AG; }
 };
 
@@ -109,13 +110,6 @@ struct Bucket {
   int n_zrs = 0, n_zag = 0;
   int64_t e_zrs = 0, e_zag = 0;
   Slice *zrs_ps = nullptr, *zag_ps = nullptr;
-  std::vector<Unit> zag_host;  // host copy of the AG units (copy-engine all-gather)
-  // DEAR_CE_AG split: AG units [0, n_zcc) go to the copy engines (zcc_u: the
-  // same units for the bf16 pass), [n_zcc, n_zag) to the AG kernel (zsm_u).
-  Unit *zcc_u = nullptr, *zsm_u = nullptr;
-  int n_zcc = 0, n_zsm = 0;
-  int64_t e_zcc = 0, e_zsm = 0;
-  Slice *zcc_ps = nullptr, *zsm_ps = nullptr;
   Unit* dir_u = nullptr;                           // P = 1 direct update (grad -> param)
   int n_dir = 0;
   int64_t e_dir = 0;
@@ -139,6 +133,7 @@ using namespace dear;
 
 struct dear_local_group {
   int P = 0;
+  int transport = DEAR_LOCAL_RING;
   std::vector<dear_ctx*> ranks;
   std::map<int, float**> bufs_dev;  // bucket -> device array of P buffers
   cudaEvent_t arrive[64] = {};
@@ -185,15 +180,11 @@ struct dear_ctx {
   bool zc = false;
   bool zc_tables = false;  // finalize built the zero-copy unit tables
   PeerArgs ga{}, qa{};
-  // DEAR_CE_AG=1 (zero-copy only): the all-gather's NVLink reads run on the
-  // copy engines (one cudaMemcpyAsync per AG unit from the owner's mapped
-  // parameters) and a local in-place pass writes the bf16 copies, so the
-  // SMs the forward GEMMs use are not held waiting on NVLink loads.
-  bool ce_ag = false;
-  double ce_frac = 0.0;  // DEAR_CE_AG=<fraction of AG elements on the copy engines>
-  static constexpr int kCeStreams = 1;
-  cudaStream_t ce_stream[kCeStreams] = {};
-  cudaEvent_t ce_fork = nullptr, ce_join[kCeStreams] = {};
+  // Same-device peer group (dear_local_group_create_ex(.., DEAR_LOCAL_PEER)):
+  // the P ranks are contexts of this process on one device, and the peer
+  // kernels address each other's memory with in-process deltas instead of
+  // IPC mappings.
+  bool same_dev = false;
   std::vector<void*> peer_maps;  // cudaIpcOpenMemHandle mappings to close
   bool timing = false;
   std::vector<std::string> trace;
@@ -358,6 +349,9 @@ void dear_local_group::drain() {
 }
 
 dear_ctx::~dear_ctx() {
+  // Same-device peer group: the other ranks' kernels read this context's
+  // memory; the caller synchronised every rank, so this only drains the device.
+  if (same_dev) cudaDeviceSynchronize();
   if (comm_stream) cudaStreamSynchronize(comm_stream);
   for (Bucket& b : buckets) {
     free_events(b.ready_events);
@@ -371,11 +365,6 @@ dear_ctx::~dear_ctx() {
   for (void* m : peer_maps) cudaIpcCloseMemHandle(m);
   if (arena) cudaFree(arena);
   if (comm_stream) cudaStreamDestroy(comm_stream);
-  for (int k = 0; k < kCeStreams; ++k) {
-    if (ce_stream[k]) cudaStreamDestroy(ce_stream[k]);
-    if (ce_join[k]) cudaEventDestroy(ce_join[k]);
-  }
-  if (ce_fork) cudaEventDestroy(ce_fork);
   if (group) {
     for (auto& r : group->ranks)
       if (r == this) r = nullptr;
@@ -485,36 +474,7 @@ void dear_ctx::exec(const Op& op) {
       break;
     case OP_AG:
       if (!local) record_t(op.bucket, T_AG0);
-      if (zc && ce_ag) {
-        // Split all-gather: the first `ce_frac` of the bucket's AG units are
-        // pulled by the copy engines on a side stream while the AG kernel
-        // pulls the rest; then a local in-place pass (the AG kernel with zero
-        // source deltas) writes the bf16 copies of the copy-engine part.
-        cuda_check(launch_wait_peers(&B->flags->updated, &B->flags->updated, pa, comm_stream),
-                   "wait kernel");
-        cuda_check(cudaEventRecord(ce_fork, comm_stream), "cudaEventRecord");
-        cuda_check(cudaStreamWaitEvent(ce_stream[0], ce_fork, 0), "cudaStreamWaitEvent");
-        for (int i = 0; i < B->n_zcc; ++i) {
-          const Unit& U = B->zag_host[static_cast<size_t>(i)];
-          const void* src = reinterpret_cast<const char*>(U.a) + qa.delta[U.peer];
-          cuda_check(cudaMemcpyAsync(U.b, src, static_cast<size_t>(U.len) * sizeof(float),
-                                     cudaMemcpyDefault, ce_stream[0]),
-                     "cudaMemcpyAsync(ce ag)");
-        }
-        cuda_check(cudaEventRecord(ce_join[0], ce_stream[0]), "cudaEventRecord");
-        if (B->n_zsm > 0)
-          cuda_check(launch_ag_unpack_peer(B->zsm_u, B->zsm_ps, B->e_zsm, B->any_shadow ? 1 : 0,
-                                           pa, qa, B->flags, kZcSlices, comm_stream),
-                     "zero-copy ag kernel");
-        cuda_check(cudaStreamWaitEvent(comm_stream, ce_join[0], 0), "cudaStreamWaitEvent");
-        if (B->any_shadow && B->n_zcc > 0) {
-          PeerArgs za = qa;
-          for (int k = 0; k < kMaxPeers; ++k) za.delta[k] = 0;
-          cuda_check(launch_ag_unpack_peer(B->zcc_u, B->zcc_ps, B->e_zcc, 1, pa, za, B->flags,
-                                           kZcSlices, comm_stream),
-                     "bf16 copy kernel");
-        }
-      } else if (zc) {
+      if (zc) {
         // Each owner's updated parameters, read over NVLink into ours.
         cuda_check(launch_ag_unpack_peer(B->zag_u, B->zag_ps, B->e_zag, B->any_shadow ? 1 : 0,
                                          pa, qa, B->flags, kZcSlices, comm_stream),
@@ -553,6 +513,9 @@ void dear_ctx::exec(const Op& op) {
         cuda_check(cudaEventRecord(packed_ev, comm_stream), "cudaEventRecord");
       }
       cuda_check(cudaStreamWaitEvent(op.stream, packed_ev, 0), "cudaStreamWaitEvent");
+      break;
+    case OP_SET_LR:
+      cuda_check(launch_set_lr(hp_dev, op.value, comm_stream), "set-lr kernel");
       break;
   }
 }
@@ -669,10 +632,19 @@ int dear_comm_destroy(void* comm) {
 }
 
 int dear_local_group_create(int32_t P, dear_local_group** group) {
+  return dear_local_group_create_ex(P, DEAR_LOCAL_RING, group);
+}
+
+int dear_local_group_create_ex(int32_t P, int32_t transport, dear_local_group** group) {
   DEAR_API_BEGIN
   if (P < 1 || P > 64 || !group) invalid("dear_local_group_create: P must be in 1..64");
+  if (transport != DEAR_LOCAL_RING && transport != DEAR_LOCAL_PEER)
+    invalid("dear_local_group_create_ex: transport must be DEAR_LOCAL_RING or DEAR_LOCAL_PEER");
+  if (transport == DEAR_LOCAL_PEER && P > kMaxPeers)
+    invalid("dear_local_group_create_ex: the peer transport supports at most 16 ranks");
   auto* g = new dear_local_group();
   g->P = P;
+  g->transport = transport;
   g->ranks.assign(static_cast<size_t>(P), nullptr);
   *group = g;
   DEAR_API_END
@@ -752,7 +724,10 @@ int dear_create_local(dear_local_group* group, int32_t rank, void* compute_strea
   if (group->ranks[static_cast<size_t>(rank)]) invalid("dear_create_local: rank already created");
   std::unique_ptr<dear_ctx> c(new dear_ctx());
   create_common(c.get(), rank, group->P, compute_stream, cfg);
-  c->local = true;
+  // Ring transport: ops queue and the group drains them in lock-step. Peer
+  // transport: ops execute at once, like one process per GPU.
+  c->local = group->transport == DEAR_LOCAL_RING;
+  c->same_dev = group->transport == DEAR_LOCAL_PEER;
   c->group = group;
   group->ranks[static_cast<size_t>(rank)] = c.get();
   *out = c.release();
@@ -852,9 +827,6 @@ int dear_finalize(dear_ctx* ctx) {
   c.direct = c.P == 1 && !c.peer && c.cfg.momentum == 0.0 && !(dir_env && dir_env[0] == '0');
   // Zero-copy tables for a later dear_peer_connect (multi-process only).
   c.zc_tables = !c.local && c.P > 1;
-  const char* ce_env = std::getenv("DEAR_CE_AG");
-  c.ce_frac = ce_env ? std::min(1.0, std::max(0.0, std::atof(ce_env))) : 0.0;
-  c.ce_ag = c.ce_frac > 0.0;
   // Unit tables.
   std::vector<Unit> host_units;
   struct Span { size_t pack, upd, unpack; };
@@ -879,7 +851,7 @@ int dear_finalize(dear_ctx* ctx) {
   const size_t unit_bytes = (units * sizeof(Unit) + 255) / 256 * 256;
   const size_t per_bucket_slices = 3 * static_cast<size_t>(kSlices) + 2 * kPeerSlices +
                                    kPackPeerSlices + (c.direct ? kSlices : 0) +
-                                   (c.zc_tables ? 4 * kZcSlices : 0);
+                                   (c.zc_tables ? 2 * kZcSlices : 0);
   const size_t n_slices = plan.size() * per_bucket_slices;
   const size_t slice_bytes = (n_slices * sizeof(Slice) + 255) / 256 * 256;
   // Layout: [bucket buffers + momentum][flags] is identical on every rank (the
@@ -986,21 +958,6 @@ int dear_finalize(dear_ctx* ctx) {
       }
       B.n_zag = static_cast<int>(host_units.size() - static_cast<size_t>(B.zag_u - up));
       B.e_zag = set_starts(host_units, static_cast<size_t>(B.zag_u - up));
-      B.zag_host.assign(host_units.begin() + (B.zag_u - up), host_units.end());
-      {
-        const int64_t target = static_cast<int64_t>(c.ce_frac * static_cast<double>(B.e_zag));
-        int64_t acc = 0;
-        while (B.n_zcc < B.n_zag && acc + B.zag_host[static_cast<size_t>(B.n_zcc)].len <= target)
-          acc += B.zag_host[static_cast<size_t>(B.n_zcc++)].len;
-        if (c.ce_frac >= 1.0) B.n_zcc = B.n_zag;
-        B.n_zsm = B.n_zag - B.n_zcc;
-        B.zcc_u = up + host_units.size();
-        host_units.insert(host_units.end(), B.zag_host.begin(), B.zag_host.begin() + B.n_zcc);
-        B.e_zcc = set_starts(host_units, static_cast<size_t>(B.zcc_u - up));
-        B.zsm_u = up + host_units.size();
-        host_units.insert(host_units.end(), B.zag_host.begin() + B.n_zcc, B.zag_host.end());
-        B.e_zsm = set_starts(host_units, static_cast<size_t>(B.zsm_u - up));
-      }
     }
     // Equal element slices per CTA for each op (one wave of kSlices CTAs).
     Slice* hs = host_slices.data() + g * per_bucket_slices;
@@ -1031,14 +988,6 @@ int dear_finalize(dear_ctx* ctx) {
                   kZcSlices, 2);
       B.zrs_ps = B.pack_s + z0;
       B.zag_ps = B.zrs_ps + kZcSlices;
-      B.zcc_ps = B.zag_ps + kZcSlices;
-      B.zsm_ps = B.zcc_ps + kZcSlices;
-      if (B.n_zcc > 0)
-        make_slices(host_units.data() + (B.zcc_u - up), B.n_zcc, B.e_zcc, hs + z0 + 2 * kZcSlices,
-                    kZcSlices, 2);
-      if (B.n_zsm > 0)
-        make_slices(host_units.data() + (B.zsm_u - up), B.n_zsm, B.e_zsm, hs + z0 + 3 * kZcSlices,
-                    kZcSlices, 2);
     }
     B.ag_done = new_event(false);
     for (int k = 0; k < T_COUNT; ++k) B.t[k] = new_event(true);
@@ -1072,7 +1021,7 @@ int dear_finalize(dear_ctx* ctx) {
   for (const LayerReg& R : c.layers) h = fnv(h, static_cast<uint64_t>(R.numel));
   h = fnv(h, static_cast<uint64_t>(c.cfg.policy));
   h = fnv(h, static_cast<uint64_t>(c.cfg.fusion_buffer_bytes));
-  if (c.local) {
+  if (c.local || c.same_dev) {
     for (dear_ctx* o : c.group->ranks) {
       if (o && o != &c && o->finalized) {
         if (o->buckets.size() != c.buckets.size())
@@ -1279,15 +1228,13 @@ int dear_set_lr(dear_ctx* ctx, double lr) {
   if (!(lr >= 0.0)) invalid("lr must be >= 0");
   ctx->cfg.lr = lr;
   ctx->hp_host.lr = static_cast<float>(lr);
-  // Stream-ordered on the comm stream, so updates already enqueued keep the
-  // old value. The source is a field of the context, read at enqueue time by
-  // the copy engine only after prior comm work; keep a per-call copy alive.
-  static thread_local HyperParams staged;
-  staged = ctx->hp_host;
-  cuda_check(cudaMemcpyAsync(ctx->hp_dev, &staged, sizeof(HyperParams), cudaMemcpyHostToDevice,
-                             ctx->comm_stream),
-             "cudaMemcpyAsync(hp)");
-  cuda_check(cudaStreamSynchronize(ctx->comm_stream), "cudaStreamSynchronize");
+  // A one-thread kernel on the comm stream (value passed by argument): updates
+  // enqueued before keep the old rate, later ones see the new; no host sync,
+  // and legal inside a CUDA-graph capture. Local-group contexts queue it in
+  // order with their pending ops.
+  Op op{OP_SET_LR, -1, nullptr};
+  op.value = static_cast<float>(lr);
+  ctx->enqueue(op);
   DEAR_API_END
 }
 
@@ -1302,7 +1249,9 @@ struct TensorSpan {
 
 using MemGetAddressRange = int (*)(uintptr_t*, size_t*, uintptr_t);
 
-TensorSpan tensor_span(const dear_ctx& c, bool grads) {
+// need_alloc: the tensors must lie in one device allocation (the IPC export
+// unit); the same-device peer group only needs their relative layout.
+TensorSpan tensor_span(const dear_ctx& c, bool grads, bool need_alloc = true) {
   TensorSpan sp;
   static MemGetAddressRange range = [] {
     void* fn = nullptr;
@@ -1311,7 +1260,7 @@ TensorSpan tensor_span(const dear_ctx& c, bool grads) {
       return static_cast<MemGetAddressRange>(nullptr);
     return reinterpret_cast<MemGetAddressRange>(fn);
   }();
-  if (!range) return sp;
+  if (need_alloc && !range) return sp;
   char *lo = nullptr, *hi = nullptr;
   for (const LayerReg& R : c.layers) {
     char* p = reinterpret_cast<char*>(grads ? R.grad : R.param);
@@ -1320,10 +1269,12 @@ TensorSpan tensor_span(const dear_ctx& c, bool grads) {
     if (!hi || p + R.numel * 4 > hi) hi = p + R.numel * 4;
   }
   if (!lo) return sp;
-  uintptr_t base = 0;
+  uintptr_t base = reinterpret_cast<uintptr_t>(lo);
   size_t size = 0;
-  if (range(&base, &size, reinterpret_cast<uintptr_t>(lo)) != 0) return sp;
-  if (reinterpret_cast<uintptr_t>(hi) > base + size) return sp;  // several allocations
+  if (need_alloc) {
+    if (range(&base, &size, reinterpret_cast<uintptr_t>(lo)) != 0) return sp;
+    if (reinterpret_cast<uintptr_t>(hi) > base + size) return sp;  // several allocations
+  }
   uint64_t h = 1469598103934665603ULL;
   for (const LayerReg& R : c.layers) {
     const char* p = reinterpret_cast<const char*>(grads ? R.grad : R.param);
@@ -1345,10 +1296,93 @@ constexpr size_t kH_ZC = 76, kH_G = 80, kH_Q = 144, kH_GOFF = 208, kH_QOFF = 216
                  kH_GLAY = 224, kH_QLAY = 232;
 }  // namespace
 
+namespace {
+// DEAR_PEER_TIMEOUT_S (default 600 s, torch's NCCL watchdog default; 0 =
+// wait forever): how long a cross-GPU wait spins before the kernel traps. A
+// rank doing rank-local work (eval, checkpoint) for longer must barrier first.
+long long peer_spin_limit(int device) {
+  const char* e = std::getenv("DEAR_PEER_TIMEOUT_S");
+  const double s = e ? std::atof(e) : 600.0;
+  if (!(s > 0.0)) return 0;
+  int khz = 0;
+  if (cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, device) != cudaSuccess || khz <= 0)
+    khz = 2000000;
+  return static_cast<long long>(s * static_cast<double>(khz) * 1000.0);
+}
+
+// Switches a finalized context to the peer kernels: pa = arena deltas, ga / qa
+// = gradient / parameter deltas (zero-copy only).
+void enable_peer(dear_ctx& c, PeerArgs pa, PeerArgs ga, PeerArgs qa, bool zc) {
+  pa.spin_limit = peer_spin_limit(c.device);
+  ga.spin_limit = qa.spin_limit = pa.spin_limit;
+  ga.grid = qa.grid = pa.grid;
+  c.pa = pa;
+  c.ga = ga;
+  c.qa = qa;
+  c.peer = true;
+  if (zc) {
+    // No pack, so no pre-scaling: the update applies 1/P after the ring sum
+    // (collective.cpp:159-164's order; for P = 2^k the same bits either way).
+    c.zc = true;
+    c.hp_host.prescaled = 0;
+    cuda_check(cudaMemcpy(c.hp_dev, &c.hp_host, sizeof(HyperParams), cudaMemcpyHostToDevice),
+               "cudaMemcpy(hp)");
+  }
+}
+}  // namespace
+
+int dear_local_group_connect(dear_local_group* group, int32_t allow_zero_copy) {
+  DEAR_API_BEGIN
+  if (!group || group->transport != DEAR_LOCAL_PEER)
+    invalid("dear_local_group_connect: needs a group created with DEAR_LOCAL_PEER");
+  const int P = group->P;
+  for (dear_ctx* c : group->ranks) {
+    if (!c || !c->finalized) invalid("dear_local_group_connect: create and finalize every rank first");
+    if (c->peer) invalid("dear_local_group_connect: already connected");
+  }
+  // Zero-copy when every rank's gradients (and parameters) have the same
+  // layout relative to its lowest tensor address, in the same 16 B phase.
+  const char* env = std::getenv("DEAR_ZERO_COPY");
+  bool zc = allow_zero_copy && P > 1 && !(env && env[0] == '0');
+  std::vector<TensorSpan> gs(static_cast<size_t>(P)), qs(static_cast<size_t>(P));
+  for (int r = 0; r < P && zc; ++r) {
+    const dear_ctx& c = *group->ranks[static_cast<size_t>(r)];
+    gs[static_cast<size_t>(r)] = tensor_span(c, true, false);
+    qs[static_cast<size_t>(r)] = tensor_span(c, false, false);
+    const TensorSpan &g = gs[static_cast<size_t>(r)], &q = qs[static_cast<size_t>(r)];
+    zc = g.ok && q.ok && g.layout == gs[0].layout && q.layout == qs[0].layout &&
+         ((reinterpret_cast<uintptr_t>(g.lo) ^ reinterpret_cast<uintptr_t>(gs[0].lo)) & 15) == 0 &&
+         ((reinterpret_cast<uintptr_t>(q.lo) ^ reinterpret_cast<uintptr_t>(qs[0].lo)) & 15) == 0;
+  }
+  int sms = 148;
+  cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount,
+                                    group->ranks[0]->device), "cudaDeviceGetAttribute");
+  for (int r = 0; r < P; ++r) {
+    dear_ctx& c = *group->ranks[static_cast<size_t>(r)];
+    PeerArgs pa{}, ga{}, qa{};
+    pa.P = ga.P = qa.P = P;
+    pa.rank = ga.rank = qa.rank = r;
+    // Every rank's spinning peer kernel must be resident at once on the one
+    // device: a grid of sms / P CTAs each (at most one per SM and rank).
+    pa.grid = std::max(1, sms / P);
+    for (int k = 0; k < P; ++k) {
+      const dear_ctx& o = *group->ranks[static_cast<size_t>(k)];
+      pa.delta[k] = static_cast<int64_t>(o.arena - c.arena);
+      if (zc) {
+        ga.delta[k] = static_cast<int64_t>(gs[static_cast<size_t>(k)].lo - gs[static_cast<size_t>(r)].lo);
+        qa.delta[k] = static_cast<int64_t>(qs[static_cast<size_t>(k)].lo - qs[static_cast<size_t>(r)].lo);
+      }
+    }
+    enable_peer(c, pa, ga, qa, zc);
+  }
+  DEAR_API_END
+}
+
 int dear_peer_handle(dear_ctx* ctx, uint8_t out[DEAR_PEER_HANDLE_BYTES]) {
   DEAR_API_BEGIN
   need(ctx, true);
-  if (ctx->local) invalid("dear_peer_handle: local-group contexts have no peer backend");
+  if (ctx->local || ctx->same_dev)
+    invalid("dear_peer_handle: local-group contexts connect with dear_local_group_connect");
   if (!out) invalid("dear_peer_handle: null output");
   static_assert(sizeof(cudaIpcMemHandle_t) == 64, "ipc handle size");
   cudaIpcMemHandle_t h;
@@ -1388,7 +1422,8 @@ int dear_peer_connect(dear_ctx* ctx, const uint8_t* handles, int32_t n) {
   DEAR_API_BEGIN
   need(ctx, true);
   dear_ctx& c = *ctx;
-  if (c.local) invalid("dear_peer_connect: local-group contexts have no peer backend");
+  if (c.local || c.same_dev)
+    invalid("dear_peer_connect: local-group contexts connect with dear_local_group_connect");
   if (c.peer) invalid("dear_peer_connect: already connected");
   if (!handles || n != c.P) invalid("dear_peer_connect: need one handle per rank");
   if (c.P > kMaxPeers) invalid("dear_peer_connect: at most 16 ranks");
@@ -1453,27 +1488,8 @@ int dear_peer_connect(dear_ctx* ctx, const uint8_t* handles, int32_t n) {
     for (void* m : maps) cudaIpcCloseMemHandle(m);
     throw;
   }
-  c.pa = pa;
-  c.ga = ga;
-  c.qa = qa;
   c.peer_maps = std::move(maps);
-  c.peer = true;
-  if (zc) {
-    // No pack, so no pre-scaling: the update applies 1/P after the ring sum
-    // (collective.cpp:159-164's order; for P = 2^k the same bits either way).
-    c.zc = true;
-    c.hp_host.prescaled = 0;
-    cuda_check(cudaMemcpy(c.hp_dev, &c.hp_host, sizeof(HyperParams), cudaMemcpyHostToDevice),
-               "cudaMemcpy(hp)");
-    if (c.ce_ag) {
-      c.ce_fork = new_event(false);
-      for (int k = 0; k < dear_ctx::kCeStreams; ++k) {
-        cuda_check(cudaStreamCreateWithFlags(&c.ce_stream[k], cudaStreamNonBlocking),
-                   "cudaStreamCreateWithFlags");
-        c.ce_join[k] = new_event(false);
-      }
-    }
-  }
+  enable_peer(c, pa, ga, qa, zc);
   DEAR_API_END
 }
 
@@ -1615,7 +1631,7 @@ int dear_check_replicas(dear_ctx* ctx, int32_t* identical) {
   if (c.ags_deferred) c.enqueue_feedpipe(c.compute);
   cuda_check(cudaStreamSynchronize(c.comm_stream), "cudaStreamSynchronize");
   const unsigned long long h = hash_params(c);
-  if (c.local) {
+  if (c.local || c.same_dev) {
     bool same = true;
     for (dear_ctx* o : c.group->ranks) {
       if (!o || o == &c) continue;

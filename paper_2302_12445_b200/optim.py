@@ -19,6 +19,15 @@ readiness (BackPipe), a forward pre-hook per module waits for that module's
 buckets (FeedPipe). The wrapped optimizer supplies the hyper-parameters; the
 update itself runs shard-locally on the GPU between reduce-scatter and
 all-gather, so the wrapped optimizer's own ``step`` is never called.
+The learning rate is read from ``param_groups[0]["lr"]`` when the first
+gradient of an iteration is reported (the updates run during backward), so an
+LR scheduler stepped between iterations takes effect on the next iteration's
+update, exactly as with ``torch.optim.SGD``.
+
+One-GPU multi-rank runs: pass ``comm=LocalGroup(P, transport="peer")`` and a
+distinct ``rank`` (and compute ``stream``) per replica, then call
+``group.connect()`` once every replica's DistOptim exists.
+
 Only ``torch.optim.SGD`` is supported — the reference's update is SGD
 (collective.cpp:166-194); momentum / weight decay / nesterov are an unpinned
 extension following torch semantics.
@@ -45,8 +54,12 @@ class DistOptim:
         g = optimizer.param_groups[0]
         if g.get("maximize", False):
             raise ValueError("maximize=True is not supported")
+        if model is None and defer_allgather:
+            raise ValueError("defer_allgather needs the model: its forward pre-hooks flush "
+                             "the deferred all-gathers")
         self.optimizer = optimizer
         self.model = model
+        self._stream = stream
         params = list(model.parameters()) if model is not None else list(g["params"])
         opt_ids = {id(p) for p in g["params"]}
         params = [p for p in params if p.requires_grad and id(p) in opt_ids]
@@ -54,6 +67,7 @@ class DistOptim:
             raise ValueError("build_fusion_plan: empty model")
         self.params = params
         self._lr = float(g["lr"])
+        self._in_backward = False
         if isinstance(comm, LocalGroup):
             world, rank_ = comm.P, rank
         elif isinstance(comm, Communicator):
@@ -118,6 +132,11 @@ class DistOptim:
             if param.grad is None or param.grad.data_ptr() != self._grad_ptr[layer]:
                 raise RuntimeError(f"gradient storage of layer {layer} changed; use "
                                    "DistOptim.zero_grad() (in-place) instead of set_to_none")
+            if not self._in_backward:
+                # First gradient of the iteration: this iteration's updates are
+                # enqueued from now on, so the current LR must be on the device.
+                self._in_backward = True
+                self._sync_lr()
             self.runtime.grad_ready(layer)
         return hook
 
@@ -127,14 +146,23 @@ class DistOptim:
                 self.runtime.param_wait(layer)
         return hook
 
+    def _sync_lr(self):
+        lr = float(self.optimizer.param_groups[0]["lr"])
+        if lr != self._lr:
+            self.runtime.set_lr(lr)  # stream-ordered on the comm stream, no host sync
+            self._lr = lr
+
     def step(self, closure=None):
         if closure is not None:
             raise ValueError("closures are not supported")
-        lr = float(self.optimizer.param_groups[0]["lr"])
-        if lr != self._lr:
-            self.runtime.set_lr(lr)
-            self._lr = lr
-        self.runtime.step()
+        self._in_backward = False
+        self.runtime.step(self._stream)
+        # The wrapped optimizer's update ran on the GPU: tell LR schedulers so.
+        self.optimizer._opt_called = True
+        if self.model is None:
+            # No forward pre-hooks gate the parameters: make the caller's
+            # stream wait for the all-gathers that rewrite them.
+            self.runtime.join(self._stream)
 
     def zero_grad(self, set_to_none: bool = False):
         for p in self.params:

@@ -74,16 +74,34 @@ class Communicator:
 
 
 class LocalGroup:
-    """P ranks emulated in one process on one device (ring-order collectives).
+    """P ranks in one process on one device.
 
-    Drive the P contexts in lock-step: every rank makes the same sequence of
-    calls, and all ranks finish an iteration's ``step`` before any rank starts
-    the next forward."""
+    ``transport="ring"``: ring-order collective kernels over all ranks'
+    buffers (the reference's ring rounds, collective.cpp:59-152). Drive the P
+    contexts in lock-step: every rank makes the same sequence of calls, and
+    all ranks finish an iteration's ``step`` before any rank starts the next
+    forward.
 
-    def __init__(self, P: int):
+    ``transport="peer"``: the contexts run the multi-GPU NVLink peer kernels
+    (zero-copy or slot reduce-scatter + update, all-gather) against each
+    other's memory on the one device — the N > 1 data path on one GPU. Call
+    :meth:`connect` after every rank's ``finalize``; give every rank its own
+    compute stream (a rank's ``step`` fence waits on the other ranks'
+    reduce-scatters)."""
+
+    TRANSPORTS = {"ring": 0, "peer": 1}
+
+    def __init__(self, P: int, transport: str = "ring"):
+        if transport not in self.TRANSPORTS:
+            raise ValueError("transport must be 'ring' or 'peer'")
         self.P = P
+        self.transport = transport
         self._g = C.c_void_p()
-        check(lib().dear_local_group_create(P, C.byref(self._g)))
+        check(lib().dear_local_group_create_ex(P, self.TRANSPORTS[transport], C.byref(self._g)))
+
+    def connect(self, zero_copy: bool = True) -> None:
+        """Peer transport: map the ranks onto each other (dear_local_group_connect)."""
+        check(lib().dear_local_group_connect(self._g, int(zero_copy)))
 
     @property
     def handle(self) -> int:
@@ -109,16 +127,26 @@ class Runtime:
                              f"{', '.join(POLICIES)}")
         if backend not in ("auto", "nccl", "peer"):
             raise ValueError("backend must be 'auto', 'nccl' or 'peer'")
-        if backend == "auto":
+        if isinstance(comm, LocalGroup):
+            # A local group's transport decides the collectives: "local" (the
+            # ring-order emulation kernels) or "peer" (the NVLink peer kernels).
+            if comm.transport == "peer":
+                if backend == "nccl":
+                    raise ValueError("a LocalGroup(transport='peer') runs the peer kernels")
+                backend = "peer"
+            else:
+                if backend == "peer":
+                    raise ValueError("use LocalGroup(P, transport='peer') for the peer kernels "
+                                     "on one device")
+                backend = "local"
+        elif backend == "auto":
             # The NVLink peer path (fused RS+update / AG+unpack kernels) when
             # several processes share torch.distributed; NCCL otherwise.
             backend = "peer" if (isinstance(comm, Communicator) and comm.world_size > 1
                                  and _dist_ready()) else "nccl"
-        if backend == "peer" and isinstance(comm, LocalGroup):
-            raise ValueError("the peer backend needs one process per GPU (not a LocalGroup)")
         self.policy = policy
         self.backend = backend
-        self.zero_copy = False  # set by the peer handshake (dear_peer_zero_copy)
+        self._group = comm if isinstance(comm, LocalGroup) else None
         cfg = DearCfg(POLICIES[policy], int(fusion_buffer_bytes) if "FUSED" in policy else 0,
                       int(dear_group_dependency), float(lr),
                       float(momentum), float(dampening), float(weight_decay), int(nesterov),
@@ -158,8 +186,17 @@ class Runtime:
 
     def finalize(self) -> None:
         check(lib().dear_finalize(self._ctx))
-        if self.backend == "peer" and self.world_size > 1:
+        if self.backend == "peer" and self.world_size > 1 and self._group is None:
             self._connect_peers()
+
+    @property
+    def zero_copy(self) -> bool:
+        """The peer backend took the zero-copy path (dear_peer_zero_copy)."""
+        if not self._ctx.value:
+            return False
+        on = C.c_int32()
+        check(lib().dear_peer_zero_copy(self._ctx, C.byref(on)))
+        return bool(on.value)
 
     def _connect_peers(self) -> None:
         """Exchange arena IPC handles over torch.distributed and map the peers."""
@@ -171,9 +208,6 @@ class Runtime:
         dist.all_gather_object(handles, buf.raw)
         check(lib().dear_peer_connect(self._ctx, b"".join(handles), self.world_size))
         dist.barrier()
-        on = C.c_int32()
-        check(lib().dear_peer_zero_copy(self._ctx, C.byref(on)))
-        self.zero_copy = bool(on.value)
 
     # -- schedule hooks ----------------------------------------------------
     def grad_ready(self, layer: int, stream=None) -> None:
@@ -258,13 +292,26 @@ class Runtime:
         return bool(ok.value)
 
     def close(self) -> None:
+        """Destroy the context. On the multi-process peer backend this is
+        collective: peers may still read this rank's arena / tensors through
+        their mappings, so every rank drains its comm stream and meets the
+        others at a barrier before any unmaps or frees."""
         if self._ctx.value:
+            if self.backend == "peer" and self.world_size > 1 and self._group is None \
+                    and _dist_ready():
+                import torch.distributed as dist
+
+                check(lib().dear_synchronize(self._ctx))
+                dist.barrier()
             check(lib().dear_destroy(self._ctx))
             self._ctx = C.c_void_p()
             self._keep = []
 
     def __del__(self):
+        # Best effort at interpreter teardown (no barrier: peers may be gone).
         try:
-            self.close()
+            if self._ctx.value:
+                check(lib().dear_destroy(self._ctx))
+                self._ctx = C.c_void_p()
         except Exception:
             pass

@@ -27,19 +27,22 @@ def initial_weights(o: Restated, numels, seed: int = 77) -> np.ndarray:
 
 def oracle_run(o: Restated, numels, P: int, steps: int, policy: str, buffer_bytes: int,
                lr: float, momentum=0.0, dampening=0.0, weight_decay=0.0, nesterov=False,
-               f32: bool = True, seed0: int = 1000, wseed: int = 77):
+               f32: bool = True, seed0: int = 1000, wseed: int = 77, w0=None, grads_fn=None,
+               lr_schedule=None):
     """Apply the oracle's S-SGD step per fusion bucket (chunk layout is per
     bucket), for `steps` steps. f32=True uses the fp32 ring-order
     restatement (bit-exact target for the local group); f32=False the fp64
     restatement of collective.cpp (tolerance target)."""
     offs = np.concatenate([[0], np.cumsum(numels)]).astype(np.int64)
-    w = initial_weights(o, numels, wseed)
-    w = w.astype(np.float32 if f32 else np.float64)
+    w = initial_weights(o, numels, wseed) if w0 is None else w0
+    w = np.array(w, dtype=np.float32 if f32 else np.float64)
     bufs = {}
     plan = bucket_plan(numels, policy, buffer_bytes)
     prescale = (P & (P - 1)) == 0
     for s in range(steps):
-        g = seeded_grads(o, P, numels, s, seed0)
+        g = grads_fn(s) if grads_fn is not None else seeded_grads(o, P, numels, s, seed0)
+        if lr_schedule is not None:
+            lr = lr_schedule[s]
         for lo, hi in plan:
             a, b = offs[lo - 1], offs[hi]
             if b == a:
@@ -67,10 +70,19 @@ def oracle_run(o: Restated, numels, P: int, steps: int, policy: str, buffer_byte
 def run_local(numels, P: int, steps: int, policy: str, buffer_bytes: int, lr: float,
               momentum=0.0, dampening=0.0, weight_decay=0.0, nesterov=False,
               defer_allgather=False, seed0: int = 1000, wseed: int = 77, shadow: bool = False,
-              comm_order=None):
+              comm_order=None, transport: str = "ring", flat: bool = False,
+              zero_copy: bool = True, w0=None, grads_fn=None, lr_schedule=None):
     """Drive P local-group ranks in lock-step through `steps` iterations of
     backward (layers L..1) + step + forward waits. Returns (params [P, D],
-    shadows or None, traces, runtimes-closed)."""
+    shadows or None, traces, runtimes-closed).
+
+    transport="ring": ring-order emulation kernels; "peer": the multi-GPU
+    NVLink peer kernels on one device (each rank on its own stream). flat=True
+    lays every rank's parameters / gradients out as 64-element aligned views
+    of one tensor each (the zero-copy peer layout). w0: initial fp32 weights
+    (default: the seeded generator); grads_fn(step) -> [P, D] fp32 gradients
+    (default: seeded_grads). lr_schedule: per-step learning rates (set_lr
+    before each step's backward)."""
     import torch
 
     from paper_2302_12445_b200 import LocalGroup, Runtime
@@ -79,19 +91,33 @@ def run_local(numels, P: int, steps: int, policy: str, buffer_bytes: int, lr: fl
     dev = torch.device("cuda")
     L = len(numels)
     offs = np.concatenate([[0], np.cumsum(numels)]).astype(np.int64)
-    w0 = initial_weights(o, numels, wseed)
-    group = LocalGroup(P)
+    if w0 is None:
+        w0 = initial_weights(o, numels, wseed)
+    group = LocalGroup(P, transport)
+    peer = transport == "peer"
+    streams = [torch.cuda.Stream() for _ in range(P)] if peer else [None] * P
     rts, params, grads, shadows = [], [], [], []
+    aoffs = [0]
+    for n in numels:
+        aoffs.append(aoffs[-1] + (n + 63) // 64 * 64)
     for r in range(P):
         rt = Runtime(group, r, P, policy=policy, fusion_buffer_bytes=buffer_bytes, lr=lr,
                      momentum=momentum, dampening=dampening, weight_decay=weight_decay,
                      nesterov=nesterov, defer_allgather=defer_allgather,
-                     dear_group_dependency=comm_order is not None)
+                     dear_group_dependency=comm_order is not None, stream=streams[r])
         ps, gs, ss = [], [], []
+        if flat:
+            pflat = torch.zeros(aoffs[-1] + 64, device=dev)
+            gflat = torch.zeros_like(pflat)
         for l in range(1, L + 1):
             a, b = offs[l - 1], offs[l]
-            p = torch.from_numpy(w0[a:b].copy()).to(dev)
-            g = torch.zeros_like(p)
+            src = torch.from_numpy(np.ascontiguousarray(w0[a:b], np.float32)).to(dev)
+            if flat:
+                p = pflat[aoffs[l - 1]:aoffs[l - 1] + (b - a)]
+                p.copy_(src)
+                g = gflat[aoffs[l - 1]:aoffs[l - 1] + (b - a)]
+            else:
+                p, g = src, torch.zeros_like(src)
             sh = torch.zeros(max(b - a, 1), dtype=torch.bfloat16, device=dev) if shadow else None
             rt.register(l, p, g, sh)
             ps.append(p)
@@ -101,24 +127,31 @@ def run_local(numels, P: int, steps: int, policy: str, buffer_bytes: int, lr: fl
         params.append(ps)
         grads.append(gs)
         shadows.append(ss)
+    torch.cuda.synchronize()
     for rt in rts:
         rt.finalize()
         if comm_order is not None:
             rt.set_comm_order(comm_order)
+    if peer:
+        group.connect(zero_copy)
     traces = []
     for s in range(steps):
-        G = seeded_grads(o, P, numels, s, seed0)
+        G = grads_fn(s) if grads_fn is not None else seeded_grads(o, P, numels, s, seed0)
+        if lr_schedule is not None:
+            for rt in rts:
+                rt.set_lr(lr_schedule[s])
         # forward of iteration s: wait for each layer's bucket (flushes AGs)
         for l in range(1, L + 1):
             for r in range(P):
-                rts[r].param_wait(l)
+                rts[r].param_wait(l, streams[r])
         for l in range(L, 0, -1):
             a, b = offs[l - 1], offs[l]
             for r in range(P):
-                grads[r][l - 1].copy_(torch.from_numpy(G[r, a:b].copy()).to(dev))
-                rts[r].grad_ready(l)
+                with torch.cuda.stream(streams[r] or torch.cuda.current_stream()):
+                    grads[r][l - 1].copy_(torch.from_numpy(np.ascontiguousarray(G[r, a:b])).to(dev))
+                rts[r].grad_ready(l, streams[r])
         for r in range(P):
-            rts[r].step()
+            rts[r].step(streams[r])
         traces.append([rt.trace() for rt in rts])
     for rt in rts:
         rt.synchronize()
@@ -130,6 +163,7 @@ def run_local(numels, P: int, steps: int, policy: str, buffer_bytes: int, lr: fl
         sh_out = np.stack([np.concatenate([s[: numels[i]].float().cpu().numpy()
                                            for i, s in enumerate(shadows[r])]) for r in range(P)])
     same = [rt.check_replicas() for rt in rts]
+    run_local.zero_copy = [rt.zero_copy for rt in rts]
     for rt in rts:
         rt.close()
     group.close()

@@ -25,16 +25,3 @@ def test_nccl_parity(case):
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     print(out.stdout[-4000:])
     assert out.returncode == 0, out.stdout[-4000:] + out.stderr[-4000:]
-
-
-def test_peer_parity_copy_engine_allgather():
-    """The zero-copy peer case with the all-gather on the copy engines
-    (DEAR_CE_AG=1, runtime.cpp OP_AG): the same bit-exact checks as `peer`."""
-    n = _nproc()
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr", "127.0.0.1", "--master-port", str(30500 + (os.getpid() % 1000)),
-           os.path.join(HERE, "dist_worker.py"), "peer"]
-    env = dict(os.environ, DEAR_CE_AG="1")
-    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
-    print(out.stdout[-4000:])
-    assert out.returncode == 0, out.stdout[-4000:] + out.stderr[-4000:]
