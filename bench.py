@@ -79,6 +79,12 @@ def parse():
     ap.add_argument("--extra-workload", default="bert_large",
                     help="also measure DeAR vs WFBP on this workload (north-star "
                          "comparison); 'none' to skip")
+    ap.add_argument("--no-parity", action="store_true",
+                    help="skip the post-timing oracle parity check of one bucket")
+    ap.add_argument("--parity-steps", type=int, default=3)
+    ap.add_argument("--no-timeline", action="store_true",
+                    help="skip the post-timing measured-timeline validation")
+    ap.add_argument("--timeline-out", default="", help="write the measured Chrome trace here")
     ap.add_argument("--profile-steps", type=int, default=0,
                     help="only run this many graph replays (for ncu launch lists)")
     return ap.parse_args()
@@ -137,9 +143,11 @@ def peaks():
 
 
 # ------------------------------------------------------------ reference arm --
-def reference_arm(a, wl, world: int, rank: int, emit: bool = True):
+def reference_arm(a, wl, world: int, rank: int, emit: bool = True, threads: int = 0):
     """The reference's own CPU path (oracle/_ref: proj/src/collective.cpp
-    sgd_step per fusion bucket, fp64, P = N virtual workers), all host cores."""
+    sgd_step per fusion bucket, fp64, P = N virtual workers), all host cores
+    (threads = 0) or `threads` threads (1 = the reference's own single-threaded
+    execution)."""
     if rank != 0:
         return None
     import numpy as np
@@ -153,7 +161,7 @@ def reference_arm(a, wl, world: int, rank: int, emit: bool = True):
     plan = fusion_plan([4 * c for c in counts], a.buffer if "FUSED" in a.policy else 0)
     buckets = [sum(counts[lo - 1:hi]) for lo, hi in plan]
     D = sum(buckets)
-    cores = os.cpu_count() or 1
+    cores = threads if threads > 0 else (os.cpu_count() or 1)
     # Bound memory (P replicas + P grads in fp64, ~3x transient) to ~12 GB and
     # the sample to the requested seconds: take whole buckets in plan order.
     cap = int(12e9 / (8 * P * 5))
@@ -481,6 +489,11 @@ def gpu_arm(a, wl, world, rank, local_rank):
     extra = None
     if a.extra_workload != "none" and a.extra_workload != a.workload:
         extra = compare_policies(a, a.extra_workload, comm, world, rank, stream)
+    # Post-timing checks (nothing below is timed): one measured iteration in the
+    # reference's trace schema, validated; oracle parity of one full bucket at
+    # the bench configuration.
+    timeline = None if a.no_timeline else _measured_timeline(a, model, comm, rank, world, stream)
+    parity = None if a.no_parity else _bench_parity(a, model, comm, rank, world, stream)
     if rank != 0:
         return None
     samples = batch * world
@@ -520,8 +533,11 @@ def gpu_arm(a, wl, world, rank, local_rank):
     line = {
         "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": res["dear_ms"],
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-        "data": "synthetic",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        # the DeAR path (params, grads, reduction, update) is fp32 as the north
+        # star requires; the synthetic layer GEMMs compute in bf16
+        "dtype": "fp32", "compute_dtype": "bf16",
+        "data": "synthetic (seeded inputs; random-init params; no dataset)",
         "config": {"workload": wl["config"], "policy": a.policy, "collectives": backend_used,
                    "zero_copy": zero_copy,
                    "dear_group_dependency": bool(a.group_dependency),
@@ -566,9 +582,182 @@ def gpu_arm(a, wl, world, rank, local_rank):
         line["busbw_gbs"] = busbw
     if extra is not None:
         line["north_star"] = extra
+    if parity is not None:
+        line["parity"] = parity
+    if timeline is not None:
+        line["timeline"] = timeline
     if world == 1 and not a.no_cpu:
-        line["cpu_baseline"] = reference_arm(a, wl, world, rank, emit=False)
+        # BASELINE.md §2's plan: the reference's single-threaded execution;
+        # the all-cores figure (each bucket's sgd_step on its own thread) beside it.
+        line["cpu_baseline"] = reference_arm(a, wl, world, rank, emit=False, threads=1)
+        line["cpu_baseline_all_cores"] = reference_arm(a, wl, world, rank, emit=False)
     return line
+
+
+def _measured_timeline(a, model, comm, rank, world, stream):
+    """One iteration in the reference's framing — BP_L..BP_1 then FF_1..FF_L of
+    the next iteration (task_graph.cpp:127-146), with the bucket collectives in
+    between — measured from two consecutive graph replays of the bench step
+    (per-layer compute-stream events + the runtime's comm-stream stamps, all
+    from one base event) and checked with timeline.validate: RS_g after the BP
+    of g's lowest layer (:148-154), FF_l after the all-gather + unpack of
+    g(l) (:207), no overlap on the compute stream (simulate.cpp:161-210)."""
+    import torch
+
+    from paper_2302_12445_b200 import timeline as T
+
+    rt = make_runtime(a, model, comm, rank, world, stream, a.policy, True)
+    L = model.L
+
+    def ev():
+        return torch.cuda.Event(enable_timing=True, external=True)
+    ff = [(ev(), ev()) for _ in range(L)]
+    bp = [(ev(), ev()) for _ in range(L)]
+
+    class Marked(Step):
+        def __call__(self):
+            m, s = self.m, self.s
+            with torch.cuda.stream(s):
+                for l in range(1, L + 1):
+                    rt.param_wait(l, s)
+                    ff[l - 1][0].record(s)
+                    m.forward_layer(l, s)
+                    ff[l - 1][1].record(s)
+                m.zero_grad()
+                for l in range(L, 0, -1):
+                    bp[l - 1][0].record(s)
+                    m.backward_layer(l, s)
+                    bp[l - 1][1].record(s)
+                    rt.grad_ready(l, s)
+                rt.step(s)
+                rt.join(s)
+
+    rt.set_timing(True)
+    run = make_runner(Marked(model, rt, stream), True, stream)
+    for _ in range(3):
+        run()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    run()
+    torch.cuda.synchronize()
+    st_i = rt.timeline(t0)
+    bp_i = [(f"BP l{l}", t0.elapsed_time(bp[l - 1][0]), t0.elapsed_time(bp[l - 1][1]))
+            for l in range(L, 0, -1)]
+    run()
+    torch.cuda.synchronize()
+    st_n = rt.timeline(t0)
+    ff_n = [(f"FF l{l}", t0.elapsed_time(ff[l - 1][0]), t0.elapsed_time(ff[l - 1][1]))
+            for l in range(1, L + 1)]
+    # Reduction side from replay i; an all-gather from replay i when it ran in
+    # that replay's backprop window (WFBP, back-filled DeAR), else from replay
+    # i+1 (deferred into the next forward).
+    bp0 = bp_i[0][1]
+    stamps = []
+    for si, sn in zip(st_i, st_n):
+        s = dict(si)
+        if not (si["ag0"] is not None and si["ag0"] >= bp0):
+            for k in ("ag0", "ag1", "unpack1"):
+                s[k] = sn[k]
+        stamps.append(s)
+    buckets = rt.buckets()
+    rt.set_timing(False)
+    rt.synchronize()
+    rt.close()
+    tl = T.build(bp_i + ff_n, buckets, stamps, a.policy)
+    if rank != 0:
+        return None
+    if a.timeline_out:
+        with open(a.timeline_out, "w") as f:
+            f.write(T.dumps(tl))
+    comm_ev = [e for e in tl["events"] if e["resource"] == "Comm"]
+    # The two replays are separated by a host sync: the iteration is the BP
+    # window of replay i (to its last comm event) plus the FF window of replay
+    # i+1 (from its first comm event), without the gap in between.
+    ff0 = ff_n[0][1]
+    bp_win = max([bp_i[-1][2]] + [e["end"] for e in comm_ev if e["start"] < ff0]) - bp0
+    ff_win = ff_n[-1][2] - min([ff0] + [e["start"] for e in comm_ev if e["start"] >= ff0 - 1e-3])
+    it = bp_win + ff_win
+    return {"framing": "BP of replay i + FF of replay i+1 (the reference's iteration)",
+            "iteration_ms": it, "bp_window_ms": bp_win, "ff_window_ms": ff_win,
+            "ff_ms": tl["ff_ms"], "bp_ms": tl["bp_ms"],
+            "exposed_comm_ms": max(0.0, it - tl["ff_ms"] - tl["bp_ms"]), "compute_events": 2 * L,
+            "comm_events": len(comm_ev), "violations": tl["violations"]}
+
+
+def _bench_parity(a, model, comm, rank, world, stream):
+    """Oracle parity at the bench configuration (a checker, run after all
+    timing): the bench's own runtime (same policy, buffer, backend, kernels)
+    driven for --parity-steps S-SGD steps on seeded inputs (the reference
+    tests' generator: w0 seed 77, rank r's gradients row r of seed 1000+step),
+    then the largest bucket is compared with the oracle's fp32 ring-order
+    restatement (bit-exact expected) and its fp64 sgd_step (collective.cpp:
+    166-194; max relative deviation, tolerance 1e-5)."""
+    import numpy as np
+    import torch
+
+    import paper_2302_12445_b200 as dear
+    from oracle.lib import Restated
+
+    o = Restated()
+    rt = dear.Runtime(comm, rank, world, policy=a.policy, fusion_buffer_bytes=a.buffer,
+                      lr=a.lr, momentum=a.momentum, backend=a.backend, stream=stream)
+    for l in range(1, model.L + 1):
+        rt.register(l, model.params[l - 1], model.grads[l - 1], model.shadows[l - 1])
+    rt.finalize()
+    buckets = rt.buckets()
+    gi = max(range(len(buckets)), key=lambda i: buckets[i]["elems"])
+    lo, hi, d = buckets[gi]["low"], buckets[gi]["high"], buckets[gi]["elems"]
+    layers = list(range(lo, hi + 1))
+    offs = np.cumsum([0] + [model.numels[l - 1] for l in layers])
+    w0 = o.random_vectors_f32(1, d, 77)[0]
+    with torch.cuda.stream(stream):
+        model.params_flat.zero_()
+        for j, l in enumerate(layers):
+            model.params[l - 1].copy_(torch.from_numpy(w0[offs[j]:offs[j + 1]]))
+    torch.cuda.synchronize()
+    P, S = world, a.parity_steps
+    for s in range(S):
+        g = o.random_vectors_f32(P, d, 1000 + s)
+        with torch.cuda.stream(stream):
+            for l in range(1, model.L + 1):
+                rt.param_wait(l, stream)
+            model.grads_flat.zero_()
+            for j, l in enumerate(layers):
+                model.grads[l - 1].copy_(torch.from_numpy(g[rank, offs[j]:offs[j + 1]]))
+            for l in range(model.L, 0, -1):
+                rt.grad_ready(l, stream)
+            rt.step(stream)
+    rt.synchronize()
+    torch.cuda.synchronize()
+    got = torch.cat([model.params[l - 1].detach().float() for l in layers]).cpu().numpy()
+    same = rt.check_replicas()
+    backend, zc = rt.backend, rt.zero_copy
+    rt.close()
+    if rank != 0:
+        return None
+    w32, buf, has = w0.copy(), np.zeros(d, np.float32), False
+    w64 = w0.astype(np.float64)
+    for s in range(S):
+        g = o.random_vectors_f32(P, d, 1000 + s)
+        w32, buf, has = o.sgd_step_f32(w32, buf, has, g, a.lr, a.momentum, 0.0, 0.0, False,
+                                       (P & (P - 1)) == 0)
+        if a.momentum:
+            w64 = None
+        else:
+            w64 = o.sgd_step(w64, g.astype(np.float64), a.lr)
+    rel = None
+    if w64 is not None:
+        rel = float(np.max(np.abs(got - w64) / np.maximum(1.0, np.abs(w64))))
+    return {"bucket": gi + 1, "layers": [lo, hi], "elems": d, "steps": S, "ranks": P,
+            "collectives": backend, "zero_copy": zc,
+            "bit_exact_fp32_ring": bool(np.array_equal(got, w32)),
+            "max_rel_vs_fp64": rel, "tolerance": 1e-5,
+            "within_tolerance": rel is not None and rel <= 1e-5,
+            "replicas_identical": bool(same),
+            "oracle": "oracle/dear_oracle.c sgd_step_f32 (ring order) and sgd_step (fp64)"}
 
 
 def _ncu_traffic(workload):

@@ -13,10 +13,21 @@ from __future__ import annotations
 import json
 
 
+def _first(st: dict, *keys):
+    for k in keys:
+        if st.get(k) is not None:
+            return st[k]
+    return None
+
+
 def build(compute: list[tuple[str, float, float]], buckets: list[dict], stamps: list[dict],
           policy: str) -> dict:
-    """compute: (label, start_ms, end_ms) for "FF l.." / "BP l.." in issue
-    order; buckets: Runtime.buckets(); stamps: Runtime.timeline(base).
+    """compute: (label, start_ms, end_ms) for "BP l.." / "FF l.." in issue
+    order — the reference's iteration is BP_L..BP_1 then FF_1..FF_L
+    (task_graph.cpp:127-146), the feed-forward gated on the all-gathers;
+    buckets: Runtime.buckets(); stamps: Runtime.timeline(base) (the fused
+    peer kernels have no separate update / unpack stamps: the reduce-scatter
+    ends at rs1, the all-gather at ag1).
     Returns {"events": [...], "iteration_ms", "ff_ms", "bp_ms",
     "exposed_comm_ms", "violations": [...]}."""
     dear = policy.startswith("DEAR")
@@ -26,16 +37,17 @@ def build(compute: list[tuple[str, float, float]], buckets: list[dict], stamps: 
         events.append({"label": label, "resource": "Compute", "start": s, "end": e})
     for g, (b, st) in enumerate(zip(buckets, stamps), start=1):
         subj = f"g{g}" if (dear or fused) else f"l{b['high']}"
+        ag_end = _first(st, "unpack1", "ag1")
         if dear:
             if st["pack0"] is not None and st["rs1"] is not None:
                 events.append({"label": f"RS {subj}", "resource": "Comm", "start": st["pack0"],
                                "end": st["rs1"]})
-            if st["ag0"] is not None and st["unpack1"] is not None:
+            if st["ag0"] is not None and ag_end is not None:
                 events.append({"label": f"AG {subj}", "resource": "Comm", "start": st["ag0"],
-                               "end": st["unpack1"]})
-        elif st["pack0"] is not None and st["unpack1"] is not None:
+                               "end": ag_end})
+        elif st["pack0"] is not None and ag_end is not None:
             events.append({"label": f"AR {subj}", "resource": "Comm", "start": st["pack0"],
-                           "end": st["unpack1"]})
+                           "end": ag_end})
         for name, a, z in (("PACK", "pack0", "pack1"), ("UPDATE", "rs1", "update1"),
                            ("UNPACK", "ag1", "unpack1")):
             if st[a] is not None and st[z] is not None:
@@ -67,10 +79,19 @@ def validate(compute, buckets, stamps, policy: str, tol_ms: float = 1e-3) -> lis
         prev_end = e
     bp_end = {int(l.split("l")[1]): e for l, _, e in compute if l.startswith("BP")}
     ff_start = {int(l.split("l")[1]): s for l, s, _ in compute if l.startswith("FF")}
+    kind = "AG" if policy.startswith("DEAR") else "AR"
     for g, (b, st) in enumerate(zip(buckets, stamps), start=1):
         low = b["low"]
         if st["pack0"] is not None and low in bp_end and st["pack0"] < bp_end[low] - tol_ms:
             bad.append(f"bucket g{g}: reduction starts before BP l{low} ends")
+        # FF_l <- AG_{g(l)} (DeAR) / AR_{g(l)} (WFBP), the parameters' last
+        # writer being the all-gather's unpack (task_graph.cpp:170-171, :207)
+        ag_end = _first(st, "unpack1", "ag1")
+        if ag_end is None:
+            continue
+        for l in range(b["low"], b["high"] + 1):
+            if l in ff_start and ff_start[l] < ag_end - tol_ms:
+                bad.append(f"FF l{l} starts before {kind} g{g} (+ unpack) ends")
     return bad
 
 
