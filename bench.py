@@ -655,13 +655,18 @@ def _measured_timeline(a, model, comm, rank, world, stream):
     # that replay's backprop window (WFBP, back-filled DeAR), else from replay
     # i+1 (deferred into the next forward).
     bp0 = bp_i[0][1]
-    stamps = []
+    stamps, ends_i, starts_n = [], [], []
     for si, sn in zip(st_i, st_n):
         s = dict(si)
         if not (si["ag0"] is not None and si["ag0"] >= bp0):
             for k in ("ag0", "ag1", "unpack1"):
                 s[k] = sn[k]
+            if sn["ag0"] is not None:
+                starts_n.append(sn["ag0"])
         stamps.append(s)
+        ends_i += [v for k, v in s.items() if v is not None and k in ("pack1", "rs1", "update1")]
+        if si["ag0"] is not None and si["ag0"] >= bp0:
+            ends_i += [v for v in (si["ag1"], si["unpack1"]) if v is not None]
     buckets = rt.buckets()
     rt.set_timing(False)
     rt.synchronize()
@@ -676,9 +681,8 @@ def _measured_timeline(a, model, comm, rank, world, stream):
     # The two replays are separated by a host sync: the iteration is the BP
     # window of replay i (to its last comm event) plus the FF window of replay
     # i+1 (from its first comm event), without the gap in between.
-    ff0 = ff_n[0][1]
-    bp_win = max([bp_i[-1][2]] + [e["end"] for e in comm_ev if e["start"] < ff0]) - bp0
-    ff_win = ff_n[-1][2] - min([ff0] + [e["start"] for e in comm_ev if e["start"] >= ff0 - 1e-3])
+    bp_win = max([bp_i[-1][2]] + ends_i) - bp0
+    ff_win = ff_n[-1][2] - min([ff_n[0][1]] + starts_n)
     it = bp_win + ff_win
     return {"framing": "BP of replay i + FF of replay i+1 (the reference's iteration)",
             "iteration_ms": it, "bp_window_ms": bp_win, "ff_window_ms": ff_win,
