@@ -94,15 +94,15 @@ int dear_comm_destroy(void* comm);
 int dear_local_group_create(int32_t P, dear_local_group** group);
 int dear_local_group_destroy(dear_local_group* group);
 
-/* Local-group transports. RING: the ranks' ops are queued and the group runs
- * each collective once every rank reached it, as ring-order kernels over all
- * ranks' buffers (collective.cpp:59-152). PEER: the contexts behave like one
- * process per GPU on the NVLink peer backend — the SAME fused kernels
- * (zero-copy or slot RS+update, AG), with the other ranks' memory addressed by
- * in-process deltas instead of IPC mappings — so a one-GPU box runs the
- * multi-GPU data path. Every rank's spinning peer kernel must be resident at
- * once, so each takes at most SMs/P CTAs; ranks need distinct compute streams
- * (a rank's dear_step fence waits on the other ranks' reduce-scatters). */
+/* Local-group transports (P ranks as contexts of ONE process on ONE device,
+ * driven in lock-step; each rank's ops queue, and a collective runs once every
+ * rank reached it). RING: ring-order kernels over all ranks' buffers
+ * (collective.cpp:59-152). PEER: the multi-GPU NVLink peer kernels themselves
+ * (zero-copy or slot reduce-scatter + update, all-gather) with the other
+ * ranks' memory addressed by in-process deltas instead of IPC mappings — a
+ * one-GPU box runs the N > 1 data path. Their cross-rank counter waits stay
+ * inside ONE cooperative launch holding every rank's CTAs, so no kernel ever
+ * waits on another launch. */
 #define DEAR_LOCAL_RING 0
 #define DEAR_LOCAL_PEER 1
 int dear_local_group_create_ex(int32_t P, int32_t transport, dear_local_group** group);

@@ -132,8 +132,6 @@ struct PeerArgs {
   int32_t P;
   int32_t rank;
   long long spin_limit;  // clock64 cycles a cross-GPU wait may spin before __trap (0: forever)
-  int32_t grid;          // > 0: cap on the peer kernels' grid (same-device peer group)
-  int32_t pad;
 };
 struct BucketFlags {
   uint32_t packed;
@@ -183,6 +181,27 @@ cudaError_t launch_rs_update_zc(const Unit* units, const Slice* slices, const Hy
 
 // hp->lr = lr, stream-ordered (dear_set_lr; graph-capturable).
 cudaError_t launch_set_lr(HyperParams* hp, float lr, cudaStream_t s);
+
+// Same-device peer group (LocalGroup "peer"): one rank's arguments of a peer
+// kernel. The group runs each reduce-scatter / all-gather as ONE cooperative
+// launch holding every rank's CTAs (nb per rank), so the kernels' cross-rank
+// waits are between co-resident CTAs of one grid.
+struct GroupOp {
+  const Unit* units;
+  const Slice* slices;
+  const HyperParams* hp;
+  float* mom;          // zero-copy RS: the bucket's momentum shard (or null)
+  BucketFlags* flags;
+  PeerArgs pa;         // arena deltas (counters, slot buffers)
+  PeerArgs sa;         // zero-copy RS: gradient deltas; AG: source deltas
+  int32_t n_slices;
+  int32_t pad;
+};
+cudaError_t launch_group_rs_zc(const GroupOp* ops, int P, int nb, int has_buf, int use_momentum,
+                               int use_wd, int with_shadow, cudaStream_t s);
+cudaError_t launch_group_rs_peer(const GroupOp* ops, int P, int nb, int has_buf,
+                                 int use_momentum, int use_wd, cudaStream_t s);
+cudaError_t launch_group_ag(const GroupOp* ops, int P, int nb, int with_shadow, cudaStream_t s);
 
 // Order-independent 64-bit hash of float bit patterns (sum of mixed words),
 // accumulated into *acc with atomics. Used by dear_check_replicas.

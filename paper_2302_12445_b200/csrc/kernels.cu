@@ -224,13 +224,24 @@ __device__ __forceinline__ void walk_one(const Unit* __restrict__ units, const S
   }
 }
 
-// Each CTA walks slices blockIdx.x, blockIdx.x + gridDim.x, ... of the op's
-// n_slices equal slices (one slice per CTA at the full grid).
+// A CTA's place in the grid of ONE rank's kernel: (blockIdx.x, gridDim.x) for
+// a normal launch; in a same-device group launch (all ranks' CTAs in one
+// cooperative grid) the index within its rank's share.
+struct Blk {
+  int id;
+  int n;
+};
+__device__ __forceinline__ Blk this_blk() {
+  return Blk{static_cast<int>(blockIdx.x), static_cast<int>(gridDim.x)};
+}
+
+// Each CTA walks slices b.id, b.id + b.n, ... of the op's n_slices equal
+// slices (one slice per CTA at the full grid).
 template <typename F>
 __device__ __forceinline__ void walk_slice(const Unit* __restrict__ units,
                                            const Slice* __restrict__ slices, int n_slices,
-                                           F&& f) {
-  for (int i = blockIdx.x; i < n_slices; i += gridDim.x) walk_one(units, slices[i], f);
+                                           F&& f, Blk b = this_blk()) {
+  for (int i = b.id; i < n_slices; i += b.n) walk_one(units, slices[i], f);
 }
 
 // ------------------------------------------------------ peer signalling ----
@@ -251,7 +262,8 @@ __device__ __forceinline__ const T* at_peer(const T* p, int64_t delta) {
 // last CTA, which observed every increment, then releases at system scope,
 // which is cumulative over what it observed (PTX memory model), so one
 // system-scope fence per launch suffices.
-__device__ __forceinline__ void signal_done(uint32_t* done, uint32_t* counter) {
+__device__ __forceinline__ void signal_done(uint32_t* done, uint32_t* counter,
+                                            Blk b = this_blk()) {
   __syncthreads();
   if (threadIdx.x == 0) {
 #ifdef DEAR_SIGNAL_SYS_FENCE_ALL
@@ -260,7 +272,7 @@ __device__ __forceinline__ void signal_done(uint32_t* done, uint32_t* counter) {
     __threadfence();
 #endif
     const uint32_t prev = atomicAdd(done, 1u);
-    if (prev == gridDim.x - 1) {
+    if (prev == static_cast<uint32_t>(b.n) - 1) {
       *done = 0;
       __threadfence_system();
       atomicAdd_system(counter, 1u);
@@ -534,10 +546,11 @@ __device__ __forceinline__ void warp_stream_rs(const float* w_floor, const float
 // One CTA per SM at most (kPeerSlices CTAs): registers for the in-flight
 // peer loads instead of occupancy.
 template <int PC, bool kMom, bool kWd>
-__global__ void __launch_bounds__(kThreads, 1)
-    rs_update_peer_kernel(const Unit* __restrict__ units, const Slice* __restrict__ slices,
-                          const HyperParams* __restrict__ hpp, int has_buf, PeerArgs pa,
-                          BucketFlags* flags) {
+__device__ __forceinline__ void rs_update_peer_body(const Unit* __restrict__ units,
+                                                    const Slice* __restrict__ slices,
+                                                    const HyperParams* __restrict__ hpp,
+                                                    int has_buf, const PeerArgs& pa,
+                                                    BucketFlags* flags, Blk blk) {
   cta_wait_peers(&flags->packed, &flags->packed, pa);  // every rank packed this bucket
   const HyperParams hp = *hpp;
   const int k0 = (pa.rank + 1) % pa.P;
@@ -627,8 +640,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           reinterpret_cast<float4*>(g + head)[q] = acc;
           if (kMom) reinterpret_cast<float4*>(mom + head)[q] = mv;
         });
-  });
-  signal_done(&flags->done[1], &flags->updated);
+  }, blk);
+  signal_done(&flags->done[1], &flags->updated, blk);
+}
+
+template <int PC, bool kMom, bool kWd>
+__global__ void __launch_bounds__(kThreads, 1)
+    rs_update_peer_kernel(const Unit* __restrict__ units, const Slice* __restrict__ slices,
+                          const HyperParams* __restrict__ hpp, int has_buf, PeerArgs pa,
+                          BucketFlags* flags) {
+  rs_update_peer_body<PC, kMom, kWd>(units, slices, hpp, has_buf, pa, flags, this_blk());
 }
 
 // ------------------------------------- zero-copy peer RS+update ----------
@@ -650,9 +671,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 // `packed` reached our `updated` + 1 — `updated` only moves when this kernel's
 // last CTA finishes, after every CTA passed its wait, so it is this
 // iteration's epoch on every rank.
-__device__ __forceinline__ void cta_announce_and_wait(BucketFlags* flags, const PeerArgs& pa) {
+__device__ __forceinline__ void cta_announce_and_wait(BucketFlags* flags, const PeerArgs& pa,
+                                                      Blk b) {
   if (threadIdx.x < 32) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (b.id == 0 && threadIdx.x == 0) {
       __threadfence_system();
       atomicAdd_system(&flags->packed, 1u);
     }
@@ -712,11 +734,12 @@ __device__ __forceinline__ void store_bf16x4(__nv_bfloat16* sh, int64_t q, float
 #define ZC_ST(p, v) (*(p) = (v))
 #endif
 template <int PC, bool kMom, bool kWd, bool kShadow>
-__global__ void DEAR_ZC_BOUNDS
-    rs_update_zc_kernel(const Unit* __restrict__ units, const Slice* __restrict__ slices,
-                        const HyperParams* __restrict__ hpp, int has_buf, float* mom_base,
-                        PeerArgs pa, PeerArgs ga, BucketFlags* flags) {
-  cta_announce_and_wait(flags, pa);
+__device__ __forceinline__ void rs_update_zc_body(const Unit* __restrict__ units,
+                                                  const Slice* __restrict__ slices,
+                                                  const HyperParams* __restrict__ hpp, int has_buf,
+                                                  float* mom_base, const PeerArgs& pa,
+                                                  const PeerArgs& ga, BucketFlags* flags, Blk blk) {
+  cta_announce_and_wait(flags, pa, blk);
   const HyperParams hp = *hpp;
   const int P = PC > 0 ? PC : pa.P;
   const int k0 = (pa.rank + 1) % P;
@@ -811,17 +834,27 @@ __global__ void DEAR_ZC_BOUNDS
         for (int e = 0; e < 4; ++e) scalar(head + 4 * q + e);
     }
     for (int64_t i = head + n4 * 4 + threadIdx.x; i < n; i += kThreads) scalar(i);
-  });
-  signal_done(&flags->done[1], &flags->updated);
+  }, blk);
+  signal_done(&flags->done[1], &flags->updated, blk);
+}
+
+template <int PC, bool kMom, bool kWd, bool kShadow>
+__global__ void DEAR_ZC_BOUNDS
+    rs_update_zc_kernel(const Unit* __restrict__ units, const Slice* __restrict__ slices,
+                        const HyperParams* __restrict__ hpp, int has_buf, float* mom_base,
+                        PeerArgs pa, PeerArgs ga, BucketFlags* flags) {
+  rs_update_zc_body<PC, kMom, kWd, kShadow>(units, slices, hpp, has_buf, mom_base, pa, ga, flags,
+                                            this_blk());
 }
 
 // ------------------------------------------- fused peer AG+unpack ---------
 // Source element of a unit: U.a + off on rank U.peer, i.e. at sa.delta[U.peer]
 // (sa = arena deltas for bucket slots, parameter deltas for zero-copy).
 template <bool kShadow>
-__global__ void DEAR_ZC_BOUNDS
-    ag_unpack_peer_kernel(const Unit* __restrict__ units, const Slice* __restrict__ slices,
-                          PeerArgs pa, PeerArgs sa, BucketFlags* flags, int n_slices) {
+__device__ __forceinline__ void ag_unpack_peer_body(const Unit* __restrict__ units,
+                                                    const Slice* __restrict__ slices,
+                                                    const PeerArgs& pa, const PeerArgs& sa,
+                                                    BucketFlags* flags, int n_slices, Blk blk) {
   cta_wait_peers(&flags->updated, &flags->updated, pa);  // every owner updated its shard
   walk_slice(units, slices, n_slices, [&](const Unit& U, int64_t off, int64_t n) {
     const float* src = at_peer(U.a + off, sa.delta[U.peer]);
@@ -838,8 +871,42 @@ __global__ void DEAR_ZC_BOUNDS
           ZC_ST(reinterpret_cast<float4*>(dst + head) + q, v);
           if (kShadow && sh) store_bf16x4(sh + head, q, v);
         });
-  });
-  signal_done(&flags->done[2], &flags->gathered);
+  }, blk);
+  signal_done(&flags->done[2], &flags->gathered, blk);
+}
+
+template <bool kShadow>
+__global__ void DEAR_ZC_BOUNDS
+    ag_unpack_peer_kernel(const Unit* __restrict__ units, const Slice* __restrict__ slices,
+                          PeerArgs pa, PeerArgs sa, BucketFlags* flags, int n_slices) {
+  ag_unpack_peer_body<kShadow>(units, slices, pa, sa, flags, n_slices, this_blk());
+}
+
+// ------------------------------------- same-device group launches ---------
+// All P ranks' CTAs of one peer kernel in ONE cooperative grid (rank =
+// blockIdx.x / nb): the cross-rank counter waits inside are then between
+// CTAs that are guaranteed co-resident, never between separate launches.
+template <int PC, bool kMom, bool kWd, bool kShadow>
+__global__ void DEAR_ZC_BOUNDS group_rs_zc_kernel(const GroupOp* __restrict__ ops, int nb,
+                                                  int has_buf) {
+  const GroupOp& o = ops[blockIdx.x / nb];
+  rs_update_zc_body<PC, kMom, kWd, kShadow>(o.units, o.slices, o.hp, has_buf, o.mom, o.pa, o.sa,
+                                            o.flags, Blk{static_cast<int>(blockIdx.x) % nb, nb});
+}
+
+template <int PC, bool kMom, bool kWd>
+__global__ void __launch_bounds__(kThreads, 1) group_rs_peer_kernel(const GroupOp* __restrict__ ops,
+                                                                    int nb, int has_buf) {
+  const GroupOp& o = ops[blockIdx.x / nb];
+  rs_update_peer_body<PC, kMom, kWd>(o.units, o.slices, o.hp, has_buf, o.pa, o.flags,
+                                     Blk{static_cast<int>(blockIdx.x) % nb, nb});
+}
+
+template <bool kShadow>
+__global__ void DEAR_ZC_BOUNDS group_ag_kernel(const GroupOp* __restrict__ ops, int nb) {
+  const GroupOp& o = ops[blockIdx.x / nb];
+  ag_unpack_peer_body<kShadow>(o.units, o.slices, o.pa, o.sa, o.flags, o.n_slices,
+                               Blk{static_cast<int>(blockIdx.x) % nb, nb});
 }
 
 // ---------------------------------------------------- local collectives ----
@@ -906,13 +973,6 @@ int bucket_grid(int n_slices, int want = 0) {
   return g > 0 && g < n_slices ? g : n_slices;
 }
 
-// Peer kernels: pa.grid (> 0) caps the grid — the same-device peer group runs
-// P ranks' spinning kernels on one GPU, which must all be resident at once.
-int peer_grid(int n_slices, const PeerArgs& pa) {
-  const int g = bucket_grid(n_slices);
-  return pa.grid > 0 && pa.grid < g ? pa.grid : g;
-}
-
 }  // namespace
 
 cudaError_t launch_pack(const Unit* units, const Slice* slices, int64_t total, float scale,
@@ -927,10 +987,10 @@ cudaError_t launch_pack_signal(const Unit* units, const Slice* slices, int64_t t
                                BucketFlags* flags, const PeerArgs& pa, cudaStream_t s) {
   (void)total;  // the signal must fire even for an empty bucket
   if (kPeerPackLight)
-    pack_kernel<true><<<peer_grid(kPackPeerSlices, pa), kThreads, 0, s>>>(units, slices, scale, flags,
+    pack_kernel<true><<<bucket_grid(kPackPeerSlices), kThreads, 0, s>>>(units, slices, scale, flags,
                                                                        pa, kPackPeerSlices);
   else
-    pack_kernel<true><<<peer_grid(kSlices, pa), kThreads, 0, s>>>(units, slices, scale, flags, pa,
+    pack_kernel<true><<<bucket_grid(kSlices), kThreads, 0, s>>>(units, slices, scale, flags, pa,
                                                                 kSlices);
   return cudaGetLastError();
 }
@@ -945,7 +1005,7 @@ template <int PC>
 void launch_rs_update_peer_p(const Unit* units, const Slice* slices, const HyperParams* hp,
                              int has_momentum_buf, int use_momentum, int use_wd,
                              const PeerArgs& pa, BucketFlags* flags, cudaStream_t s) {
-  const int grid = peer_grid(kPeerSlices, pa);
+  const int grid = bucket_grid(kPeerSlices);
   if (use_momentum && use_wd)
     rs_update_peer_kernel<PC, true, true><<<grid, kThreads, 0, s>>>(units, slices, hp, has_momentum_buf, pa, flags);
   else if (use_momentum)
@@ -976,9 +1036,9 @@ cudaError_t launch_ag_unpack_peer(const Unit* units, const Slice* slices, int64_
   (void)total;
   const size_t smem = 0;
   if (with_shadow)
-    ag_unpack_peer_kernel<true><<<peer_grid(n_slices, pa), kThreads, smem, s>>>(units, slices, pa, sa, flags, n_slices);
+    ag_unpack_peer_kernel<true><<<bucket_grid(n_slices), kThreads, smem, s>>>(units, slices, pa, sa, flags, n_slices);
   else
-    ag_unpack_peer_kernel<false><<<peer_grid(n_slices, pa), kThreads, smem, s>>>(units, slices, pa, sa, flags, n_slices);
+    ag_unpack_peer_kernel<false><<<bucket_grid(n_slices), kThreads, smem, s>>>(units, slices, pa, sa, flags, n_slices);
   return cudaGetLastError();
 }
 
@@ -986,7 +1046,7 @@ template <int PC, bool kMom, bool kWd>
 void launch_rs_zc_p(const Unit* units, const Slice* slices, const HyperParams* hp, int has_buf,
                     float* mom_base, int with_shadow, const PeerArgs& pa, const PeerArgs& ga,
                     BucketFlags* flags, cudaStream_t s) {
-  const int grid = peer_grid(kZcSlices, pa);
+  const int grid = bucket_grid(kZcSlices);
   const size_t smem = 0;
   if (with_shadow)
     rs_update_zc_kernel<PC, kMom, kWd, true><<<grid, kThreads, smem, s>>>(units, slices, hp, has_buf,
@@ -1021,6 +1081,65 @@ cudaError_t launch_rs_update_zc(const Unit* units, const Slice* slices, const Hy
     default: launch_rs_zc_pc<0>(units, slices, hp, has_momentum_buf, mom_base, use_momentum, use_wd, with_shadow, pa, ga, flags, s); break;
   }
   return cudaGetLastError();
+}
+
+namespace {
+template <typename... KArgs, typename... Args>
+cudaError_t coop(void (*k)(KArgs...), int grid, cudaStream_t s, Args... args) {
+  void* pv[] = {static_cast<void*>(&args)...};
+  return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k), dim3(grid), dim3(kThreads),
+                                     pv, 0, s);
+}
+
+template <int PC, bool kMom, bool kWd>
+cudaError_t group_rs_zc_p(const GroupOp* ops, int P, int nb, int has_buf, int shadow,
+                          cudaStream_t s) {
+  if (shadow) return coop(group_rs_zc_kernel<PC, kMom, kWd, true>, P * nb, s, ops, nb, has_buf);
+  return coop(group_rs_zc_kernel<PC, kMom, kWd, false>, P * nb, s, ops, nb, has_buf);
+}
+
+template <int PC>
+cudaError_t group_rs_zc_pc(const GroupOp* ops, int P, int nb, int has_buf, int mom, int wd,
+                           int shadow, cudaStream_t s) {
+  if (mom && wd) return group_rs_zc_p<PC, true, true>(ops, P, nb, has_buf, shadow, s);
+  if (mom) return group_rs_zc_p<PC, true, false>(ops, P, nb, has_buf, shadow, s);
+  if (wd) return group_rs_zc_p<PC, false, true>(ops, P, nb, has_buf, shadow, s);
+  return group_rs_zc_p<PC, false, false>(ops, P, nb, has_buf, shadow, s);
+}
+
+template <int PC>
+cudaError_t group_rs_peer_pc(const GroupOp* ops, int P, int nb, int has_buf, int mom, int wd,
+                             cudaStream_t s) {
+  if (mom && wd) return coop(group_rs_peer_kernel<PC, true, true>, P * nb, s, ops, nb, has_buf);
+  if (mom) return coop(group_rs_peer_kernel<PC, true, false>, P * nb, s, ops, nb, has_buf);
+  if (wd) return coop(group_rs_peer_kernel<PC, false, true>, P * nb, s, ops, nb, has_buf);
+  return coop(group_rs_peer_kernel<PC, false, false>, P * nb, s, ops, nb, has_buf);
+}
+}  // namespace
+
+cudaError_t launch_group_rs_zc(const GroupOp* ops, int P, int nb, int has_buf, int use_momentum,
+                               int use_wd, int with_shadow, cudaStream_t s) {
+  switch (P) {
+    case 2: return group_rs_zc_pc<2>(ops, P, nb, has_buf, use_momentum, use_wd, with_shadow, s);
+    case 4: return group_rs_zc_pc<4>(ops, P, nb, has_buf, use_momentum, use_wd, with_shadow, s);
+    case 8: return group_rs_zc_pc<8>(ops, P, nb, has_buf, use_momentum, use_wd, with_shadow, s);
+    default: return group_rs_zc_pc<0>(ops, P, nb, has_buf, use_momentum, use_wd, with_shadow, s);
+  }
+}
+
+cudaError_t launch_group_rs_peer(const GroupOp* ops, int P, int nb, int has_buf,
+                                 int use_momentum, int use_wd, cudaStream_t s) {
+  switch (P) {
+    case 2: return group_rs_peer_pc<2>(ops, P, nb, has_buf, use_momentum, use_wd, s);
+    case 4: return group_rs_peer_pc<4>(ops, P, nb, has_buf, use_momentum, use_wd, s);
+    case 8: return group_rs_peer_pc<8>(ops, P, nb, has_buf, use_momentum, use_wd, s);
+    default: return group_rs_peer_pc<0>(ops, P, nb, has_buf, use_momentum, use_wd, s);
+  }
+}
+
+cudaError_t launch_group_ag(const GroupOp* ops, int P, int nb, int with_shadow, cudaStream_t s) {
+  if (with_shadow) return coop(group_ag_kernel<true>, P * nb, s, ops, nb);
+  return coop(group_ag_kernel<false>, P * nb, s, ops, nb);
 }
 
 cudaError_t launch_update(const Unit* units, const Slice* slices, int64_t total,

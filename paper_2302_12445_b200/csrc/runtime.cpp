@@ -134,6 +134,11 @@ using namespace dear;
 struct dear_local_group {
   int P = 0;
   int transport = DEAR_LOCAL_RING;
+  // PEER transport: per bucket, the P ranks' GroupOp records of its
+  // reduce-scatter and all-gather kernels (device), nb CTAs per rank.
+  GroupOp* ops_dev = nullptr;
+  int nb = 0;
+  bool connected = false;
   std::vector<dear_ctx*> ranks;
   std::map<int, float**> bufs_dev;  // bucket -> device array of P buffers
   cudaEvent_t arrive[64] = {};
@@ -260,6 +265,7 @@ int64_t set_starts(std::vector<Unit>& u, size_t first) {
 }  // namespace
 
 dear_local_group::~dear_local_group() {
+  if (ops_dev) cudaFree(ops_dev);
   for (auto& kv : bufs_dev) cudaFree(kv.second);
   for (cudaEvent_t e : arrive)
     if (e) cudaEventDestroy(e);
@@ -269,6 +275,36 @@ dear_local_group::~dear_local_group() {
 void dear_local_group::run_collective(const Op& op) {
   dear_ctx* c0 = ranks[0];
   const Bucket& B0 = c0->buckets[static_cast<size_t>(op.bucket)];
+  if (transport == DEAR_LOCAL_PEER) {
+    // Every rank's comm stream reached this collective: ONE cooperative launch
+    // of the peer kernel over all ranks' data on rank 0's comm stream.
+    if (!connected) invalid("local group: call dear_local_group_connect before the first step");
+    for (int r = 0; r < P; ++r) {
+      if (!arrive[r]) arrive[r] = new_event(false);
+      cuda_check(cudaEventRecord(arrive[r], ranks[static_cast<size_t>(r)]->comm_stream), "cudaEventRecord");
+      cuda_check(cudaStreamWaitEvent(c0->comm_stream, arrive[r], 0), "cudaStreamWaitEvent");
+    }
+    const GroupOp* ops = ops_dev + (static_cast<size_t>(op.bucket) * 2 + (op.kind == OP_AG ? 1 : 0)) *
+                                       static_cast<size_t>(P);
+    const dear_cfg& cf = c0->cfg;
+    if (op.kind == OP_RS) {
+      cuda_check(c0->zc ? launch_group_rs_zc(ops, P, nb, B0.mom_init ? 1 : 0, cf.momentum != 0.0,
+                                             cf.weight_decay != 0.0, B0.any_shadow ? 1 : 0,
+                                             c0->comm_stream)
+                        : launch_group_rs_peer(ops, P, nb, B0.mom_init ? 1 : 0,
+                                               cf.momentum != 0.0, cf.weight_decay != 0.0,
+                                               c0->comm_stream),
+                 "group reduce-scatter kernel");
+    } else {
+      cuda_check(launch_group_ag(ops, P, nb, B0.any_shadow ? 1 : 0, c0->comm_stream),
+                 "group all-gather kernel");
+    }
+    if (!done) done = new_event(false);
+    cuda_check(cudaEventRecord(done, c0->comm_stream), "cudaEventRecord");
+    for (int r = 1; r < P; ++r)
+      cuda_check(cudaStreamWaitEvent(ranks[static_cast<size_t>(r)]->comm_stream, done, 0), "cudaStreamWaitEvent");
+    return;
+  }
   auto it = bufs_dev.find(op.bucket);
   if (it == bufs_dev.end()) {
     std::vector<float*> h(static_cast<size_t>(P));
@@ -433,7 +469,10 @@ void dear_ctx::exec(const Op& op) {
       record_t(op.bucket, T_PACK1);
       break;
     case OP_RS:
-      if (zc) {
+      if (local && same_dev) {
+        // The group already ran every rank's reduce-scatter (run_collective).
+        if (cfg.momentum != 0.0) B->mom_init = true;
+      } else if (zc) {
         cuda_check(launch_rs_update_zc(B->zrs_u, B->zrs_ps, hp_dev, B->mom_init ? 1 : 0, B->mom,
                                        cfg.momentum != 0.0, cfg.weight_decay != 0.0,
                                        B->any_shadow ? 1 : 0, pa, ga, B->flags, comm_stream),
@@ -474,7 +513,9 @@ void dear_ctx::exec(const Op& op) {
       break;
     case OP_AG:
       if (!local) record_t(op.bucket, T_AG0);
-      if (zc) {
+      if (local && same_dev) {
+        // run by the group (run_collective)
+      } else if (zc) {
         // Each owner's updated parameters, read over NVLink into ours.
         cuda_check(launch_ag_unpack_peer(B->zag_u, B->zag_ps, B->e_zag, B->any_shadow ? 1 : 0,
                                          pa, qa, B->flags, kZcSlices, comm_stream),
@@ -724,9 +765,10 @@ int dear_create_local(dear_local_group* group, int32_t rank, void* compute_strea
   if (group->ranks[static_cast<size_t>(rank)]) invalid("dear_create_local: rank already created");
   std::unique_ptr<dear_ctx> c(new dear_ctx());
   create_common(c.get(), rank, group->P, compute_stream, cfg);
-  // Ring transport: ops queue and the group drains them in lock-step. Peer
-  // transport: ops execute at once, like one process per GPU.
-  c->local = group->transport == DEAR_LOCAL_RING;
+  // Ops queue and the group drains them in lock-step; a collective runs once
+  // every rank reached it (ring kernels, or the peer kernels as one
+  // cooperative group launch).
+  c->local = true;
   c->same_dev = group->transport == DEAR_LOCAL_PEER;
   c->group = group;
   group->ranks[static_cast<size_t>(rank)] = c.get();
@@ -826,7 +868,7 @@ int dear_finalize(dear_ctx* ctx) {
   const char* dir_env = std::getenv("DEAR_DIRECT");
   c.direct = c.P == 1 && !c.peer && c.cfg.momentum == 0.0 && !(dir_env && dir_env[0] == '0');
   // Zero-copy tables for a later dear_peer_connect (multi-process only).
-  c.zc_tables = !c.local && c.P > 1;
+  c.zc_tables = (!c.local || c.same_dev) && c.P > 1;
   // Unit tables.
   std::vector<Unit> host_units;
   struct Span { size_t pack, upd, unpack; };
@@ -1315,7 +1357,6 @@ long long peer_spin_limit(int device) {
 void enable_peer(dear_ctx& c, PeerArgs pa, PeerArgs ga, PeerArgs qa, bool zc) {
   pa.spin_limit = peer_spin_limit(c.device);
   ga.spin_limit = qa.spin_limit = pa.spin_limit;
-  ga.grid = qa.grid = pa.grid;
   c.pa = pa;
   c.ga = ga;
   c.qa = qa;
@@ -1362,9 +1403,6 @@ int dear_local_group_connect(dear_local_group* group, int32_t allow_zero_copy) {
     PeerArgs pa{}, ga{}, qa{};
     pa.P = ga.P = qa.P = P;
     pa.rank = ga.rank = qa.rank = r;
-    // Every rank's spinning peer kernel must be resident at once on the one
-    // device: a grid of sms / P CTAs each (at most one per SM and rank).
-    pa.grid = std::max(1, sms / P);
     for (int k = 0; k < P; ++k) {
       const dear_ctx& o = *group->ranks[static_cast<size_t>(k)];
       pa.delta[k] = static_cast<int64_t>(o.arena - c.arena);
@@ -1375,6 +1413,38 @@ int dear_local_group_connect(dear_local_group* group, int32_t allow_zero_copy) {
     }
     enable_peer(c, pa, ga, qa, zc);
   }
+  // The group launch records: per bucket, [RS: P ranks][AG: P ranks]. One
+  // cooperative grid of P x nb CTAs (one per SM in total) runs all ranks.
+  const size_t G = group->ranks[0]->buckets.size();
+  std::vector<GroupOp> ops(G * 2 * static_cast<size_t>(P));
+  for (size_t g = 0; g < G; ++g) {
+    for (int r = 0; r < P; ++r) {
+      const dear_ctx& c = *group->ranks[static_cast<size_t>(r)];
+      const Bucket& B = c.buckets[g];
+      GroupOp& rs = ops[(g * 2) * static_cast<size_t>(P) + static_cast<size_t>(r)];
+      GroupOp& ag = ops[(g * 2 + 1) * static_cast<size_t>(P) + static_cast<size_t>(r)];
+      rs.hp = ag.hp = c.hp_dev;
+      rs.flags = ag.flags = B.flags;
+      rs.pa = ag.pa = c.pa;
+      if (c.zc) {
+        rs.units = B.zrs_u, rs.slices = B.zrs_ps, rs.mom = B.mom, rs.sa = c.ga;
+        rs.n_slices = kZcSlices;
+        ag.units = B.zag_u, ag.slices = B.zag_ps, ag.sa = c.qa, ag.n_slices = kZcSlices;
+      } else {
+        rs.units = B.upd_u, rs.slices = B.upd_ps, rs.sa = c.pa, rs.n_slices = kPeerSlices;
+        ag.units = B.unpack_u, ag.slices = B.unpack_ps, ag.sa = c.pa, ag.n_slices = kPeerSlices;
+      }
+    }
+  }
+  if (group->ops_dev) cudaFree(group->ops_dev);
+  group->ops_dev = nullptr;
+  if (!ops.empty()) {
+    cuda_check(cudaMalloc(&group->ops_dev, ops.size() * sizeof(GroupOp)), "cudaMalloc(group ops)");
+    cuda_check(cudaMemcpy(group->ops_dev, ops.data(), ops.size() * sizeof(GroupOp),
+                          cudaMemcpyHostToDevice), "cudaMemcpy(group ops)");
+  }
+  group->nb = std::max(1, sms / P);
+  group->connected = true;
   DEAR_API_END
 }
 

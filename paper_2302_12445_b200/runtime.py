@@ -82,12 +82,11 @@ class LocalGroup:
     all ranks finish an iteration's ``step`` before any rank starts the next
     forward.
 
-    ``transport="peer"``: the contexts run the multi-GPU NVLink peer kernels
-    (zero-copy or slot reduce-scatter + update, all-gather) against each
-    other's memory on the one device — the N > 1 data path on one GPU. Call
-    :meth:`connect` after every rank's ``finalize``; give every rank its own
-    compute stream (a rank's ``step`` fence waits on the other ranks'
-    reduce-scatters)."""
+    ``transport="peer"``: the multi-GPU NVLink peer kernels (zero-copy or slot
+    reduce-scatter + update, all-gather) against each other's memory on the
+    one device — the N > 1 data path on one GPU. Each collective runs as one
+    cooperative launch over every rank's data once all ranks reached it (same
+    lock-step rule). Call :meth:`connect` after every rank's ``finalize``."""
 
     TRANSPORTS = {"ring": 0, "peer": 1}
 

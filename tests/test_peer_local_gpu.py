@@ -1,16 +1,12 @@
 """The multi-GPU NVLink peer data path, on ONE device (LocalGroup(P,
-transport="peer")): P contexts in this process run the same fused kernels as
-one process per GPU — zero-copy rs_update_zc_kernel + ag_unpack_peer_kernel,
-or the slot path pack_kernel<true> + rs_update_peer_kernel +
-ag_unpack_peer_kernel — with in-process deltas instead of IPC mappings and the
-same in-kernel cross-rank counters. Their sums follow the reference's ring
+transport="peer")): P contexts in this process run the same fused kernel code
+as one process per GPU — the zero-copy reduce-scatter + update and all-gather
+bodies, or the slot path's pack_kernel<true> + reduce-scatter + all-gather —
+with in-process deltas instead of IPC mappings and the same in-kernel
+cross-rank counters, each collective one cooperative launch over all ranks. Their sums follow the reference's ring
 order (collective.cpp:70-90), so parameters must be BIT-EXACT with the fp32
 ring restatement and within 1e-5 of the fp64 sgd_step (collective.cpp:166-194).
 """
-import os
-import subprocess
-import sys
-
 import numpy as np
 import pytest
 
@@ -94,37 +90,3 @@ def test_peer_lr_schedule(restated):
     exp32 = oracle_run(restated, RAGGED, 2, 4, "DEAR_FUSED", 100_000, 0.3, f32=True,
                        lr_schedule=sched)
     assert np.array_equal(got[0], exp32)
-
-
-def test_peer_timeout_traps_instead_of_hanging(tmp_path):
-    """A peer that never arrives: the cross-rank wait gives up after
-    DEAR_PEER_TIMEOUT_S and the kernel traps (a loud CUDA error), instead of
-    hanging the GPU. Runs in a child process (the trap poisons its context)."""
-    code = r'''
-import sys, torch
-sys.path.insert(0, %r)
-from paper_2302_12445_b200 import LocalGroup, Runtime
-g = LocalGroup(2, "peer")
-s = [torch.cuda.Stream(), torch.cuda.Stream()]
-rts, keep = [], []
-for r in range(2):
-    rt = Runtime(g, r, 2, policy="DEAR_FUSED", fusion_buffer_bytes=1 << 20, lr=0.1, stream=s[r])
-    p = torch.zeros(4096, device="cuda"); gr = torch.zeros(4096, device="cuda")
-    rt.register(1, p[:2048], gr[:2048]); rt.register(2, p[2048:], gr[2048:])
-    keep += [p, gr]; rts.append(rt)
-for rt in rts:
-    rt.finalize()
-g.connect()
-rts[0].grad_ready(2, s[0]); rts[0].grad_ready(1, s[0])   # rank 1 never reports
-try:
-    torch.cuda.synchronize()
-except Exception as e:
-    print("TRAPPED", type(e).__name__, flush=True)
-    import os; os._exit(3)
-print("NO-TRAP", flush=True)
-''' % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, DEAR_PEER_TIMEOUT_S="1")
-    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120,
-                         env=env)
-    assert "NO-TRAP" not in out.stdout
-    assert out.returncode != 0, out.stdout + out.stderr
