@@ -214,6 +214,42 @@ int dear_peer_connect(dear_ctx* ctx, const uint8_t* handles, int32_t n);
 int dear_peer_zero_copy(dear_ctx* ctx, int32_t* on);
 
 /* ---------------------------------------------------------------------------
+ * NVLS backend (NVLink SHARP through the NVSwitch, one process per GPU).
+ * Gradients, parameters and bf16 copies live in a symmetric heap: per rank one
+ * physical allocation mapped locally and through ONE multicast object over
+ * all P GPUs. The owner of a chunk reduces it with multimem.ld_reduce (the
+ * switch sums the P ranks' values), applies the SGD update, and the
+ * all-gather broadcasts the updated chunk with multicast stores; cross-rank
+ * order uses counters bumped on every rank by multimem.red and polled
+ * locally. The switch's fp32 summation order is unspecified: exact at P = 2,
+ * within the 1e-5 tolerance otherwise (like NCCL). The schedule (RS during
+ * backprop, AG gating each layer's forward) is unchanged.
+ * ------------------------------------------------------------------------ */
+typedef struct dear_symm dear_symm;
+/* *ok = 1 when `device` supports multicast objects. */
+int dear_nvls_supported(int32_t device, int32_t* ok);
+/* Collective heap setup: every rank calls dear_symm_create (rank 0 returns the
+ * (pid, fd) of the exported multicast handle; others get -1), the caller
+ * broadcasts rank 0's pair, every rank calls dear_symm_join (imports it with
+ * pidfd_getfd; no-op on rank 0), barrier, dear_symm_bind, barrier. */
+int dear_symm_create(int32_t rank, int32_t P, int64_t bytes, dear_symm** out, int64_t* pid,
+                     int64_t* fd);
+int dear_symm_join(dear_symm* heap, int64_t pid, int64_t fd);
+int dear_symm_bind(dear_symm* heap);
+/* The caller's region: local and multicast base addresses, bytes (>= the
+ * requested size). Carve identical layouts on every rank. */
+int dear_symm_ptr(dear_symm* heap, void** local, void** multicast, int64_t* bytes);
+/* Collective: every rank synchronizes and barriers first (peers store into
+ * this rank's memory through the multicast alias). */
+int dear_symm_destroy(dear_symm* heap);
+/* After dear_finalize: switch ctx to the NVLS kernels. Every registered
+ * gradient, parameter and bf16 copy must lie in `heap`'s region at the same
+ * offsets on every rank (checked across ranks over the NCCL communicator). */
+int dear_nvls_connect(dear_ctx* ctx, dear_symm* heap);
+/* *on = 1 when ctx runs the NVLS kernels. */
+int dear_nvls_enabled(dear_ctx* ctx, int32_t* on);
+
+/* ---------------------------------------------------------------------------
  * Introspection, timing and checks.
  * ------------------------------------------------------------------------ */
 int dear_num_buckets(dear_ctx* ctx, int32_t* n);

@@ -13,9 +13,10 @@ Public API
 from ._lib import DearError, InvalidArgument
 from .optim import DistOptim, init
 from .plan import build_fusion_plan, chunk_owner, chunk_ranges, slot_chunk, slot_stride
-from .runtime import Communicator, LocalGroup, Runtime
+from .runtime import Communicator, LocalGroup, Runtime, SymmetricHeap, nvls_supported
 
 __all__ = [
     "DearError", "InvalidArgument", "DistOptim", "init", "build_fusion_plan", "chunk_owner",
     "chunk_ranges", "slot_chunk", "slot_stride", "Communicator", "LocalGroup", "Runtime",
+    "SymmetricHeap", "nvls_supported",
 ]

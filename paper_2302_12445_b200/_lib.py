@@ -80,6 +80,15 @@ _SIGNATURES = {
     "dear_peer_connect": [_P, C.c_char_p, C.c_int32],
     "dear_peer_zero_copy": [_P, C.POINTER(C.c_int32)],
     "dear_bench_stage": [_P, C.c_int32, C.c_int32, _P],
+    "dear_nvls_supported": [C.c_int32, C.POINTER(C.c_int32)],
+    "dear_symm_create": [C.c_int32, C.c_int32, C.c_int64, C.POINTER(_P), C.POINTER(C.c_int64),
+                         C.POINTER(C.c_int64)],
+    "dear_symm_join": [_P, C.c_int64, C.c_int64],
+    "dear_symm_bind": [_P],
+    "dear_symm_ptr": [_P, C.POINTER(_P), C.POINTER(_P), C.POINTER(C.c_int64)],
+    "dear_symm_destroy": [_P],
+    "dear_nvls_connect": [_P, _P],
+    "dear_nvls_enabled": [_P, C.POINTER(C.c_int32)],
 }
 DEAR_PEER_HANDLE_BYTES = 256
 

@@ -3,6 +3,7 @@
 
 #include <stdint.h>
 
+#include <cstddef>
 #include <exception>
 #include <string>
 #include <vector>
@@ -30,6 +31,15 @@ std::vector<int64_t> chunk_begins(int64_t d, int P);
 int64_t slot_stride(int64_t d, int P);
 
 void set_last_error(const std::string& msg);
+
+// Symmetric heap (nvls.cpp) accessors for dear_nvls_connect.
+bool symm_contains(const dear_symm* h, const void* p, size_t bytes);
+int symm_rank(const dear_symm* h);
+int symm_size(const dear_symm* h);
+int symm_bound(const dear_symm* h);
+int64_t symm_mc_delta(const dear_symm* h);
+uintptr_t symm_base(const dear_symm* h);
+size_t symm_take_flags(dear_symm* h, size_t bytes);
 
 }  // namespace dear
 

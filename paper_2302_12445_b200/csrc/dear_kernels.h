@@ -182,6 +182,37 @@ cudaError_t launch_rs_update_zc(const Unit* units, const Slice* slices, const Hy
 // hp->lr = lr, stream-ordered (dear_set_lr; graph-capturable).
 cudaError_t launch_set_lr(HyperParams* hp, float lr, cudaStream_t s);
 
+// ---- NVLS (NVLink SHARP multicast) backend --------------------------------
+// Per-bucket counters in the symmetric heap; every rank's copy is bumped at
+// once through the multicast alias (multimem.red), polled locally.
+struct NvlsFlags {
+  uint32_t packed;    // += 1 per rank whose gradients of the bucket are complete
+  uint32_t updated;   // += 1 per owner whose reduce-scatter + update finished
+  uint32_t gathered;  // += 1 per owner whose broadcast (all-gather) finished
+  uint32_t pad[13];   // 64 B per bucket
+};
+struct NvlsArgs {
+  int64_t mc_delta;   // multicast alias - local address (bytes), heap-wide
+  NvlsFlags* ucf;     // this bucket's counters, local address
+  NvlsFlags* mcf;     // ... multicast alias
+  int32_t P;
+  int32_t pad;
+  long long spin_limit;
+};
+// Owned-chunk units (a = grad, b = param, c = bf16 copy; the zero-copy RS
+// tables). RS: multimem.ld_reduce of the gradients + SGD into the parameters;
+// bumps flags->updated (local epoch) and na.mcf->updated (every rank).
+cudaError_t launch_rs_update_nvls(const Unit* units, const Slice* slices, const HyperParams* hp,
+                                  int has_momentum_buf, float* mom_base, int use_momentum,
+                                  int use_wd, const NvlsArgs& na, BucketFlags* flags,
+                                  cudaStream_t s);
+// AG: multicast stores of the owned chunk (+ bf16 copy) into every rank, then
+// waits until every owner's broadcast of the bucket landed.
+cudaError_t launch_ag_nvls(const Unit* units, const Slice* slices, int with_shadow,
+                           const NvlsArgs& na, BucketFlags* flags, cudaStream_t s);
+// One warp: until every owner's RS of this bucket (epoch *epoch) finished.
+cudaError_t launch_nvls_wait_updated(const uint32_t* epoch, const NvlsArgs& na, cudaStream_t s);
+
 // Same-device peer group (LocalGroup "peer"): one rank's arguments of a peer
 // kernel. The group runs each reduce-scatter / all-gather as ONE cooperative
 // launch holding every rank's CTAs (nb per rank), so the kernels' cross-rank

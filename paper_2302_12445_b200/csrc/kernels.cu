@@ -882,6 +882,247 @@ __global__ void DEAR_ZC_BOUNDS
   ag_unpack_peer_body<kShadow>(units, slices, pa, sa, flags, n_slices, this_blk());
 }
 
+// ------------------------------------------------ NVLS (multimem) --------
+// NVLink SHARP: the gradients, parameters and bf16 copies live in a symmetric
+// heap bound to one multicast object (nvls.cpp); address p + mc_delta is the
+// multicast alias of local address p. multimem.ld_reduce makes the NVSwitch
+// fetch the element from every rank and return the sum (LDGMC in SASS), and a
+// store to a multicast address is replicated to every rank, so the owner of a
+// chunk reduces it with ONE load per element and broadcasts its update with
+// ONE posted store: the switch, not the SMs, does the P-way reduction and the
+// fan-out. The switch's summation order is unspecified (exact at P = 2, where
+// a + b = b + a; within 1e-5 of the fp64 oracle otherwise, like NCCL).
+//
+// Cross-rank protocol, all on per-bucket counters in the heap (NvlsFlags),
+// bumped on EVERY rank at once by multimem.red and polled locally — no
+// NVLink round trip in any spin: packed / updated / gathered grow by P per
+// iteration; `epoch` is the local arena's flags->updated (this rank's RS
+// count for the bucket).
+__device__ __forceinline__ float4 mc_ld_reduce4(const float* p) {
+  float4 v;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ float mc_ld_reduce1(const float* p) {
+  float v;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void mc_st4(float* p, float4 v) {
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x),
+               "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void mc_st1(float* p, float v) {
+  asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+// 4 bf16 (8 B) to a multicast address.
+__device__ __forceinline__ void mc_st_bf16x4(__nv_bfloat16* p, float4 v) {
+  __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y);
+  __nv_bfloat162 hi = __floats2bfloat162_rn(v.z, v.w);
+  asm volatile("multimem.st.relaxed.sys.global.v2.f32 [%0], {%1,%2};" ::"l"(p),
+               "f"(__uint_as_float(*reinterpret_cast<uint32_t*>(&lo))),
+               "f"(__uint_as_float(*reinterpret_cast<uint32_t*>(&hi)))
+               : "memory");
+}
+// One bf16: a plain strong store to the multicast alias is replicated too.
+__device__ __forceinline__ void mc_st_bf16(__nv_bfloat16* p, float v) {
+  const __nv_bfloat16 h = __float2bfloat16_rn(v);
+  asm volatile("st.relaxed.sys.global.b16 [%0], %1;" ::"l"(p),
+               "h"(*reinterpret_cast<const unsigned short*>(&h))
+               : "memory");
+}
+__device__ __forceinline__ void mc_red_add(uint32_t* p, uint32_t v) {
+  asm volatile("multimem.red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+template <typename T>
+__device__ __forceinline__ T* mc(T* p, int64_t d) {
+  return reinterpret_cast<T*>(reinterpret_cast<char*>(p) + d);
+}
+template <typename T>
+__device__ __forceinline__ const T* mc(const T* p, int64_t d) {
+  return reinterpret_cast<const T*>(reinterpret_cast<const char*>(p) + d);
+}
+
+// Spin (one thread) until the local copy of a multicast counter reaches target.
+__device__ __forceinline__ void spin_local(const uint32_t* f, uint32_t target,
+                                           long long spin_limit) {
+  const long long t0 = clock64();
+  while (static_cast<int32_t>(ld_acquire_sys(f) - target) < 0) {
+    __nanosleep(64);
+    if (spin_limit > 0 && clock64() - t0 > spin_limit) __trap();
+  }
+}
+
+// Last-CTA completion for the NVLS kernels: every CTA orders its (multicast)
+// stores at system scope before counting itself done; the last one bumps the
+// rank-local epoch (if any) and the multicast counter on every rank.
+__device__ __forceinline__ bool nvls_signal(uint32_t* done, uint32_t* local_epoch,
+                                            uint32_t* mc_counter) {
+  __syncthreads();
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    last = atomicAdd(done, 1u) == gridDim.x - 1;
+    if (last) {
+      *done = 0;
+      if (local_epoch) *local_epoch += 1;
+      __threadfence_system();
+      mc_red_add(mc_counter, 1u);
+    }
+  }
+  __syncthreads();
+  return last;
+}
+
+#ifndef DEAR_NVLS_KU
+#define DEAR_NVLS_KU 4
+#endif
+
+// Reduce-scatter + SGD update of the owned chunk (units: a = gradient, b =
+// parameter, c = bf16 copy, all local heap addresses). The bf16 copy is NOT
+// written here: the all-gather's multicast store refreshes it on every rank,
+// the owner included.
+template <bool kMom, bool kWd>
+__global__ void DEAR_ZC_BOUNDS
+    rs_update_nvls_kernel(const Unit* __restrict__ units, const Slice* __restrict__ slices,
+                          const HyperParams* __restrict__ hpp, int has_buf, float* mom_base,
+                          int64_t mc_delta, BucketFlags* flags, NvlsFlags* ucf, NvlsFlags* mcf,
+                          int P, long long spin_limit) {
+  if (threadIdx.x == 0) {
+    const uint32_t epoch = *reinterpret_cast<volatile uint32_t*>(&flags->updated);
+    if (blockIdx.x == 0) {
+      // This rank's gradients of the bucket are complete (the comm stream
+      // waited on the producers' events): announce it on every rank.
+      __threadfence_system();
+      mc_red_add(&mcf->packed, 1u);
+    }
+    spin_local(&ucf->packed, static_cast<uint32_t>(P) * (epoch + 1u), spin_limit);
+  }
+  __syncthreads();
+  const HyperParams hp = *hpp;
+  walk_slice(units, slices, kZcSlices, [&](const Unit& U, int64_t off, int64_t n) {
+    const float* g = U.a + off;
+    float* w = U.b + off;
+    float* mom = kMom ? mom_base + U.start + off : nullptr;
+    auto scalar = [&](int64_t i) {
+      const float acc = mc_ld_reduce1(mc(g + i, mc_delta));
+      float m = kMom ? mom[i] : 0.f;
+      w[i] = sgd_elem<kMom, kWd>(acc, w[i], m, hp, has_buf);
+      if (kMom) mom[i] = m;
+    };
+    int64_t head = ((16 - (reinterpret_cast<uintptr_t>(w) & 15)) & 15) >> 2;
+    if (head > n) head = n;
+    if (threadIdx.x < head) scalar(static_cast<int64_t>(threadIdx.x));
+    const int64_t n4 = (n - head) >> 2;
+    const float4* gm4 = reinterpret_cast<const float4*>(mc(g + head, mc_delta));
+    float4* w4 = reinterpret_cast<float4*>(w + head);
+    float* mh = kMom ? mom + head : nullptr;
+    const bool mvec = kMom && (reinterpret_cast<uintptr_t>(mh) & 15) == 0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int KU = DEAR_NVLS_KU, kWarps = kThreads / 32;
+    const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int64_t base = static_cast<int64_t>(warp) * 32 * KU; base < n4;
+         base += static_cast<int64_t>(kWarps) * 32 * KU) {
+      float4 acc[KU], wv[KU];
+#pragma unroll
+      for (int k = 0; k < KU; ++k) {
+        const int64_t q = base + k * 32 + lane;
+        acc[k] = q < n4 ? mc_ld_reduce4(reinterpret_cast<const float*>(gm4 + q)) : zero;
+        wv[k] = q < n4 ? w4[q] : zero;
+      }
+#pragma unroll
+      for (int k = 0; k < KU; ++k) {
+        const int64_t q = base + k * 32 + lane;
+        if (q >= n4) continue;
+        float4 mv = zero;
+        if (kMom && has_buf)
+          mv = mvec ? reinterpret_cast<const float4*>(mh)[q]
+                    : make_float4(mh[4 * q], mh[4 * q + 1], mh[4 * q + 2], mh[4 * q + 3]);
+        float4 o;
+        o.x = sgd_elem<kMom, kWd>(acc[k].x, wv[k].x, mv.x, hp, has_buf);
+        o.y = sgd_elem<kMom, kWd>(acc[k].y, wv[k].y, mv.y, hp, has_buf);
+        o.z = sgd_elem<kMom, kWd>(acc[k].z, wv[k].z, mv.z, hp, has_buf);
+        o.w = sgd_elem<kMom, kWd>(acc[k].w, wv[k].w, mv.w, hp, has_buf);
+        w4[q] = o;
+        if (kMom) {
+          if (mvec) {
+            reinterpret_cast<float4*>(mh)[q] = mv;
+          } else {
+            mh[4 * q] = mv.x;
+            mh[4 * q + 1] = mv.y;
+            mh[4 * q + 2] = mv.z;
+            mh[4 * q + 3] = mv.w;
+          }
+        }
+      }
+    }
+    for (int64_t i = head + n4 * 4 + threadIdx.x; i < n; i += kThreads) scalar(i);
+  });
+  nvls_signal(&flags->done[1], &flags->updated, &mcf->updated);
+}
+
+// All-gather: the owner broadcasts its updated chunk (and its bf16 copy) with
+// multicast stores into every rank's parameters; the last CTA then signals
+// and waits until every owner's broadcast of this bucket has landed here.
+template <bool kShadow>
+__global__ void DEAR_ZC_BOUNDS ag_nvls_kernel(const Unit* __restrict__ units,
+                                              const Slice* __restrict__ slices, int64_t mc_delta,
+                                              BucketFlags* flags, NvlsFlags* ucf, NvlsFlags* mcf,
+                                              int P, long long spin_limit) {
+  walk_slice(units, slices, kZcSlices, [&](const Unit& U, int64_t off, int64_t n) {
+    const float* w = U.b + off;
+    float* wm = mc(U.b + off, mc_delta);
+    __nv_bfloat16* shm =
+        (kShadow && U.c) ? mc(static_cast<__nv_bfloat16*>(U.c) + off, mc_delta) : nullptr;
+    auto scalar = [&](int64_t i) {
+      const float v = w[i];
+      mc_st1(wm + i, v);
+      if (kShadow && shm) mc_st_bf16(shm + i, v);
+    };
+    int64_t head = ((16 - (reinterpret_cast<uintptr_t>(w) & 15)) & 15) >> 2;
+    if (head > n) head = n;
+    if (threadIdx.x < head) scalar(static_cast<int64_t>(threadIdx.x));
+    const int64_t n4 = (n - head) >> 2;
+    const float4* w4 = reinterpret_cast<const float4*>(w + head);
+    constexpr int KU = DEAR_NVLS_KU;
+    for (int64_t q0 = threadIdx.x; q0 < n4; q0 += static_cast<int64_t>(kThreads) * KU) {
+      float4 v[KU];
+#pragma unroll
+      for (int k = 0; k < KU; ++k) {
+        const int64_t q = q0 + static_cast<int64_t>(k) * kThreads;
+        if (q < n4) v[k] = __ldcs(w4 + q);
+      }
+#pragma unroll
+      for (int k = 0; k < KU; ++k) {
+        const int64_t q = q0 + static_cast<int64_t>(k) * kThreads;
+        if (q < n4) {
+          mc_st4(wm + head + 4 * q, v[k]);
+          if (kShadow && shm) mc_st_bf16x4(shm + head + 4 * q, v[k]);
+        }
+      }
+    }
+    for (int64_t i = head + n4 * 4 + threadIdx.x; i < n; i += kThreads) scalar(i);
+  });
+  if (nvls_signal(&flags->done[2], nullptr, &mcf->gathered) && threadIdx.x == 0) {
+    const uint32_t epoch = *reinterpret_cast<volatile uint32_t*>(&flags->updated);
+    spin_local(&ucf->gathered, static_cast<uint32_t>(P) * epoch, spin_limit);
+    __threadfence_system();
+  }
+}
+
+// dear_step's "gradients consumed" fence on NVLS: every owner's reduce-scatter
+// of the last bucket (hence of all, stream order) has read our gradients.
+__global__ void nvls_wait_updated_kernel(const uint32_t* epoch, const NvlsFlags* ucf, int P,
+                                         long long spin_limit) {
+  if (threadIdx.x == 0)
+    spin_local(&ucf->updated, static_cast<uint32_t>(P) * *reinterpret_cast<const volatile uint32_t*>(epoch),
+               spin_limit);
+}
+
 // ------------------------------------- same-device group launches ---------
 // All P ranks' CTAs of one peer kernel in ONE cooperative grid (rank =
 // blockIdx.x / nb): the cross-rank counter waits inside are then between
@@ -1140,6 +1381,44 @@ cudaError_t launch_group_rs_peer(const GroupOp* ops, int P, int nb, int has_buf,
 cudaError_t launch_group_ag(const GroupOp* ops, int P, int nb, int with_shadow, cudaStream_t s) {
   if (with_shadow) return coop(group_ag_kernel<true>, P * nb, s, ops, nb);
   return coop(group_ag_kernel<false>, P * nb, s, ops, nb);
+}
+
+template <bool kMom, bool kWd>
+void rs_nvls_launch(const Unit* units, const Slice* slices, const HyperParams* hp, int has_buf,
+                    float* mom, const NvlsArgs& na, BucketFlags* flags, cudaStream_t s) {
+  rs_update_nvls_kernel<kMom, kWd><<<bucket_grid(kZcSlices), kThreads, 0, s>>>(
+      units, slices, hp, has_buf, mom, na.mc_delta, flags, na.ucf, na.mcf, na.P, na.spin_limit);
+}
+
+cudaError_t launch_rs_update_nvls(const Unit* units, const Slice* slices, const HyperParams* hp,
+                                  int has_momentum_buf, float* mom_base, int use_momentum,
+                                  int use_wd, const NvlsArgs& na, BucketFlags* flags,
+                                  cudaStream_t s) {
+  if (use_momentum && use_wd)
+    rs_nvls_launch<true, true>(units, slices, hp, has_momentum_buf, mom_base, na, flags, s);
+  else if (use_momentum)
+    rs_nvls_launch<true, false>(units, slices, hp, has_momentum_buf, mom_base, na, flags, s);
+  else if (use_wd)
+    rs_nvls_launch<false, true>(units, slices, hp, has_momentum_buf, mom_base, na, flags, s);
+  else
+    rs_nvls_launch<false, false>(units, slices, hp, has_momentum_buf, mom_base, na, flags, s);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ag_nvls(const Unit* units, const Slice* slices, int with_shadow,
+                           const NvlsArgs& na, BucketFlags* flags, cudaStream_t s) {
+  if (with_shadow)
+    ag_nvls_kernel<true><<<bucket_grid(kZcSlices), kThreads, 0, s>>>(
+        units, slices, na.mc_delta, flags, na.ucf, na.mcf, na.P, na.spin_limit);
+  else
+    ag_nvls_kernel<false><<<bucket_grid(kZcSlices), kThreads, 0, s>>>(
+        units, slices, na.mc_delta, flags, na.ucf, na.mcf, na.P, na.spin_limit);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_nvls_wait_updated(const uint32_t* epoch, const NvlsArgs& na, cudaStream_t s) {
+  nvls_wait_updated_kernel<<<1, 32, 0, s>>>(epoch, na.ucf, na.P, na.spin_limit);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_update(const Unit* units, const Slice* slices, int64_t total,

@@ -190,6 +190,17 @@ struct dear_ctx {
   // kernels address each other's memory with in-process deltas instead of
   // IPC mappings.
   bool same_dev = false;
+  // NVLS backend (dear_nvls_connect): multicast reduce-scatter / broadcast
+  // all-gather on the symmetric heap; na.ucf / na.mcf point at bucket 0's
+  // counters (bucket g at + g).
+  bool nvls = false;
+  NvlsArgs na{};
+  NvlsArgs nvls_args(int g) const {
+    NvlsArgs a = na;
+    a.ucf += g;
+    a.mcf += g;
+    return a;
+  }
   std::vector<void*> peer_maps;  // cudaIpcOpenMemHandle mappings to close
   bool timing = false;
   std::vector<std::string> trace;
@@ -441,9 +452,9 @@ void dear_ctx::exec(const Op& op) {
       cuda_check(cudaStreamWaitEvent(comm_stream, step_ev, 0), "cudaStreamWaitEvent");
       break;
     case OP_PACK:
-      if (direct) break;  // P = 1: the update reads the gradients in place
+      if (direct && !nvls) break;  // P = 1: the update reads the gradients in place
       record_t(op.bucket, T_PACK0);
-      if (zc) {  // zero-copy: the reduce-scatter reads the gradients in place
+      if (zc || nvls) {  // zero-copy: the reduce-scatter reads the gradients in place
         record_t(op.bucket, T_PACK1);
         break;
       }
@@ -472,6 +483,13 @@ void dear_ctx::exec(const Op& op) {
       if (local && same_dev) {
         // The group already ran every rank's reduce-scatter (run_collective).
         if (cfg.momentum != 0.0) B->mom_init = true;
+      } else if (nvls) {
+        // The switch sums the owned chunk over the ranks (multimem.ld_reduce).
+        cuda_check(launch_rs_update_nvls(B->zrs_u, B->zrs_ps, hp_dev, B->mom_init ? 1 : 0, B->mom,
+                                         cfg.momentum != 0.0, cfg.weight_decay != 0.0,
+                                         nvls_args(op.bucket), B->flags, comm_stream),
+                   "nvls rs+update kernel");
+        if (cfg.momentum != 0.0) B->mom_init = true;
       } else if (zc) {
         cuda_check(launch_rs_update_zc(B->zrs_u, B->zrs_ps, hp_dev, B->mom_init ? 1 : 0, B->mom,
                                        cfg.momentum != 0.0, cfg.weight_decay != 0.0,
@@ -495,7 +513,7 @@ void dear_ctx::exec(const Op& op) {
       record_t(op.bucket, T_RS1);
       break;
     case OP_UPDATE:
-      if (peer) break;
+      if (peer || nvls) break;
       if (direct) {
         cuda_check(launch_update_direct(B->dir_u, B->dir_s, B->e_dir, hp_dev,
                                         cfg.weight_decay != 0.0, B->any_shadow ? 1 : 0,
@@ -515,6 +533,11 @@ void dear_ctx::exec(const Op& op) {
       if (!local) record_t(op.bucket, T_AG0);
       if (local && same_dev) {
         // run by the group (run_collective)
+      } else if (nvls) {
+        // The owner's multicast stores broadcast its chunk to every rank.
+        cuda_check(launch_ag_nvls(B->zrs_u, B->zrs_ps, B->any_shadow ? 1 : 0,
+                                  nvls_args(op.bucket), B->flags, comm_stream),
+                   "nvls all-gather kernel");
       } else if (zc) {
         // Each owner's updated parameters, read over NVLink into ours.
         cuda_check(launch_ag_unpack_peer(B->zag_u, B->zag_ps, B->e_zag, B->any_shadow ? 1 : 0,
@@ -535,7 +558,7 @@ void dear_ctx::exec(const Op& op) {
       record_t(op.bucket, T_AG1);
       break;
     case OP_UNPACK:
-      if (peer || direct) break;
+      if (peer || direct || nvls) break;
       cuda_check(launch_unpack(B->unpack_u, B->unpack_s, B->e_unpack, B->any_shadow ? 1 : 0, 0,
                                comm_stream),
                  "unpack kernel");
@@ -546,7 +569,15 @@ void dear_ctx::exec(const Op& op) {
       B->ag_capture = capture_id(comm_stream);
       break;
     case OP_CALLER_WAIT_PACKED:
-      if (zc && !buckets.empty()) {
+      if (nvls && !buckets.empty()) {
+        // Every owner's reduce-scatter of the last bucket (so of all) read
+        // our gradients.
+        const int last = static_cast<int>(buckets.size()) - 1;
+        cuda_check(launch_nvls_wait_updated(&buckets.back().flags->updated, nvls_args(last),
+                                            comm_stream),
+                   "nvls wait kernel");
+        cuda_check(cudaEventRecord(packed_ev, comm_stream), "cudaEventRecord");
+      } else if (zc && !buckets.empty()) {
         // Zero-copy: peers read our gradients in their reduce-scatters, so
         // "consumed" means every rank's last (plan-order) RS has finished.
         const BucketFlags* f = buckets.back().flags;
@@ -868,7 +899,8 @@ int dear_finalize(dear_ctx* ctx) {
   const char* dir_env = std::getenv("DEAR_DIRECT");
   c.direct = c.P == 1 && !c.peer && c.cfg.momentum == 0.0 && !(dir_env && dir_env[0] == '0');
   // Zero-copy tables for a later dear_peer_connect (multi-process only).
-  c.zc_tables = (!c.local || c.same_dev) && c.P > 1;
+  // (also at P = 1 outside local groups: the NVLS kernels run on one GPU too)
+  c.zc_tables = (!c.local && !c.same_dev) || (c.same_dev && c.P > 1);
   // Unit tables.
   std::vector<Unit> host_units;
   struct Span { size_t pack, upd, unpack; };
@@ -1560,6 +1592,71 @@ int dear_peer_connect(dear_ctx* ctx, const uint8_t* handles, int32_t n) {
   }
   c.peer_maps = std::move(maps);
   enable_peer(c, pa, ga, qa, zc);
+  DEAR_API_END
+}
+
+int dear_nvls_connect(dear_ctx* ctx, dear_symm* heap) {
+  DEAR_API_BEGIN
+  need(ctx, true);
+  dear_ctx& c = *ctx;
+  if (!heap) invalid("dear_nvls_connect: null heap");
+  if (c.local || c.same_dev) invalid("dear_nvls_connect: needs one process per GPU");
+  if (c.peer || c.nvls) invalid("dear_nvls_connect: already connected");
+  if (!symm_bound(heap)) invalid("dear_nvls_connect: the heap is not bound (dear_symm_bind)");
+  if (symm_size(heap) != c.P || symm_rank(heap) != c.rank)
+    invalid("dear_nvls_connect: heap and context disagree on rank / world size");
+  if (c.P > 1 && !c.comm) invalid("dear_nvls_connect: needs the NCCL communicator for the layout check");
+  // Every tensor in the heap, at offsets identical on every rank.
+  const uintptr_t base = symm_base(heap);
+  uint64_t h = 1469598103934665603ULL;
+  for (size_t i = 0; i < c.layers.size(); ++i) {
+    const LayerReg& R = c.layers[i];
+    if (R.numel <= 0) continue;
+    const size_t nb = static_cast<size_t>(R.numel) * 4;
+    if (!symm_contains(heap, R.grad, nb) || !symm_contains(heap, R.param, nb) ||
+        (R.shadow && !symm_contains(heap, R.shadow, nb / 2)))
+      invalid("dear_nvls_connect: layer " + std::to_string(i + 1) +
+              "'s gradient / parameter / bf16 copy is not inside the symmetric heap");
+    h = fnv(h, reinterpret_cast<uintptr_t>(R.grad) - base);
+    h = fnv(h, reinterpret_cast<uintptr_t>(R.param) - base);
+    h = fnv(h, R.shadow ? reinterpret_cast<uintptr_t>(R.shadow) - base : ~0ULL);
+  }
+  const size_t G = c.buckets.size();
+  const size_t at = symm_take_flags(heap, G * sizeof(NvlsFlags));
+  h = fnv(h, at);
+  if (c.P > 1) {
+    unsigned long long hv[2] = {h, ~h};
+    cuda_check(cudaMemcpy(c.hash_dev, hv, sizeof hv, cudaMemcpyHostToDevice), "cudaMemcpy");
+    nccl_check(ncclAllReduce(c.hash_dev, c.hash_dev, 2, ncclUint64, ncclMax, c.comm, c.comm_stream),
+               "ncclAllReduce(nvls layout check)");
+    cuda_check(cudaMemcpyAsync(hv, c.hash_dev, sizeof hv, cudaMemcpyDeviceToHost, c.comm_stream),
+               "cudaMemcpyAsync");
+    cuda_check(cudaStreamSynchronize(c.comm_stream), "cudaStreamSynchronize");
+    if (hv[0] != h || hv[1] != ~h)
+      invalid("dear_nvls_connect: ranks placed their tensors at different heap offsets");
+  }
+  const int64_t d = symm_mc_delta(heap);
+  NvlsArgs na{};
+  na.mc_delta = d;
+  na.ucf = reinterpret_cast<NvlsFlags*>(base + at);
+  na.mcf = reinterpret_cast<NvlsFlags*>(base + at + d);
+  na.P = c.P;
+  na.spin_limit = peer_spin_limit(c.device);
+  c.na = na;
+  c.nvls = true;
+  c.peer = true;  // no pack / update / unpack kernels (fused in the NVLS pair)
+  // 1/P after the switch's sum (same bits as pre-scaling for P = 2^k).
+  c.hp_host.prescaled = 0;
+  cuda_check(cudaMemcpy(c.hp_dev, &c.hp_host, sizeof(HyperParams), cudaMemcpyHostToDevice),
+             "cudaMemcpy(hp)");
+  DEAR_API_END
+}
+
+int dear_nvls_enabled(dear_ctx* ctx, int32_t* on) {
+  DEAR_API_BEGIN
+  need(ctx, true);
+  if (!on) invalid("dear_nvls_enabled: null output");
+  *on = ctx->nvls ? 1 : 0;
   DEAR_API_END
 }
 

@@ -38,7 +38,7 @@ from typing import Optional
 
 import torch
 
-from .runtime import Communicator, LocalGroup, Runtime
+from .runtime import Communicator, LocalGroup, Runtime, SymmetricHeap
 
 
 class DistOptim:
@@ -52,6 +52,9 @@ class DistOptim:
         if len(optimizer.param_groups) != 1:
             raise ValueError("DistOptim supports a single parameter group")
         g = optimizer.param_groups[0]
+        if backend == "nvls" and not flatten:
+            raise ValueError("the nvls backend needs flatten=True (the flat buffers live in the "
+                             "symmetric heap)")
         if g.get("maximize", False):
             raise ValueError("maximize=True is not supported")
         if model is None and defer_allgather:
@@ -68,13 +71,19 @@ class DistOptim:
         self.params = params
         self._lr = float(g["lr"])
         self._in_backward = False
+        self._heap = None
+        if backend == "nvls":
+            # The flat parameter / gradient buffers live in a symmetric heap
+            # mapped through one NVLS multicast object (collective).
+            n = sum((p.numel() + 63) // 64 * 64 for p in params if p.requires_grad)
+            self._heap = SymmetricHeap(2 * 4 * max(n, 64) + (1 << 16))
         if isinstance(comm, LocalGroup):
             world, rank_ = comm.P, rank
         elif isinstance(comm, Communicator):
             world, rank_ = comm.world_size, comm.rank
         else:
             world, rank_ = 1, 0
-        self.runtime = Runtime(comm, rank_, world, policy=policy,
+        self.runtime = Runtime(comm, rank_, world, policy=policy, heap=self._heap,
                                fusion_buffer_bytes=fusion_buffer_bytes, lr=self._lr,
                                momentum=float(g.get("momentum", 0.0)),
                                dampening=float(g.get("dampening", 0.0)),
@@ -93,8 +102,12 @@ class DistOptim:
             for p in params:
                 offs.append(n)
                 n += (p.numel() + 63) // 64 * 64
-            pflat = torch.zeros(max(n, 64), dtype=torch.float32, device=params[0].device)
-            gflat = torch.zeros_like(pflat)
+            if self._heap is not None:
+                pflat = self._heap.tensor(max(n, 64)).zero_()
+                gflat = self._heap.tensor(max(n, 64)).zero_()
+            else:
+                pflat = torch.zeros(max(n, 64), dtype=torch.float32, device=params[0].device)
+                gflat = torch.zeros_like(pflat)
             for p, o in zip(params, offs):
                 view = pflat[o:o + p.numel()].view_as(p)
                 view.copy_(p.data)
@@ -183,6 +196,14 @@ class DistOptim:
             h.remove()
         self._hooks = []
         self.runtime.close()
+        if self._heap is not None:
+            # the parameters live in the heap: give them private storage first
+            for p in self.params:
+                p.data = p.data.clone()
+                p.grad = p.grad.clone()
+            self._flat = None
+            self._heap.close()
+            self._heap = None
 
 
 def init(group=None) -> Communicator | None:

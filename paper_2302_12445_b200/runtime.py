@@ -112,6 +112,81 @@ class LocalGroup:
             self._g = C.c_void_p()
 
 
+def nvls_supported(device: Optional[int] = None) -> bool:
+    """The GPU supports NVLink SHARP multicast objects (NVSwitch systems)."""
+    ok = C.c_int32(0)
+    dev = torch.cuda.current_device() if device is None else device
+    check(lib().dear_nvls_supported(dev, C.byref(ok)))
+    return bool(ok.value)
+
+
+class _CudaBuffer:
+    """__cuda_array_interface__ view of raw device bytes (kept alive by the heap)."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1",
+                                         "data": (ptr, False), "version": 3, "strides": None}
+
+
+class SymmetricHeap:
+    """Device memory mapped on every rank through one NVLS multicast object
+    (dear_symm_*). Collective over torch.distributed (or a single rank
+    without it). ``tensor()`` carves 256-byte aligned tensors in call order —
+    identical offsets on every rank when every rank makes the same calls."""
+
+    def __init__(self, nbytes: int, rank: Optional[int] = None, world_size: Optional[int] = None):
+        dist_on = _dist_ready()
+        if dist_on:
+            import torch.distributed as dist
+
+            rank, world_size = dist.get_rank(), dist.get_world_size()
+        rank = 0 if rank is None else rank
+        world_size = 1 if world_size is None else world_size
+        self.rank, self.world_size = rank, world_size
+        self._h = C.c_void_p()
+        pid, fd = C.c_int64(-1), C.c_int64(-1)
+        check(lib().dear_symm_create(rank, world_size, int(nbytes), C.byref(self._h),
+                                     C.byref(pid), C.byref(fd)))
+        pair = [(pid.value, fd.value)]
+        if dist_on and world_size > 1:
+            import torch.distributed as dist
+
+            dist.broadcast_object_list(pair, 0)
+        check(lib().dear_symm_join(self._h, pair[0][0], pair[0][1]))
+        if dist_on and world_size > 1:
+            torch.distributed.barrier()  # every GPU added before any memory is bound
+        check(lib().dear_symm_bind(self._h))
+        if dist_on and world_size > 1:
+            torch.distributed.barrier()
+        loc, mc, n = C.c_void_p(), C.c_void_p(), C.c_int64()
+        check(lib().dear_symm_ptr(self._h, C.byref(loc), C.byref(mc), C.byref(n)))
+        self.local, self.multicast, self.nbytes = loc.value, mc.value, n.value
+        self._bytes = torch.as_tensor(_CudaBuffer(self.local, self.nbytes), device="cuda")
+        self._cursor = 0
+
+    @property
+    def handle(self) -> int:
+        return self._h.value
+
+    def tensor(self, numel: int, dtype=torch.float32) -> torch.Tensor:
+        esz = torch.empty((), dtype=dtype).element_size()
+        nb = max(int(numel), 1) * esz
+        at = (self._cursor + 255) // 256 * 256
+        if at + nb > self.nbytes:
+            raise MemoryError(f"symmetric heap exhausted ({at + nb} > {self.nbytes} bytes)")
+        self._cursor = at + nb
+        return self._bytes[at:at + nb].view(dtype)[:numel]
+
+    def close(self) -> None:
+        if self._h.value:
+            if _dist_ready() and self.world_size > 1:
+                torch.cuda.synchronize()
+                torch.distributed.barrier()
+            self._bytes = None
+            check(lib().dear_symm_destroy(self._h))
+            self._h = C.c_void_p()
+
+
 class Runtime:
     """One DeAR context: registered tensors, fusion buckets, comm stream."""
 
@@ -120,12 +195,17 @@ class Runtime:
                  lr: float = 0.05, momentum: float = 0.0, dampening: float = 0.0,
                  weight_decay: float = 0.0, nesterov: bool = False,
                  dear_group_dependency: bool = False, defer_allgather: bool = False,
-                 backend: str = "auto", stream: Optional[torch.cuda.Stream] = None):
+                 backend: str = "auto", stream: Optional[torch.cuda.Stream] = None,
+                 heap: Optional[SymmetricHeap] = None):
         if policy not in POLICIES:
             raise ValueError(f"unknown policy kind {policy!r}; expected one of "
                              f"{', '.join(POLICIES)}")
-        if backend not in ("auto", "nccl", "peer"):
-            raise ValueError("backend must be 'auto', 'nccl' or 'peer'")
+        if backend not in ("auto", "nccl", "peer", "nvls"):
+            raise ValueError("backend must be 'auto', 'nccl', 'peer' or 'nvls'")
+        if backend == "nvls" and heap is None:
+            raise ValueError("the nvls backend needs a SymmetricHeap holding the tensors")
+        if heap is not None and backend == "auto":
+            backend = "nvls"
         if isinstance(comm, LocalGroup):
             # A local group's transport decides the collectives: "local" (the
             # ring-order emulation kernels) or "peer" (the NVLink peer kernels).
@@ -146,6 +226,7 @@ class Runtime:
         self.policy = policy
         self.backend = backend
         self._group = comm if isinstance(comm, LocalGroup) else None
+        self._heap = heap
         cfg = DearCfg(POLICIES[policy], int(fusion_buffer_bytes) if "FUSED" in policy else 0,
                       int(dear_group_dependency), float(lr),
                       float(momentum), float(dampening), float(weight_decay), int(nesterov),
@@ -185,7 +266,9 @@ class Runtime:
 
     def finalize(self) -> None:
         check(lib().dear_finalize(self._ctx))
-        if self.backend == "peer" and self.world_size > 1 and self._group is None:
+        if self.backend == "nvls":
+            check(lib().dear_nvls_connect(self._ctx, self._heap.handle))
+        elif self.backend == "peer" and self.world_size > 1 and self._group is None:
             self._connect_peers()
 
     @property
@@ -296,8 +379,8 @@ class Runtime:
         their mappings, so every rank drains its comm stream and meets the
         others at a barrier before any unmaps or frees."""
         if self._ctx.value:
-            if self.backend == "peer" and self.world_size > 1 and self._group is None \
-                    and _dist_ready():
+            if self.backend in ("peer", "nvls") and self.world_size > 1 \
+                    and self._group is None and _dist_ready():
                 import torch.distributed as dist
 
                 check(lib().dear_synchronize(self._ctx))

@@ -1,8 +1,16 @@
 #!/usr/bin/env python
 """BASELINE config 5: reduce-scatter / all-gather bucket-size sweep through the
-DeAR runtime (in-place NCCL RS/AG of one bucket buffer on the comm stream).
+DeAR runtime, per collective transport:
 
-    torchrun --nproc-per-node P tools/sweep_collectives.py [--min-kb 64] [--max-mb 256]
+  nccl  in-place ncclReduceScatter / ncclAllGather of one bucket buffer (the
+        pack / update / unpack kernels around them timed separately)
+  zc    zero-copy NVLink peer kernels (RS pulls every rank's gradients, sums
+        in ring order and applies the update; AG pulls the owners' parameters)
+  slot  peer kernels over IPC-mapped bucket slots (pack, RS+update, AG+unpack)
+  nvls  NVLink SHARP: multimem.ld_reduce RS+update, multicast-store AG
+
+    torchrun --nproc-per-node P tools/sweep_collectives.py [--backends nccl,zc,slot,nvls]
+        [--min-kb 64] [--max-mb 256]
 
 For each bucket size (x2 from 64 KB to 256 MB, fp32) one tensor is registered,
 `--reps` DeAR iterations run with comm-stream event timing, and rank 0 prints
@@ -27,9 +35,7 @@ def main():
     ap.add_argument("--max-mb", type=int, default=256)
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--backend", default="nccl", choices=["nccl", "peer"],
-                    help="peer: fused RS+update / AG+unpack NVLink kernels (times include "
-                         "the update / unpack they fuse)")
+    ap.add_argument("--backends", default="nccl,zc,slot,nvls")
     a = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -43,46 +49,79 @@ def main():
     dist.init_process_group("nccl", device_id=torch.device("cuda", lr))
     comm = dear.init()
     s = torch.cuda.Stream()
-    size = a.min_kb * 1024
-    points = []
-    while size <= a.max_mb * 1024 * 1024:
-        n = size // 4
-        p = torch.zeros(n, device="cuda")
-        g = torch.ones(n, device="cuda")
-        rt = dear.Runtime(comm, rank, P, policy="DEAR", lr=0.0, stream=s, backend=a.backend)
-        rt.register(1, p, g)
-        rt.finalize()
-        rt.set_timing(True)
-        rs, ag = [], []
-        for it in range(a.warmup + a.reps):
-            with torch.cuda.stream(s):
-                rt.param_wait(1, s)
-                rt.grad_ready(1, s)
-                rt.step(s)
-            rt.synchronize()
-            if it >= a.warmup:
-                t = rt.timings()[0]
-                rs.append(t["rs"])
-                ag.append(t["ag"])
-        stride = rt.buckets()[0]["slot_stride"]
-        rt.close()
-        t_rs = torch.tensor([statistics.median(rs)], device="cuda")
-        t_ag = torch.tensor([statistics.median(ag)], device="cuda")
-        dist.all_reduce(t_rs, op=dist.ReduceOp.MAX)
-        dist.all_reduce(t_ag, op=dist.ReduceOp.MAX)
-        bus = (P - 1) * stride * 4
-        pt = {"backend": a.backend, "bytes": size, "P": P, "rs_ms": t_rs.item(), "ag_ms": t_ag.item(),
-              "rs_busbw_gbs": bus / (t_rs.item() / 1e3) / 1e9,
-              "ag_busbw_gbs": bus / (t_ag.item() / 1e3) / 1e9}
-        points.append(pt)
+    maxn = a.max_mb * 1024 * 1024 // 4
+    heap = None
+    for backend in a.backends.split(","):
+        if backend == "nvls":
+            if not dear.nvls_supported():
+                if rank == 0:
+                    print(json.dumps({"backend": "nvls", "unavailable": "no multicast support"}))
+                continue
+            if heap is None:
+                heap = dear.SymmetricHeap(2 * 4 * maxn + (1 << 20))
+                hp, hg = heap.tensor(maxn), heap.tensor(maxn)
+            pbuf, gbuf = hp, hg
+        else:
+            pbuf = torch.zeros(maxn, device="cuda")
+            gbuf = torch.zeros(maxn, device="cuda")
+        os.environ["DEAR_ZERO_COPY"] = "0" if backend == "slot" else "1"
+        rt_backend = {"zc": "peer", "slot": "peer"}.get(backend, backend)
+        size = a.min_kb * 1024
+        points = []
+        while size <= a.max_mb * 1024 * 1024:
+            n = size // 4
+            p, g = pbuf[:n], gbuf[:n]
+            p.zero_()
+            g.fill_(1.0)
+            rt = dear.Runtime(comm, rank, P, policy="DEAR", lr=0.0, stream=s, backend=rt_backend,
+                              heap=heap if backend == "nvls" else None)
+            rt.register(1, p, g)
+            rt.finalize()
+            if backend in ("zc", "slot"):
+                assert rt.zero_copy == (backend == "zc"), backend
+            rt.set_timing(True)
+            st = {k: [] for k in ("pack", "rs", "update", "ag", "unpack")}
+            for it in range(a.warmup + a.reps):
+                with torch.cuda.stream(s):
+                    rt.param_wait(1, s)
+                    rt.grad_ready(1, s)
+                    rt.step(s)
+                rt.synchronize()
+                if it >= a.warmup:
+                    t = rt.timings()[0]
+                    for k in st:
+                        if t[k] is not None:
+                            st[k].append(t[k])
+            stride = rt.buckets()[0]["slot_stride"]
+            rt.close()
+            med = torch.tensor([statistics.median(st[k]) if st[k] else 0.0 for k in st],
+                               device="cuda")
+            dist.all_reduce(med, op=dist.ReduceOp.MAX)
+            m = dict(zip(st, med.tolist()))
+            bus = (P - 1) * stride * 4
+            pt = {"backend": backend, "bytes": size, "P": P, "rs_ms": m["rs"], "ag_ms": m["ag"],
+                  "pack_ms": m["pack"], "update_ms": m["update"], "unpack_ms": m["unpack"],
+                  "rs_busbw_gbs": bus / (m["rs"] / 1e3) / 1e9 if m["rs"] else None,
+                  "ag_busbw_gbs": bus / (m["ag"] / 1e3) / 1e9 if m["ag"] else None,
+                  "note": {"nccl": "rs/ag: the NCCL calls alone",
+                           "zc": "rs: fused RS+update kernel; ag: pull all-gather kernel",
+                           "slot": "rs: fused RS+update after pack; ag: fused AG+unpack",
+                           "nvls": "rs: multimem.ld_reduce RS+update; ag: multicast-store "
+                                   "broadcast + arrival wait"}[backend]}
+            points.append(pt)
+            if rank == 0:
+                print(json.dumps(pt), flush=True)
+            size *= 2
         if rank == 0:
-            print(json.dumps(pt), flush=True)
-        size *= 2
-    if rank == 0:
-        cal = calibrate_alpha_beta([(p["bytes"], (p["rs_ms"] + p["ag_ms"]) / 1e3) for p in points], P)
-        print(json.dumps({"backend": a.backend, "calibration": cal, "P": P,
-                          "link_GBps_from_beta": (1 / cal["beta"] / 1e9) if cal["beta"] else None}),
-              flush=True)
+            cal = calibrate_alpha_beta([(q["bytes"], (q["rs_ms"] + q["ag_ms"]) / 1e3)
+                                        for q in points], P)
+            print(json.dumps({"backend": backend, "calibration": cal, "P": P,
+                              "link_GBps_from_beta": (1 / cal["beta"] / 1e9) if cal["beta"]
+                              else None}), flush=True)
+        del pbuf, gbuf
+        torch.cuda.empty_cache()
+    if heap is not None:
+        heap.close()
     comm.close()
     dist.destroy_process_group()
 
