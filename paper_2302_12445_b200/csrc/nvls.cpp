@@ -209,6 +209,7 @@ int dear_symm_create(int32_t rank, int32_t P, int64_t bytes, dear_symm** out, in
                      int64_t* fd) {
   DEAR_API_BEGIN
   if (!out || P < 1 || rank < 0 || rank >= P || bytes < 0) bad("dear_symm_create: bad arguments");
+  if (P < 2) bad("dear_symm_create: a multicast team needs at least 2 GPUs");
   const Driver& d = drv();
   auto* h = new dear_symm();
   try {
@@ -221,6 +222,9 @@ int dear_symm_create(int32_t rank, int32_t P, int64_t bytes, dear_symm** out, in
     prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
     prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
     prop.location.id = h->device;
+    // An exported / imported multicast object binds only externally
+    // shareable memory.
+    prop.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
     size_t g1 = 0, g2 = 0;
     cu_check(d.granularity(&g1, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED),
              "cuMemGetAllocationGranularity");
