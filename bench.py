@@ -59,9 +59,9 @@ def parse():
     ap.add_argument("--lr", type=float, default=0.05)
     ap.add_argument("--momentum", type=float, default=0.0)
     ap.add_argument("--no-graph", action="store_true")
-    ap.add_argument("--backend", default="auto", choices=["auto", "nccl", "peer"],
-                    help="bucket collectives: fused NVLink peer kernels (auto when N > 1) "
-                         "or NCCL RS/AG")
+    ap.add_argument("--backend", default="auto", choices=["auto", "nccl", "peer", "nvls"],
+                    help="bucket collectives: fused NVLink peer kernels (auto when N > 1), "
+                         "NVLS multicast kernels on a symmetric heap, or NCCL RS/AG")
     ap.add_argument("--group-dependency", type=int, default=1,
                     help="DEAR with dear_group_dependency (AG_g <- RS_g) and the comm "
                          "dispatch order simulated on measured times (0: global barrier)")
@@ -315,7 +315,8 @@ def make_runtime(a, model, comm, rank, world, stream, policy, defer):
     gd = bool(a.group_dependency) and policy.startswith("DEAR")
     rt = dear.Runtime(comm, rank, world, policy=policy, fusion_buffer_bytes=a.buffer,
                       lr=a.lr, momentum=a.momentum, defer_allgather=defer,
-                      backend=a.backend, stream=stream, dear_group_dependency=gd)
+                      backend=a.backend, stream=stream, dear_group_dependency=gd,
+                      heap=model.heap if a.backend == "nvls" else None)
     for l in range(1, model.L + 1):
         rt.register(l, model.params[l - 1], model.grads[l - 1], model.shadows[l - 1])
     rt.finalize()
@@ -410,7 +411,8 @@ def gpu_arm(a, wl, world, rank, local_rank):
     batch = a.batch or wl["batch"]
     tokens = batch * wl["tokens_per_sample"]
     counts = preset_param_counts(wl["preset"])
-    model = SyntheticModel(counts, wl["hidden"], tokens, seed=1234)
+    model = SyntheticModel(counts, wl["hidden"], tokens, seed=1234,
+                           symmetric=a.backend == "nvls" and world > 1)
     stream = torch.cuda.Stream()
     use_graph = not a.no_graph
     hbm, tf_burst, tf_sus, peak_kind = peaks()
@@ -707,7 +709,8 @@ def _bench_parity(a, model, comm, rank, world, stream):
 
     o = Restated()
     rt = dear.Runtime(comm, rank, world, policy=a.policy, fusion_buffer_bytes=a.buffer,
-                      lr=a.lr, momentum=a.momentum, backend=a.backend, stream=stream)
+                      lr=a.lr, momentum=a.momentum, backend=a.backend, stream=stream,
+                      heap=model.heap if a.backend == "nvls" else None)
     for l in range(1, model.L + 1):
         rt.register(l, model.params[l - 1], model.grads[l - 1], model.shadows[l - 1])
     rt.finalize()
@@ -909,9 +912,14 @@ def compare_policies(a, wl_name, comm, world, rank, stream):
     dist_on = world > 1
     steps, warm = max(5, a.steps // 2), max(3, a.warmup)
 
+    import paper_2302_12445_b200 as dear
+
+    nvls_ok = world > 1 and dear.nvls_supported()
+
     def one(batch, with_nccl):
         model = SyntheticModel(preset_param_counts(wl["preset"]), wl["hidden"],
-                               batch * wl["tokens_per_sample"], seed=4321)
+                               batch * wl["tokens_per_sample"], seed=4321,
+                               symmetric=a.backend == "nvls" and world > 1)
         out = {"batch_per_gpu": batch}
         run = make_runner(Step(model, None, stream), True, stream)
         comp = time_loop(run, steps, warm, stream, dist_on)
@@ -920,9 +928,21 @@ def compare_policies(a, wl_name, comm, world, rank, stream):
         t_ff = tiles.get("ff", {}).get("us", 0.0) * model.L / 1e3
         t_bp = tiles.get("bp_group_us", 0.0) * model.L / 1e3
         # The resolved default backend first; with N > 1 also NCCL, the north
-        # star's named transport (DeAR's edge over WFBP grows with comm cost).
-        for be in [None] + (["nccl"] if with_nccl and world > 1 and a.backend != "nccl" else []):
-            res = _policy_pair(a, model, comm, world, rank, stream, batch, steps, warm, be)
+        # star's named transport (DeAR's edge over WFBP grows with comm cost),
+        # and the NVLS transport (on its own symmetric-heap copy of the model).
+        extra = []
+        if with_nccl and world > 1 and a.backend != "nccl":
+            extra.append("nccl")
+        if with_nccl and nvls_ok and a.backend != "nvls":
+            extra.append("nvls")
+        for be in [None] + extra:
+            m = model
+            if be == "nvls":
+                m = SyntheticModel(preset_param_counts(wl["preset"]), wl["hidden"],
+                                   batch * wl["tokens_per_sample"], seed=4321, symmetric=True)
+            res = _policy_pair(a, m, comm, world, rank, stream, batch, steps, warm, be)
+            if m is not model:
+                m.close()
             d, w = res[a.policy]["ms_per_step"], res[a.baseline_policy]["ms_per_step"]
             res.update({"dear_over_wfbp": w / d,
                         "exposed_comm_pct": max(0.0, 100 * (d - comp) / d),
@@ -938,7 +958,7 @@ def compare_policies(a, wl_name, comm, world, rank, stream):
             if be is None:
                 out.update(res)
             else:
-                out["nccl"] = res
+                out[be] = res
         if with_nccl and world > 1:
             # BASELINE configs 3/4 "fusion buffer sweep": the same comparison
             # with 10 MB buckets on the default transport, where per-bucket

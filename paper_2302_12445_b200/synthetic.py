@@ -39,7 +39,7 @@ def _round_up(x: int, m: int) -> int:
 
 class SyntheticModel:
     def __init__(self, numels: list[int], hidden: int, tokens: int, device="cuda", seed: int = 0,
-                 tune: bool = True, wgrad_split: int = 0):
+                 tune: bool = True, wgrad_split: int = 0, symmetric: bool = False):
         self.numels = [int(n) for n in numels]
         self.L = len(self.numels)
         self.H = int(hidden)
@@ -56,8 +56,20 @@ class SyntheticModel:
             off += _round_up(max(n, 1), 64)
         self.flat_elems = off
         g = torch.Generator(device="cpu").manual_seed(seed)
-        self.params_flat = (torch.rand(off, generator=g) * 2 - 1).mul_(0.02).to(dev)
-        self.grads_flat = torch.zeros(off, device=dev)
+        rows = [max(1, math.ceil(n / H)) for n in self.numels]
+        # symmetric=True: parameters, gradients and bf16 copies in an NVLS
+        # symmetric heap (collective over torch.distributed), for the nvls backend.
+        self.heap = None
+        if symmetric:
+            from .runtime import SymmetricHeap
+
+            self.heap = SymmetricHeap(8 * off + 2 * sum(r * H for r in rows) + (1 << 20))
+            self.params_flat = self.heap.tensor(off)
+            self.params_flat.copy_((torch.rand(off, generator=g) * 2 - 1).mul_(0.02))
+            self.grads_flat = self.heap.tensor(off).zero_()
+        else:
+            self.params_flat = (torch.rand(off, generator=g) * 2 - 1).mul_(0.02).to(dev)
+            self.grads_flat = torch.zeros(off, device=dev)
         self.params = [self.params_flat[o:o + n] for o, n in zip(self.offsets, self.numels)]
         self.grads = [self.grads_flat[o:o + n] for o, n in zip(self.offsets, self.numels)]
         # bf16 compute copies, full rows (zero pad past n_l).
@@ -65,7 +77,8 @@ class SyntheticModel:
         for r in self.rows:
             self.w_offsets.append(woff)
             woff += r * H
-        self.shadow_flat = torch.zeros(woff, dtype=torch.bfloat16, device=dev)
+        self.shadow_flat = (self.heap.tensor(woff, torch.bfloat16).zero_() if self.heap is not None
+                            else torch.zeros(woff, dtype=torch.bfloat16, device=dev))
         self.shadows = [self.shadow_flat[o:o + r * H] for o, r in zip(self.w_offsets, self.rows)]
         for p, s in zip(self.params, self.shadows):
             s[: p.numel()].copy_(p.to(torch.bfloat16))
@@ -237,3 +250,8 @@ class SyntheticModel:
     def close(self):
         for p in self.ff + self.ff_t + self.dgrad + self.wgrad:
             p.close()
+        if self.heap is not None:
+            self.params = self.grads = self.shadows = None
+            self.params_flat = self.grads_flat = self.shadow_flat = None
+            self.heap.close()
+            self.heap = None
