@@ -389,6 +389,10 @@ def make_runtime(a, model, comm, rank, world, stream, policy, defer):
                                          for t in trials],
                           "stage_us_mean": {k: sum(x[k] or 0.0 for x in st) * 1e3 / len(st)
                                             for k in ("pack", "rs", "update", "ag", "unpack")},
+                          # per bucket (plan order): RS side (pack + RS + update) and
+                          # AG side (AG + unpack) of a comm-only iteration, ms
+                          "stage_ms": [[sum(v for v in (x["pack"], x["rs"], x["update"]) if v),
+                                        sum(v for v in (x["ag"], x["unpack"]) if v)] for x in st],
                           "t_ff_us": t_ff * 1e6, "t_bp_us": t_bp * 1e6, "buckets": len(st)}
     return rt
 
@@ -871,12 +875,14 @@ def _policy_pair(a, model, comm, world, rank, stream, batch, steps, warm, backen
     if buffer is not None:
         ab.buffer = buffer
     res = {}
+    stage_ms = None
     for policy in (a.policy, a.baseline_policy):
         rt = make_runtime(ab, model, comm, rank, world, stream, policy, True)
         res["collectives"] = rt.backend
         res["zero_copy"] = bool(getattr(rt, "zero_copy", False))
         if rt.comm_order_info:
             info = rt.comm_order_info
+            stage_ms = info["stage_ms"]
             res["comm_order"] = {k: v for k, v in info.items()
                                  if k in ("ags_during_backprop", "contention")}
             st, nb = info["stage_us_mean"], info["buckets"]
@@ -887,6 +893,31 @@ def _policy_pair(a, model, comm, world, rank, stream, batch, steps, warm, backen
         rt.synchronize()
         rt.close()
         res[policy] = {"ms_per_step": ms, "samples_per_s": batch * world / (ms / 1e3)}
+    if stage_ms is not None and model.tiles:
+        # the reference's scheduler (simulate.cpp:65-159 via
+        # costmodel.predict_iteration) fed with this run's measured per-layer
+        # GEMM chain times and per-bucket comm-only stage times, against the
+        # measured graph-replayed steps. Same buckets for both policies (same
+        # fusion buffer); WFBP's all-reduce = RS + AG.
+        from paper_2302_12445_b200 import costmodel
+
+        L = model.L
+        t_ff = [model.tiles["ff"]["us"] * 1e-6] * L
+        t_bp = [model.tiles["bp_group_us"] * 1e-6] * L
+        lb = [4 * n for n in model.numels]
+        rs = [x[0] * 1e-3 for x in stage_ms]
+        ag = [x[1] * 1e-3 for x in stage_ms]
+        pred = {}
+        for policy in (a.policy, a.baseline_policy):
+            gd = bool(a.group_dependency) and policy.startswith("DEAR")
+            sim = costmodel.predict_iteration(lb, t_ff, t_bp, policy, ab.buffer, world, 0.0, 0.0,
+                                              group_dependency=gd, rs_times=rs, ag_times=ag)
+            meas = res[policy]["ms_per_step"]
+            pred[policy] = {"predicted_ms": sim["iteration_seconds"] * 1e3, "measured_ms": meas,
+                            "measured_over_predicted": meas / (sim["iteration_seconds"] * 1e3)}
+        pred["predicted_dear_over_wfbp"] = (pred[a.baseline_policy]["predicted_ms"] /
+                                            pred[a.policy]["predicted_ms"])
+        res["simulated"] = pred
     return res
 
 

@@ -117,7 +117,10 @@ def predict_iteration(layer_bytes, t_ff, t_bp, policy: str, buffer_bytes: int, P
     order = 0
     if policy.startswith("WFBP"):
         for gi, (lo, hi) in enumerate(plan):
-            t = add("AR", gi + 1, all_reduce_time(gbytes[gi], P, alpha, beta), deps_bp[gi], order)
+            # measured stage times: the all-reduce is RS + AG
+            t_ar = (rs_times[gi] + ag_times[gi] if rs_times is not None and ag_times is not None
+                    else all_reduce_time(gbytes[gi], P, alpha, beta))
+            t = add("AR", gi + 1, t_ar, deps_bp[gi], order)
             order += 1
             for l in range(lo, hi + 1):
                 tasks[ff[l]][3].append(t)
