@@ -244,6 +244,18 @@ __device__ __forceinline__ void walk_slice(const Unit* __restrict__ units,
   for (int i = b.id; i < n_slices; i += b.n) walk_one(units, slices[i], f);
 }
 
+// --------------------------------------- programmatic dependent launch ----
+// The local bucket kernels (pack / update / unpack / direct update) launch
+// with programmatic stream serialization: each lets the next kernel of the
+// stream start as its own CTAs retire (launch_dependents at entry), and waits
+// (griddepcontrol.wait: the previous grid completed and its writes are
+// visible) before touching memory — the next launch's ramp overlaps this
+// one's tail. DEAR_PDL=0 launches them plainly.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ------------------------------------------------------ peer signalling ----
 __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
   uint32_t v;
@@ -343,6 +355,7 @@ __global__ void __launch_bounds__(kThreads, (kSignal && kPeerPackLight) ? 1 : DE
                                                            const Slice* __restrict__ slices,
                                                            float scale, BucketFlags* flags,
                                                            PeerArgs pa, int n_slices) {
+  if (!kSignal) pdl_enter();
   // Peer backend: our slots may be rewritten once every peer gathered them.
   if (kSignal) cta_wait_peers(&flags->packed, &flags->gathered, pa);
   walk_slice(units, slices, n_slices, [&](const Unit& U, int64_t off, int64_t n) {
@@ -384,6 +397,7 @@ __global__ void __launch_bounds__(kThreads, DEAR_UPD_CTAS_PER_SM) update_kernel(
                                                              const Slice* __restrict__ slices,
                                                              const HyperParams* __restrict__ hpp,
                                                              int has_buf) {
+  pdl_enter();
   const HyperParams hp = *hpp;
   walk_slice(units, slices, kUpdSlices, [&](const Unit& U, int64_t off, int64_t n) {
     const float* w = U.a + off;
@@ -419,6 +433,7 @@ template <bool kWd, bool kShadow>
 __global__ void __launch_bounds__(kThreads, DEAR_DIR_CTAS_PER_SM) update_direct_kernel(
     const Unit* __restrict__ units, const Slice* __restrict__ slices,
     const HyperParams* __restrict__ hpp) {
+  pdl_enter();
   const HyperParams hp = *hpp;
   walk_slice(units, slices, kDirSlices, [&](const Unit& U, int64_t off, int64_t n) {
     const float* g = U.a + off;
@@ -456,6 +471,7 @@ __global__ void __launch_bounds__(kThreads, DEAR_DIR_CTAS_PER_SM) update_direct_
 template <bool kShadow>
 __global__ void __launch_bounds__(kThreads, DEAR_UNPACK_CTAS_PER_SM) unpack_kernel(const Unit* __restrict__ units,
                                                              const Slice* __restrict__ slices) {
+  pdl_enter();
   walk_slice(units, slices, kUnpackSlices, [&](const Unit& U, int64_t off, int64_t n) {
     const float* src = U.a + off;
     float* dst = U.b + off;
@@ -1205,6 +1221,30 @@ __global__ void hash_kernel(const float* __restrict__ x, int64_t n, uint64_t sal
 // Grid of the bucket kernels: kSlices (one slice per CTA) unless
 // DEAR_BUCKET_CTAS caps it (CTAs then walk several slices), which leaves SMs
 // to concurrently running GEMMs.
+bool pdl_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("DEAR_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// <<<grid, kThreads, 0, s>>> with programmatic stream serialization.
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*k)(KArgs...), int grid, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_on() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
 int bucket_grid(int n_slices, int want = 0) {
   static int cap = [] {
     const char* e = std::getenv("DEAR_BUCKET_CTAS");
@@ -1219,8 +1259,8 @@ int bucket_grid(int n_slices, int want = 0) {
 cudaError_t launch_pack(const Unit* units, const Slice* slices, int64_t total, float scale,
                         int grid, cudaStream_t s) {
   if (total <= 0) return cudaSuccess;
-  pack_kernel<false><<<bucket_grid(kPackSlices, grid), kThreads, 0, s>>>(units, slices, scale, nullptr,
-                                                                         PeerArgs{}, kPackSlices);
+  launch_pdl(pack_kernel<false>, bucket_grid(kPackSlices, grid), s, units, slices, scale,
+             static_cast<BucketFlags*>(nullptr), PeerArgs{}, kPackSlices);
   return cudaGetLastError();
 }
 
@@ -1427,13 +1467,13 @@ cudaError_t launch_update(const Unit* units, const Slice* slices, int64_t total,
   if (total <= 0) return cudaSuccess;
   const int ug = bucket_grid(kUpdSlices, grid);
   if (use_momentum && use_wd)
-    update_kernel<true, true><<<ug, kThreads, 0, s>>>(units, slices, hp, has_momentum_buf);
+    launch_pdl(update_kernel<true, true>, ug, s, units, slices, hp, has_momentum_buf);
   else if (use_momentum)
-    update_kernel<true, false><<<ug, kThreads, 0, s>>>(units, slices, hp, has_momentum_buf);
+    launch_pdl(update_kernel<true, false>, ug, s, units, slices, hp, has_momentum_buf);
   else if (use_wd)
-    update_kernel<false, true><<<ug, kThreads, 0, s>>>(units, slices, hp, has_momentum_buf);
+    launch_pdl(update_kernel<false, true>, ug, s, units, slices, hp, has_momentum_buf);
   else
-    update_kernel<false, false><<<ug, kThreads, 0, s>>>(units, slices, hp, has_momentum_buf);
+    launch_pdl(update_kernel<false, false>, ug, s, units, slices, hp, has_momentum_buf);
   return cudaGetLastError();
 }
 
@@ -1442,9 +1482,9 @@ cudaError_t launch_unpack(const Unit* units, const Slice* slices, int64_t total,
   if (total <= 0) return cudaSuccess;
   const int ug = bucket_grid(kUnpackSlices, grid);
   if (with_shadow)
-    unpack_kernel<true><<<ug, kThreads, 0, s>>>(units, slices);
+    launch_pdl(unpack_kernel<true>, ug, s, units, slices);
   else
-    unpack_kernel<false><<<ug, kThreads, 0, s>>>(units, slices);
+    launch_pdl(unpack_kernel<false>, ug, s, units, slices);
   return cudaGetLastError();
 }
 
@@ -1454,13 +1494,13 @@ cudaError_t launch_update_direct(const Unit* units, const Slice* slices, int64_t
   if (total <= 0) return cudaSuccess;
   const int grid = bucket_grid(kDirSlices);
   if (use_wd && with_shadow)
-    update_direct_kernel<true, true><<<grid, kThreads, 0, s>>>(units, slices, hp);
+    launch_pdl(update_direct_kernel<true, true>, grid, s, units, slices, hp);
   else if (use_wd)
-    update_direct_kernel<true, false><<<grid, kThreads, 0, s>>>(units, slices, hp);
+    launch_pdl(update_direct_kernel<true, false>, grid, s, units, slices, hp);
   else if (with_shadow)
-    update_direct_kernel<false, true><<<grid, kThreads, 0, s>>>(units, slices, hp);
+    launch_pdl(update_direct_kernel<false, true>, grid, s, units, slices, hp);
   else
-    update_direct_kernel<false, false><<<grid, kThreads, 0, s>>>(units, slices, hp);
+    launch_pdl(update_direct_kernel<false, false>, grid, s, units, slices, hp);
   return cudaGetLastError();
 }
 
