@@ -179,6 +179,14 @@ int dear_join(dear_ctx* ctx, void* stream);
  * fully updated ("forced to synchronize ... before evaluating"). */
 int dear_synchronize(dear_ctx* ctx);
 
+/* Failure detection: *failed = 1 when the NCCL communicator
+ * reported an asynchronous error (ncclCommGetAsyncError). dear_synchronize
+ * polls the same while it waits, and with DEAR_SYNC_TIMEOUT_S set also bounds
+ * the wait; either way it aborts the communicator (ncclCommAbort) and returns
+ * DEAR_EINTERNAL instead of hanging. The NVLink peer / NVLS kernels bound
+ * their cross-GPU waits with DEAR_PEER_TIMEOUT_S (default 600 s; they trap). */
+int dear_comm_error(dear_ctx* ctx, int32_t* failed);
+
 int dear_destroy(dear_ctx* ctx);
 
 /* Learning-rate change (device-resident; CUDA-graph safe). */

@@ -89,6 +89,7 @@ _SIGNATURES = {
     "dear_symm_destroy": [_P],
     "dear_nvls_connect": [_P, _P],
     "dear_nvls_enabled": [_P, C.POINTER(C.c_int32)],
+    "dear_comm_error": [_P, C.POINTER(C.c_int32)],
 }
 DEAR_PEER_HANDLE_BYTES = 256
 

@@ -21,7 +21,9 @@
 #include <string.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdlib>
+#include <thread>
 #include <cstdio>
 #include <deque>
 #include <map>
@@ -1274,6 +1276,39 @@ int dear_join(dear_ctx* ctx, void* stream) {
   DEAR_API_END
 }
 
+// Host wait for the comm stream that watches the communicator (SURVEY §5,
+// failure detection): NCCL reports a peer's failure asynchronously
+// (ncclCommGetAsyncError) while its kernels may never finish, so poll both;
+// on an error, or after DEAR_SYNC_TIMEOUT_S seconds (0 / unset = no limit),
+// abort the communicator (ncclCommAbort unblocks its kernels) and fail with
+// DEAR_EINTERNAL instead of hanging.
+static void wait_comm_stream(dear_ctx& c) {
+  if (!c.comm) {
+    cuda_check(cudaStreamSynchronize(c.comm_stream), "cudaStreamSynchronize");
+    return;
+  }
+  const char* e = std::getenv("DEAR_SYNC_TIMEOUT_S");
+  const double limit = e ? std::atof(e) : 0.0;
+  const auto t0 = std::chrono::steady_clock::now();
+  for (unsigned spin = 0;; ++spin) {
+    const cudaError_t q = cudaStreamQuery(c.comm_stream);
+    if (q == cudaSuccess) return;
+    if (q != cudaErrorNotReady) cuda_check(q, "comm stream");
+    ncclResult_t async = ncclSuccess;
+    nccl_check(ncclCommGetAsyncError(c.comm, &async), "ncclCommGetAsyncError");
+    const double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if ((async != ncclSuccess && async != ncclInProgress) || (limit > 0.0 && s > limit)) {
+      const std::string why = async != ncclSuccess && async != ncclInProgress
+                                  ? std::string("NCCL reported ") + ncclGetErrorString(async)
+                                  : "no progress within DEAR_SYNC_TIMEOUT_S";
+      ncclCommAbort(c.comm);
+      c.comm = nullptr;
+      throw Error(DEAR_EINTERNAL, "dear_synchronize: " + why + "; communicator aborted");
+    }
+    if (spin > 64) std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+}
+
 int dear_synchronize(dear_ctx* ctx) {
   DEAR_API_BEGIN
   need(ctx, true);
@@ -1286,7 +1321,20 @@ int dear_synchronize(dear_ctx* ctx) {
   else if (ctx->ags_deferred) {
     ctx->enqueue_feedpipe(ctx->compute);
   }
-  cuda_check(cudaStreamSynchronize(ctx->comm_stream), "cudaStreamSynchronize");
+  wait_comm_stream(*ctx);
+  DEAR_API_END
+}
+
+int dear_comm_error(dear_ctx* ctx, int32_t* failed) {
+  DEAR_API_BEGIN
+  need(ctx, true);
+  if (!failed) invalid("dear_comm_error: null output");
+  *failed = 0;
+  if (ctx->comm) {
+    ncclResult_t async = ncclSuccess;
+    nccl_check(ncclCommGetAsyncError(ctx->comm, &async), "ncclCommGetAsyncError");
+    if (async != ncclSuccess && async != ncclInProgress) *failed = 1;
+  }
   DEAR_API_END
 }
 

@@ -20,7 +20,7 @@ from typing import Optional
 
 import torch
 
-from ._lib import DEAR_PEER_HANDLE_BYTES, POLICIES, DearCfg, check, lib
+from ._lib import DEAR_PEER_HANDLE_BYTES, POLICIES, DearCfg, DearError, check, lib
 
 
 def _dist_ready() -> bool:
@@ -226,6 +226,7 @@ class Runtime:
         self.policy = policy
         self.backend = backend
         self._group = comm if isinstance(comm, LocalGroup) else None
+        self._comm_obj = comm if isinstance(comm, Communicator) else None
         self._heap = heap
         cfg = DearCfg(POLICIES[policy], int(fusion_buffer_bytes) if "FUSED" in policy else 0,
                       int(dear_group_dependency), float(lr),
@@ -313,7 +314,18 @@ class Runtime:
         check(lib().dear_join(self._ctx, _stream_ptr(stream)))
 
     def synchronize(self) -> None:
-        check(lib().dear_synchronize(self._ctx))
+        try:
+            check(lib().dear_synchronize(self._ctx))
+        except DearError as e:
+            if "communicator aborted" in str(e) and self._comm_obj is not None:
+                self._comm_obj._comm = C.c_void_p()  # freed by ncclCommAbort
+            raise
+
+    def comm_failed(self) -> bool:
+        """The NCCL communicator reported an asynchronous error (dear_comm_error)."""
+        bad = C.c_int32(0)
+        check(lib().dear_comm_error(self._ctx, C.byref(bad)))
+        return bool(bad.value)
 
     def set_lr(self, lr: float) -> None:
         check(lib().dear_set_lr(self._ctx, float(lr)))
