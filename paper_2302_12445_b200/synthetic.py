@@ -161,7 +161,7 @@ class SyntheticModel:
         split0 = self.wgrad[0].info()["splits"]
         num_kb = (T + 63) // 64
         splits = ([self.wgrad_split] if self.wgrad_split > 0 else
-                  sorted({x for x in (split0, 4, 6, 10) if 1 <= x <= num_kb}))
+                  sorted({x for x in (split0, 4, 6, 8, 10, 12, 16) if 1 <= x <= num_kb}))
 
         def bp_real(i):
             if i == 0:
@@ -180,7 +180,9 @@ class SyntheticModel:
         # or red.add), dgrad at its best chain tile
         max_bn = int(os.environ.get("DEAR_GEMM_MAX_BN", "256"))  # see gemm.tile_candidates
         wtiles = list(dict.fromkeys([c[1:] for c in wg[:2]] +
-                                    [t for t in ((128, 0), (176, 0), (256, 0)) if t[0] <= max_bn]))
+                                    [t for t in ((128, 0), (176, 0), (256, 0), (128, 1),
+                                                 (256, 1)) if t[0] <= max_bn and
+                                     (t[1] == 0 or R > 128)]))
         trials = []
         for wc in wtiles:
             for sp in splits:
