@@ -23,18 +23,36 @@ sys.path.insert(0, ROOT)
 
 
 def nvlink_kib(index: int) -> tuple[int, int]:
-    """Cumulative NVLink data TX / RX (KiB) over all links of GPU `index`."""
+    """Cumulative NVLink TX / RX bytes over all links of GPU `index`: the per-link
+    NVLINK_COUNT_XMIT/RCV_BYTES fields (Blackwell), else the device-wide
+    THROUGHPUT_DATA / THROUGHPUT_RAW counters (KiB)."""
     import pynvml as N
 
     h = N.nvmlDeviceGetHandleByIndex(index)
-    vals = N.nvmlDeviceGetFieldValues(h, [N.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX,
-                                          N.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX])
-    out = []
-    for v in vals:
-        if v.nvmlReturn != 0:
-            raise RuntimeError(f"NVML field read failed ({v.nvmlReturn})")
-        out.append(int(v.value.ullVal))
-    return out[0], out[1]
+    links = int(getattr(N, "NVML_NVLINK_MAX_LINKS", 18))
+    tx = rx = 0
+    ok = False
+    for link in range(links):
+        try:
+            vals = N.nvmlDeviceGetFieldValues(h, [(N.NVML_FI_DEV_NVLINK_COUNT_XMIT_BYTES, link),
+                                                  (N.NVML_FI_DEV_NVLINK_COUNT_RCV_BYTES, link)])
+        except Exception:
+            break
+        if any(v.nvmlReturn != 0 for v in vals):
+            continue
+        ok = True
+        tx += int(vals[0].value.ullVal)
+        rx += int(vals[1].value.ullVal)
+    if ok:
+        nvlink_kib.source = "NVML NVLINK_COUNT_XMIT/RCV_BYTES, summed over links"
+        return tx, rx
+    for ftx, frx in ((N.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX, N.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX),
+                     (N.NVML_FI_DEV_NVLINK_THROUGHPUT_RAW_TX, N.NVML_FI_DEV_NVLINK_THROUGHPUT_RAW_RX)):
+        vals = N.nvmlDeviceGetFieldValues(h, [ftx, frx])
+        if all(v.nvmlReturn == 0 for v in vals):
+            nvlink_kib.source = f"NVML field {ftx}/{frx} (KiB)"
+            return int(vals[0].value.ullVal) * 1024, int(vals[1].value.ullVal) * 1024
+    raise RuntimeError("no NVLink byte counter is readable through NVML on this GPU")
 
 
 def main():
@@ -93,7 +111,7 @@ def main():
         torch.cuda.synchronize()
         tx1, rx1 = nvlink_kib(lr)
         dist.barrier()
-        t = torch.tensor([(tx1 - tx0) * 1024.0 / a.iters, (rx1 - rx0) * 1024.0 / a.iters,
+        t = torch.tensor([(tx1 - tx0) * 1.0 / a.iters, (rx1 - rx0) * 1.0 / a.iters,
                           e0.elapsed_time(e1) / a.iters], device="cuda", dtype=torch.float64)
         allv = [torch.zeros_like(t) for _ in range(P)]
         dist.all_gather(allv, t)
@@ -112,7 +130,7 @@ def main():
                 "rx_bytes_per_iter": [v[1].item() for v in allv],
                 "comm_ms_per_iter": max(v[2].item() for v in allv),
                 "alg_bytes_per_gpu_ring_convention": alg,
-                "source": "NVML NVLINK_THROUGHPUT_DATA_TX/RX counters (KiB), all links"}),
+                "source": nvlink_kib.source}),
                 flush=True)
     comm.close()
     dist.destroy_process_group()
