@@ -158,6 +158,10 @@ class Reference:
         lib.ref_simulate_json.restype = C.c_void_p
         lib.ref_simulate_json.argtypes = [_i64p, C.c_int, _f64p, _f64p, C.c_int, C.c_int64,
                                           C.c_int, C.c_int, C.c_double, C.c_double]
+        lib.ref_simulate_json_ex.restype = C.c_void_p
+        lib.ref_simulate_json_ex.argtypes = [_i64p, C.c_int, _f64p, _f64p, C.c_int, C.c_int64,
+                                             C.c_int, C.c_int, C.c_double, C.c_double,
+                                             C.c_int64, C.c_int, C.c_int]
         lib.ref_free.argtypes = [C.c_void_p]
         lib.ref_time_sgd_steps.argtypes = [_i64p, C.c_int, C.c_int, C.c_int, C.c_int,
                                            C.c_uint64, C.c_double, _f64p]
@@ -233,13 +237,15 @@ class Reference:
 
     def simulate(self, counts, t_ff, t_bp, policy: str, fusion_buffer_bytes: int = 0,
                  group_dependency: bool = False, workers: int = 2, alpha: float = 0.0,
-                 beta: float = 0.0) -> dict:
+                 beta: float = 0.0, partition_bytes: int = 0, negotiation_rounds: int = 1,
+                 negotiation_floating: bool = False) -> dict:
         c = np.ascontiguousarray(counts, np.int64)
         tf = np.ascontiguousarray(t_ff, np.float64)
         tb = np.ascontiguousarray(t_bp, np.float64)
-        p = self.lib.ref_simulate_json(c, len(c), tf, tb, self.POLICY[policy],
-                                       fusion_buffer_bytes, int(group_dependency), workers,
-                                       alpha, beta)
+        p = self.lib.ref_simulate_json_ex(c, len(c), tf, tb, self.POLICY[policy],
+                                          fusion_buffer_bytes, int(group_dependency), workers,
+                                          alpha, beta, int(partition_bytes),
+                                          int(negotiation_rounds), int(negotiation_floating))
         if not p:
             raise ValueError(self.lib.ref_last_error().decode())
         try:

@@ -196,15 +196,32 @@ int ref_sgd_step_replicas(int P, int64_t d, double lr, const double* w_in, const
 // ref_free) listing tasks (id, label, kind, subject, group_subject,
 // issue_order, duration, deps, resource, start, end) and the makespan.
 // policy: 0 WFBP, 1 WFBP_FUSED, 2 PRIORITY_PARTITION, 3 DEAR, 4 DEAR_FUSED.
+char* ref_simulate_json_ex(const int64_t* counts, int L, const double* t_ff, const double* t_bp,
+                           int policy, int64_t fusion_buffer_bytes, int group_dependency,
+                           int workers, double alpha, double beta, int64_t partition_bytes,
+                           int negotiation_rounds, int negotiation_floating);
+
 char* ref_simulate_json(const int64_t* counts, int L, const double* t_ff, const double* t_bp,
                         int policy, int64_t fusion_buffer_bytes, int group_dependency,
                         int workers, double alpha, double beta) {
+  return ref_simulate_json_ex(counts, L, t_ff, t_bp, policy, fusion_buffer_bytes,
+                              group_dependency, workers, alpha, beta, 0, 1, 0);
+}
+
+// Same, with PolicySpec's PRIORITY_PARTITION fields (policy.hpp:36-45).
+char* ref_simulate_json_ex(const int64_t* counts, int L, const double* t_ff, const double* t_bp,
+                           int policy, int64_t fusion_buffer_bytes, int group_dependency,
+                           int workers, double alpha, double beta, int64_t partition_bytes,
+                           int negotiation_rounds, int negotiation_floating) {
   try {
     const ModelSpec m = model_from_counts(counts, L, 4, t_ff, t_bp);
     PolicySpec p;
     p.kind = static_cast<PolicyKind>(policy);
     p.fusion_buffer_bytes = fusion_buffer_bytes;
     p.dear_group_dependency = group_dependency != 0;
+    p.partition_bytes = partition_bytes;
+    p.negotiation_rounds = negotiation_rounds;
+    p.negotiation_floating = negotiation_floating != 0;
     const ClusterSpec c{"capi", workers, alpha, beta};
     const TaskGraph g = build_graph(m, p, c);
     const Timeline tl = simulate(g);
@@ -239,6 +256,10 @@ char* ref_simulate_json(const int64_t* counts, int L, const double* t_ff, const 
       put(by[i]->start);
       os += ",\"end\":";
       put(by[i]->end);
+      os += ",\"part\":";
+      puti(t.part);
+      os += ",\"release\":";
+      put(t.release_delay);
       os += ",\"deps\":[";
       for (std::size_t k = 0; k < t.deps.size(); ++k) {
         if (k) os += ",";

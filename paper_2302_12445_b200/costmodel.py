@@ -83,9 +83,24 @@ def exposed_comm(iteration: float, t_ff_total: float, t_bp_total: float) -> floa
     return max(0.0, iteration - t_ff_total - t_bp_total)
 
 
+def partition_plan(layer_bytes, partition_bytes: int):
+    """PRIORITY_PARTITION parts (task_graph.cpp:215-258): layer l (L down to 1)
+    in ceil(bytes / partition_bytes) parts (one part for an empty layer);
+    returns [(layer, parts)] in that order."""
+    if partition_bytes <= 0:
+        raise ValueError("PRIORITY_PARTITION requires partition_bytes > 0")
+    out = []
+    for l in range(len(layer_bytes), 0, -1):
+        b = int(layer_bytes[l - 1])
+        out.append((l, 1 if b == 0 else (b + partition_bytes - 1) // partition_bytes))
+    return out
+
+
 def predict_iteration(layer_bytes, t_ff, t_bp, policy: str, buffer_bytes: int, P: int,
                       alpha: float, beta: float, group_dependency: bool = False,
-                      rs_times=None, ag_times=None) -> dict:
+                      rs_times=None, ag_times=None, partition_bytes: int = 0,
+                      negotiation_rounds: int = 1, negotiation_floating: bool = False,
+                      ar_times=None) -> dict:
     """Simulated steady-state iteration (seconds) of one worker: BP_L..BP_1 and
     FF_1..FF_L on the compute stream, RS/AG/AR on the comm stream, issue order
     and dependencies of task_graph.cpp:127-210, non-preemptive list
@@ -97,10 +112,11 @@ def predict_iteration(layer_bytes, t_ff, t_bp, policy: str, buffer_bytes: int, P
     +g = RS / AR of group g, -g = AG of group g, 1-based), the input of
     Runtime.set_comm_order."""
     L = len(layer_bytes)
-    tasks = []  # (kind, subject, duration, deps, order, resource)
+    tasks = []  # (kind, subject, duration, deps, order, resource, release, part)
 
-    def add(kind, subj, dur, deps, order):
-        tasks.append([kind, subj, dur, list(deps), order, 0 if kind in ("FF", "BP") else 1])
+    def add(kind, subj, dur, deps, order, release=0.0, part=0):
+        tasks.append([kind, subj, dur, list(deps), order, 0 if kind in ("FF", "BP") else 1,
+                      release, part])
         return len(tasks) - 1
 
     bp, ff, order = [0] * (L + 2), [0] * (L + 2), 0
@@ -115,7 +131,32 @@ def predict_iteration(layer_bytes, t_ff, t_bp, policy: str, buffer_bytes: int, P
     gbytes = [sum(layer_bytes[lo - 1:hi]) for lo, hi in plan]
     deps_bp = [[bp[l] for l in range(hi, lo - 1, -1)] for lo, hi in plan]
     order = 0
-    if policy.startswith("WFBP"):
+    part_ids = {}  # PRIORITY_PARTITION: AR task id -> 1-based part bucket (plan order)
+    if policy == "PRIORITY_PARTITION":
+        # add_priority_partition (task_graph.cpp:215-258): per layer, parts in
+        # issue priority (l-1)*stride + k (ascending layer = feed-forward order),
+        # each after a negotiation (on the comm stream, or as a release delay
+        # when floating).
+        parts = partition_plan(layer_bytes, partition_bytes)
+        stride = max(n for _, n in parts) + 1
+        neg = float(negotiation_rounds) * 2.0 * (float(P) - 1.0) * alpha
+        g = 0
+        for l, n in parts:
+            part_b = float(layer_bytes[l - 1]) / n
+            for k in range(n):
+                g += 1
+                issue = (l - 1) * stride + k
+                dur = (ar_times[g - 1] if ar_times is not None
+                       else all_reduce_time(part_b, P, alpha, beta))
+                if negotiation_floating:
+                    t = add("AR", l, dur, [bp[l]], issue, release=neg, part=k + 1)
+                else:
+                    nt = add("NEGOTIATE", l, neg, [bp[l]], issue, part=k + 1)
+                    t = add("AR", l, dur, [nt], issue, part=k + 1)
+                part_ids[t] = g
+                tasks[ff[l]][3].append(t)
+        plan = [(l, l) for l, _ in parts]
+    elif policy.startswith("WFBP"):
         for gi, (lo, hi) in enumerate(plan):
             # measured stage times: the all-reduce is RS + AG
             t_ar = (rs_times[gi] + ag_times[gi] if rs_times is not None and ag_times is not None
@@ -152,7 +193,7 @@ def predict_iteration(layer_bytes, t_ff, t_bp, policy: str, buffer_bytes: int, P
     for i, t in enumerate(tasks):
         for d in t[3]:
             dependents[d].append(i)
-    ev = [(0.0, 1, i) for i in range(n) if not tasks[i][3]]
+    ev = [(tasks[i][6], 1, i) for i in range(n) if not tasks[i][3]]
     heapq.heapify(ev)
     ready, running, end_at = [[], []], [-1, -1], [0.0] * n
     done = 0
@@ -168,20 +209,27 @@ def predict_iteration(layer_bytes, t_ff, t_bp, policy: str, buffer_bytes: int, P
                     finish[j] = max(finish[j], now)
                     remaining[j] -= 1
                     if remaining[j] == 0:
-                        heapq.heappush(ev, (finish[j], 1, j))
+                        heapq.heappush(ev, (finish[j] + tasks[j][6], 1, j))
             else:
                 heapq.heappush(ready[tasks[i][5]], (tasks[i][4], i))
         for r in (0, 1):
             if running[r] == -1 and ready[r]:
                 _, i = heapq.heappop(ready[r])
                 running[r] = i
-                if r == 1 and tasks[i][0] != "BARRIER":
+                if r == 1 and tasks[i][0] == "AR" and part_ids:
+                    dispatched.append(part_ids[i])
+                elif r == 1 and tasks[i][0] not in ("BARRIER", "NEGOTIATE"):
                     dispatched.append(-tasks[i][1] if tasks[i][0] == "AG" else tasks[i][1])
                 end_at[i] = now + tasks[i][2]
                 heapq.heappush(ev, (end_at[i], 0, i))
     if done != n:
         raise RuntimeError("simulate: cycle detected")
     it = max(end_at)
-    return {"iteration_seconds": it, "buckets": len(plan),
+    labels = {}
+    for i, t in enumerate(tasks):
+        if t[0] in ("AR", "NEGOTIATE") and t[7] > 0:
+            labels[i] = f"{t[0]} l{t[1]} p{t[7]}"
+    return {"iteration_seconds": it, "buckets": len(part_ids) if part_ids else len(plan),
+            "start": [end_at[i] - tasks[i][2] for i in range(n)], "part_labels": labels,
             "exposed_comm_seconds": exposed_comm(it, float(sum(t_ff)), float(sum(t_bp))),
             "comm_order": dispatched}

@@ -108,3 +108,36 @@ def test_comm_order_with_measured_stage_times():
     assert slow["comm_order"] == list(range(1, G + 1)) + [-g for g in range(G, 0, -1)]
     # comm much faster than backprop: each AG right behind its RS
     assert fast["comm_order"] == [v for g in range(1, G + 1) for v in (g, -g)]
+
+
+def test_priority_partition_matches_reference_build(reference):
+    """PRIORITY_PARTITION (task_graph.cpp:215-258): per-layer parts of
+    ceil(bytes / partition_bytes), each behind a negotiation (or a floating
+    release delay), issued by ascending layer. The restatement's makespan and
+    its AR dispatch sequence equal the reference build's on random models."""
+    import random
+
+    from paper_2302_12445_b200 import costmodel as cm
+
+    rng = random.Random(5)
+    for _ in range(120):
+        L = rng.randint(1, 7)
+        counts = [rng.choice([0, 1, 50, 700, 5000, 12000]) for _ in range(L)]
+        tf = [rng.uniform(0.1, 2) for _ in range(L)]
+        tb = [rng.uniform(0.1, 3) for _ in range(L)]
+        pb = rng.choice([1000, 4096, 8000, 30000])
+        nr, fl = rng.randint(0, 2), rng.random() < 0.5
+        P, a, b = rng.choice([2, 4, 8]), rng.choice([0.0, 1e-3]), rng.choice([0.0, 1e-6])
+        ref = reference.simulate(counts, tf, tb, "PRIORITY_PARTITION", 0, workers=P, alpha=a,
+                                 beta=b, partition_bytes=pb, negotiation_rounds=nr,
+                                 negotiation_floating=fl)
+        got = cm.predict_iteration([4 * c for c in counts], tf, tb, "PRIORITY_PARTITION", 0, P,
+                                   a, b, partition_bytes=pb, negotiation_rounds=nr,
+                                   negotiation_floating=fl)
+        assert got["iteration_seconds"] == ref["iteration_seconds"]
+        ref_ar = [t["label"] for t in sorted(ref["tasks"], key=lambda t: (t["start"], t["id"]))
+                  if t["kind"] == "AR"]
+        parts = [(l, k + 1) for l, n in cm.partition_plan([4 * c for c in counts], pb)
+                 for k in range(n)]
+        got_ar = ["AR l%d p%d" % parts[g - 1] for g in got["comm_order"]]
+        assert got_ar == ref_ar
