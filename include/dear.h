@@ -31,10 +31,13 @@ extern "C" {
 #define DEAR_EINVAL 1
 #define DEAR_EINTERNAL 2
 
-/* PolicyKind (policy.hpp:34), same numbering. PRIORITY_PARTITION (2) is out of
- * scope for the runtime and rejected with DEAR_EINVAL. */
+/* PolicyKind (policy.hpp:34), same numbering. PRIORITY_PARTITION (the
+ * ByteScheduler baseline, task_graph.cpp:215-258): every layer's all-reduce in
+ * ceil(bytes / partition_bytes) parts, dispatched by ascending layer (the
+ * order the forward consumes them) instead of gradient-readiness order. */
 #define DEAR_POLICY_WFBP 0
 #define DEAR_POLICY_WFBP_FUSED 1
+#define DEAR_POLICY_PRIORITY_PARTITION 2
 #define DEAR_POLICY_DEAR 3
 #define DEAR_POLICY_DEAR_FUSED 4
 
@@ -57,6 +60,7 @@ typedef struct {
   int32_t defer_allgather;      /* 1: AGs are enqueued by the next
                                    dear_param_wait (CUDA-graph friendly);
                                    0: by dear_step */
+  int64_t partition_bytes;      /* > 0 for PRIORITY_PARTITION (policy.cpp:58-61) */
 } dear_cfg;
 
 /* ---------------------------------------------------------------------------
@@ -170,6 +174,12 @@ int dear_step(dear_ctx* ctx, void* stream);
  * order). Requires a DEAR policy with dear_group_dependency; call between
  * iterations. */
 int dear_set_comm_order(dear_ctx* ctx, const int32_t* seq, int32_t n);
+/* PRIORITY_PARTITION uses the same call: seq lists every part (1-based, plan
+ * order: layer L's parts first) once, in the order the reference scheduler
+ * dispatches them (costmodel.predict_iteration(..., "PRIORITY_PARTITION")
+ * ["comm_order"]); a part is enqueued once it and every part before it in seq
+ * is ready. n = 0: gradient-readiness order. The negotiation of the reference
+ * (a modelled latency) has no runtime counterpart: ranks agree on seq. */
 
 /* `stream` waits for all comm-stream work enqueued so far (graph capture
  * join point). */

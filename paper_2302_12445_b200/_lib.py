@@ -14,7 +14,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, os.environ.get("DEAR_LIB", "libdear.so"))
 
 DEAR_OK, DEAR_EINVAL, DEAR_EINTERNAL = 0, 1, 2
-POLICIES = {"WFBP": 0, "WFBP_FUSED": 1, "DEAR": 3, "DEAR_FUSED": 4}
+POLICIES = {"WFBP": 0, "WFBP_FUSED": 1, "PRIORITY_PARTITION": 2, "DEAR": 3, "DEAR_FUSED": 4}
 
 
 class DearError(RuntimeError):
@@ -40,6 +40,7 @@ class DearCfg(C.Structure):
         ("weight_decay", C.c_double),
         ("nesterov", C.c_int32),
         ("defer_allgather", C.c_int32),
+        ("partition_bytes", C.c_int64),
     ]
 
 

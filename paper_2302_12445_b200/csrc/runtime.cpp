@@ -66,6 +66,7 @@ bool is_fused(int policy) {
 bool is_dear(int policy) {
   return policy == DEAR_POLICY_DEAR || policy == DEAR_POLICY_DEAR_FUSED;
 }
+bool is_pp(int policy) { return policy == DEAR_POLICY_PRIORITY_PARTITION; }
 
 enum OpKind { OP_FENCE_READY, OP_FENCE_STEP, OP_PACK, OP_RS, OP_UPDATE, OP_AG, OP_UNPACK,
               OP_AG_DONE, OP_CALLER_WAIT_PACKED, OP_SET_LR };
@@ -87,11 +88,14 @@ struct LayerReg {
   int64_t numel = -1;
   int bucket = -1;
   int64_t off = 0;  // offset of the layer inside its bucket's flat order
+  int n_parts = 1;  // PRIORITY_PARTITION: buckets bucket .. bucket + n_parts - 1
   bool ready = false;
 };
 
 struct Bucket {
   int low = 0, high = 0;
+  int part = 0;     // PRIORITY_PARTITION: 1-based part of layer `low` (== high)
+  int64_t e0 = 0;   // ... covering elements [e0, e0 + d) of that layer
   int64_t d = 0, stride = 0;
   float* buf = nullptr;  // P * stride: slot r holds chunk (r+1)%P
   float* mom = nullptr;  // stride (own shard's momentum), or null
@@ -254,6 +258,12 @@ cudaEvent_t new_event(bool timing) {
 // chunk.
 template <typename Emit>
 void for_each_piece(const dear_ctx& ctx, const Bucket& B, int64_t cb, int64_t ce, Emit&& emit) {
+  if (B.part > 0) {  // one part of one layer: its elements e0 ..
+    const int64_t s = std::max<int64_t>(0, cb), e = std::min(B.d, ce);
+    for (int64_t p = s; p < e; p += kUnitElems)
+      emit(B.low, B.e0 + p, std::min(kUnitElems, e - p), p - cb);
+    return;
+  }
   for (int l = B.low; l <= B.high; ++l) {
     const LayerReg& L = ctx.layers[static_cast<size_t>(l - 1)];
     const int64_t lb = L.off, le = L.off + L.numel;
@@ -424,6 +434,8 @@ std::string dear_ctx::label(const char* kind, int b) const {
   // task_label (task_graph.cpp:51-58): fused tasks name the group (gi+1);
   // per-layer WFBP names the layer (subject = high_layer, :170).
   const Bucket& B = buckets[static_cast<size_t>(b)];
+  if (B.part > 0)  // task_label: "AR l<layer> p<part>" (task_graph.cpp:51-58)
+    return std::string(kind) + " l" + std::to_string(B.high) + " p" + std::to_string(B.part);
   if (!is_fused(cfg.policy) && !is_dear(cfg.policy)) {
     return std::string(kind) + " l" + std::to_string(B.high);
   }
@@ -667,6 +679,17 @@ void dear_ctx::enqueue_ordered_ags() {
 void dear_ctx::complete_bucket(int b) {
   Bucket& B = buckets[static_cast<size_t>(b)];
   B.complete = true;
+  if (is_pp(cfg.policy) && !comm_order.empty()) {
+    // PRIORITY_PARTITION: the reference scheduler's dispatch sequence; a part
+    // goes once it and every part before it in the sequence is ready.
+    while (order_cursor < comm_order.size() &&
+           buckets[static_cast<size_t>(comm_order[order_cursor] - 1)].complete) {
+      enqueue_backpipe(comm_order[order_cursor] - 1);
+      ++order_cursor;
+      ++rs_cursor;  // parts issued
+    }
+    return;
+  }
   // Issue RS in plan order only (task_graph.cpp:186-194; NCCL ordering).
   while (rs_cursor < static_cast<int>(buckets.size()) &&
          buckets[static_cast<size_t>(rs_cursor)].complete) {
@@ -737,10 +760,11 @@ int dear_local_group_destroy(dear_local_group* group) {
 static void validate_cfg(const dear_cfg* cfg) {
   if (!cfg) invalid("dear_create: cfg is null");
   const int k = cfg->policy;
-  if (k == 2) invalid("PRIORITY_PARTITION is not supported by the runtime");
   if (k != DEAR_POLICY_WFBP && k != DEAR_POLICY_WFBP_FUSED && k != DEAR_POLICY_DEAR &&
-      k != DEAR_POLICY_DEAR_FUSED)
+      k != DEAR_POLICY_DEAR_FUSED && k != DEAR_POLICY_PRIORITY_PARTITION)
     invalid("unknown policy kind " + std::to_string(k));
+  if (is_pp(k) && cfg->partition_bytes <= 0)
+    invalid("PRIORITY_PARTITION requires partition_bytes > 0");
   if (is_fused(k) && cfg->fusion_buffer_bytes <= 0) {
     invalid(std::string(k == DEAR_POLICY_WFBP_FUSED ? "WFBP_FUSED" : "DEAR_FUSED") +
             " requires fusion_buffer_bytes > 0");
@@ -873,26 +897,56 @@ int dear_finalize(dear_ctx* ctx) {
   }
   std::vector<int64_t> bytes(static_cast<size_t>(L));
   for (int i = 0; i < L; ++i) bytes[static_cast<size_t>(i)] = c.layers[static_cast<size_t>(i)].numel * 4;
-  const auto plan = build_plan(bytes, is_fused(c.cfg.policy) ? c.cfg.fusion_buffer_bytes : 0);
+  std::vector<Group> plan;
+  if (is_pp(c.cfg.policy)) {
+    // PRIORITY_PARTITION (task_graph.cpp:215-258): layer L down to 1, each in
+    // ceil(bytes / partition_bytes) parts (one for an empty layer) of balanced
+    // element ranges; every part is its own bucket, all-reduced on its own.
+    for (int l = L; l >= 1; --l) {
+      LayerReg& R = c.layers[static_cast<size_t>(l - 1)];
+      const int64_t b = bytes[static_cast<size_t>(l - 1)];
+      const int64_t parts = b == 0 ? 1 : (b + c.cfg.partition_bytes - 1) / c.cfg.partition_bytes;
+      if (parts > (1 << 20)) invalid("PRIORITY_PARTITION: partition_bytes too small for layer " +
+                                     std::to_string(l));
+      const std::vector<int64_t> pb = chunk_begins(R.numel, static_cast<int>(parts));
+      R.bucket = static_cast<int>(c.buckets.size());
+      R.n_parts = static_cast<int>(parts);
+      R.off = 0;
+      for (int64_t k = 0; k < parts; ++k) {
+        Bucket B;
+        B.low = B.high = l;
+        B.part = static_cast<int>(k + 1);
+        B.e0 = pb[static_cast<size_t>(k)];
+        B.d = pb[static_cast<size_t>(k) + 1] - pb[static_cast<size_t>(k)];
+        B.any_shadow = R.shadow != nullptr;
+        c.buckets.push_back(std::move(B));
+        plan.push_back(Group{l, l});
+      }
+    }
+  } else {
+    plan = build_plan(bytes, is_fused(c.cfg.policy) ? c.cfg.fusion_buffer_bytes : 0);
+    c.buckets.resize(plan.size());
+  }
 
   // Bucket geometry and HBM layout: one arena holding every bucket buffer
   // (P slots of `stride` fp32 each), the momentum shards and the unit tables.
-  c.buckets.resize(plan.size());
   const bool mom = c.cfg.momentum != 0.0;
   size_t floats = 0, units = 0;
   for (size_t g = 0; g < plan.size(); ++g) {
     Bucket& B = c.buckets[g];
-    B.low = plan[g].low;
-    B.high = plan[g].high;
-    int64_t off = 0;
-    for (int l = B.low; l <= B.high; ++l) {
-      LayerReg& R = c.layers[static_cast<size_t>(l - 1)];
-      R.bucket = static_cast<int>(g);
-      R.off = off;
-      off += R.numel;
-      if (R.shadow) B.any_shadow = true;
+    if (B.part == 0) {
+      B.low = plan[g].low;
+      B.high = plan[g].high;
+      int64_t off = 0;
+      for (int l = B.low; l <= B.high; ++l) {
+        LayerReg& R = c.layers[static_cast<size_t>(l - 1)];
+        R.bucket = static_cast<int>(g);
+        R.off = off;
+        off += R.numel;
+        if (R.shadow) B.any_shadow = true;
+      }
+      B.d = off;
     }
-    B.d = off;
     B.stride = slot_stride(B.d, c.P);
     floats += static_cast<size_t>(B.stride) * static_cast<size_t>(c.P) + (mom ? static_cast<size_t>(B.stride) : 0);
   }
@@ -1097,6 +1151,7 @@ int dear_finalize(dear_ctx* ctx) {
   for (const LayerReg& R : c.layers) h = fnv(h, static_cast<uint64_t>(R.numel));
   h = fnv(h, static_cast<uint64_t>(c.cfg.policy));
   h = fnv(h, static_cast<uint64_t>(c.cfg.fusion_buffer_bytes));
+  h = fnv(h, static_cast<uint64_t>(is_pp(c.cfg.policy) ? c.cfg.partition_bytes : 0));
   if (c.local || c.same_dev) {
     for (dear_ctx* o : c.group->ranks) {
       if (o && o != &c && o->finalized) {
@@ -1133,17 +1188,20 @@ int dear_grad_ready(dear_ctx* ctx, int32_t layer, void* stream) {
   R.ready = true;
   ++c.reported;
   if (c.reported == 1) c.trace.clear();
-  Bucket& B = c.buckets[static_cast<size_t>(R.bucket)];
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (std::find(B.ready_streams.begin(), B.ready_streams.end(), s) == B.ready_streams.end())
-    B.ready_streams.push_back(s);
-  if (--B.layers_left == 0) {
-    // All of the bucket's gradients are enqueued: fence each producing stream.
-    while (B.ready_events.size() < B.ready_streams.size()) B.ready_events.push_back(new_event(false));
-    for (size_t i = 0; i < B.ready_streams.size(); ++i)
-      cuda_check(cudaEventRecord(B.ready_events[i], B.ready_streams[i]), "cudaEventRecord");
-    B.ready_events.resize(B.ready_streams.size());
-    c.complete_bucket(R.bucket);
+  // A layer is one bucket's member, or (PRIORITY_PARTITION) n_parts buckets.
+  for (int g = R.bucket; g < R.bucket + R.n_parts; ++g) {
+    Bucket& B = c.buckets[static_cast<size_t>(g)];
+    if (std::find(B.ready_streams.begin(), B.ready_streams.end(), s) == B.ready_streams.end())
+      B.ready_streams.push_back(s);
+    if (--B.layers_left == 0) {
+      // All of the bucket's gradients are enqueued: fence each producing stream.
+      while (B.ready_events.size() < B.ready_streams.size()) B.ready_events.push_back(new_event(false));
+      for (size_t i = 0; i < B.ready_streams.size(); ++i)
+        cuda_check(cudaEventRecord(B.ready_events[i], B.ready_streams[i]), "cudaEventRecord");
+      B.ready_events.resize(B.ready_streams.size());
+      c.complete_bucket(g);
+    }
   }
   DEAR_API_END
 }
@@ -1152,12 +1210,30 @@ int dear_set_comm_order(dear_ctx* ctx, const int32_t* seq, int32_t n) {
   DEAR_API_BEGIN
   need(ctx, true);
   dear_ctx& c = *ctx;
-  if (!is_dear(c.cfg.policy)) invalid("dear_set_comm_order: needs a DEAR policy");
-  if (!c.cfg.dear_group_dependency)
-    invalid("dear_set_comm_order: needs dear_group_dependency (AG_g waits on RS_g only)");
   if (c.reported != 0 || c.ags_deferred)
     invalid("dear_set_comm_order: call between iterations");
   const int G = static_cast<int>(c.buckets.size());
+  if (is_pp(c.cfg.policy)) {
+    // every part once, any order (the scheduler's priority dispatch)
+    if (n == 0) {
+      c.comm_order.clear();
+      c.order_cursor = 0;
+      return DEAR_OK;
+    }
+    if (!seq || n != G) invalid("dear_set_comm_order: PRIORITY_PARTITION needs every part once");
+    std::vector<char> seen(static_cast<size_t>(G), 0);
+    for (int32_t i = 0; i < n; ++i) {
+      if (seq[i] < 1 || seq[i] > G || seen[static_cast<size_t>(seq[i] - 1)])
+        invalid("dear_set_comm_order: PRIORITY_PARTITION needs every part once");
+      seen[static_cast<size_t>(seq[i] - 1)] = 1;
+    }
+    c.comm_order.assign(seq, seq + n);
+    c.order_cursor = 0;
+    return DEAR_OK;
+  }
+  if (!is_dear(c.cfg.policy)) invalid("dear_set_comm_order: needs a DEAR policy");
+  if (!c.cfg.dear_group_dependency)
+    invalid("dear_set_comm_order: needs dear_group_dependency (AG_g waits on RS_g only)");
   if (n == 0) {
     c.comm_order.clear();
     c.order_cursor = c.order_tail = 0;
@@ -1225,6 +1301,7 @@ int dear_step(dear_ctx* ctx, void* stream) {
     B.ready_streams.clear();
   }
   c.rs_cursor = 0;
+  if (is_pp(c.cfg.policy)) c.order_cursor = 0;
   c.reported = 0;
   ++c.iteration;
   DEAR_API_END
@@ -1245,25 +1322,28 @@ int dear_param_wait(dear_ctx* ctx, int32_t layer, void* stream) {
       c.enqueue_feedpipe(static_cast<cudaStream_t>(stream));
     }
   }
-  Bucket& B = c.buckets[static_cast<size_t>(c.layers[static_cast<size_t>(layer - 1)].bucket)];
-  if (!B.ag_live) return DEAR_OK;
+  const LayerReg& R = c.layers[static_cast<size_t>(layer - 1)];
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (B.waited_valid && B.waited == s) return DEAR_OK;
-  // An all-gather recorded in another capture context than this wait (inside
-  // a capture: the previous iteration of a WFBP schedule, or one issued during
-  // the previous graph's backprop under dear_group_dependency; eagerly: one
-  // recorded while capturing the previous graph) is ordered before this work
-  // by that graph's / this capture's trailing dear_join on the caller's
-  // stream. Waiting on it is illegal, so it is dropped.
-  const unsigned long long cap = capture_id(s);
-  if (B.ag_capture != cap) return DEAR_OK;
-  if (c.local) {
-    c.group->drain();
-    if (!c.queue.empty()) invalid("dear_param_wait: local group ranks are out of lock-step");
+  for (int g = R.bucket; g < R.bucket + R.n_parts; ++g) {  // PRIORITY_PARTITION: every part
+    Bucket& B = c.buckets[static_cast<size_t>(g)];
+    if (!B.ag_live) continue;
+    if (B.waited_valid && B.waited == s) continue;
+    // An all-gather recorded in another capture context than this wait (inside
+    // a capture: the previous iteration of a WFBP schedule, or one issued during
+    // the previous graph's backprop under dear_group_dependency; eagerly: one
+    // recorded while capturing the previous graph) is ordered before this work
+    // by that graph's / this capture's trailing dear_join on the caller's
+    // stream. Waiting on it is illegal, so it is dropped.
+    const unsigned long long cap = capture_id(s);
+    if (B.ag_capture != cap) continue;
+    if (c.local) {
+      c.group->drain();
+      if (!c.queue.empty()) invalid("dear_param_wait: local group ranks are out of lock-step");
+    }
+    cuda_check(cudaStreamWaitEvent(s, B.ag_done, 0), "cudaStreamWaitEvent");
+    B.waited = s;
+    B.waited_valid = true;
   }
-  cuda_check(cudaStreamWaitEvent(s, B.ag_done, 0), "cudaStreamWaitEvent");
-  B.waited = s;
-  B.waited_valid = true;
   DEAR_API_END
 }
 

@@ -196,7 +196,7 @@ class Runtime:
                  weight_decay: float = 0.0, nesterov: bool = False,
                  dear_group_dependency: bool = False, defer_allgather: bool = False,
                  backend: str = "auto", stream: Optional[torch.cuda.Stream] = None,
-                 heap: Optional[SymmetricHeap] = None):
+                 heap: Optional[SymmetricHeap] = None, partition_bytes: int = 0):
         if policy not in POLICIES:
             raise ValueError(f"unknown policy kind {policy!r}; expected one of "
                              f"{', '.join(POLICIES)}")
@@ -231,7 +231,7 @@ class Runtime:
         cfg = DearCfg(POLICIES[policy], int(fusion_buffer_bytes) if "FUSED" in policy else 0,
                       int(dear_group_dependency), float(lr),
                       float(momentum), float(dampening), float(weight_decay), int(nesterov),
-                      int(defer_allgather))
+                      int(defer_allgather), int(partition_bytes))
         self._ctx = C.c_void_p()
         sp = _stream_ptr(stream)
         if isinstance(comm, LocalGroup):
@@ -303,9 +303,10 @@ class Runtime:
         check(lib().dear_step(self._ctx, _stream_ptr(stream)))
 
     def set_comm_order(self, seq) -> None:
-        """Comm-stream dispatch sequence for dear_group_dependency
-        (dear_set_comm_order): +g = RS of bucket g, -g = AG of bucket g,
-        1-based plan order; [] restores the default."""
+        """Comm-stream dispatch sequence (dear_set_comm_order). DEAR with
+        dear_group_dependency: +g = RS of bucket g, -g = AG of bucket g, 1-based
+        plan order. PRIORITY_PARTITION: every part g once, in dispatch order.
+        [] restores the default."""
         seq = [int(v) for v in seq]
         arr = (C.c_int32 * max(1, len(seq)))(*seq)
         check(lib().dear_set_comm_order(self._ctx, arr, len(seq)))

@@ -13,6 +13,23 @@ def bucket_plan(numels, policy: str, buffer_bytes: int):
     return fusion_plan([4 * n for n in numels], buffer_bytes if fused else 0)
 
 
+def bucket_ranges(o: Restated, numels, policy: str, buffer_bytes: int, partition_bytes: int = 0):
+    """Flat element ranges [a, b) of the buckets, plan order. PRIORITY_PARTITION:
+    every layer (L down to 1) in ceil(bytes / partition_bytes) balanced parts
+    (task_graph.cpp:215-258; the split follows chunk_ranges)."""
+    offs = np.concatenate([[0], np.cumsum(numels)]).astype(np.int64)
+    if policy == "PRIORITY_PARTITION":
+        out = []
+        for l in range(len(numels), 0, -1):
+            n = int(numels[l - 1])
+            parts = 1 if n == 0 else (4 * n + partition_bytes - 1) // partition_bytes
+            b = o.chunk_ranges(n, parts)
+            out += [(int(offs[l - 1] + b[k]), int(offs[l - 1] + b[k + 1])) for k in range(parts)]
+        return out
+    return [(int(offs[lo - 1]), int(offs[hi])) for lo, hi in bucket_plan(numels, policy,
+                                                                           buffer_bytes)]
+
+
 def seeded_grads(o: Restated, P: int, numels, step: int, seed0: int = 1000) -> np.ndarray:
     """Rank-major [P, D] fp32 gradients, U(-1,1) from the reference tests'
     generator (mt19937_64 + uniform_real_distribution), one seed per step."""
@@ -28,7 +45,7 @@ def initial_weights(o: Restated, numels, seed: int = 77) -> np.ndarray:
 def oracle_run(o: Restated, numels, P: int, steps: int, policy: str, buffer_bytes: int,
                lr: float, momentum=0.0, dampening=0.0, weight_decay=0.0, nesterov=False,
                f32: bool = True, seed0: int = 1000, wseed: int = 77, w0=None, grads_fn=None,
-               lr_schedule=None):
+               lr_schedule=None, partition_bytes: int = 0):
     """Apply the oracle's S-SGD step per fusion bucket (chunk layout is per
     bucket), for `steps` steps. f32=True uses the fp32 ring-order
     restatement (bit-exact target for the local group); f32=False the fp64
@@ -37,18 +54,17 @@ def oracle_run(o: Restated, numels, P: int, steps: int, policy: str, buffer_byte
     w = initial_weights(o, numels, wseed) if w0 is None else w0
     w = np.array(w, dtype=np.float32 if f32 else np.float64)
     bufs = {}
-    plan = bucket_plan(numels, policy, buffer_bytes)
+    ranges = bucket_ranges(o, numels, policy, buffer_bytes, partition_bytes)
     prescale = (P & (P - 1)) == 0
     for s in range(steps):
         g = grads_fn(s) if grads_fn is not None else seeded_grads(o, P, numels, s, seed0)
         if lr_schedule is not None:
             lr = lr_schedule[s]
-        for lo, hi in plan:
-            a, b = offs[lo - 1], offs[hi]
+        for a, b in ranges:
             if b == a:
                 continue
             gb = g[:, a:b]
-            key = (lo, hi)
+            key = (a, b)
             if f32:
                 buf, has = bufs.get(key, (np.zeros(b - a, np.float32), False))
                 nw, nbuf, nhas = o.sgd_step_f32(w[a:b], buf, has, gb, lr, momentum, dampening,
@@ -71,7 +87,8 @@ def run_local(numels, P: int, steps: int, policy: str, buffer_bytes: int, lr: fl
               momentum=0.0, dampening=0.0, weight_decay=0.0, nesterov=False,
               defer_allgather=False, seed0: int = 1000, wseed: int = 77, shadow: bool = False,
               comm_order=None, transport: str = "ring", flat: bool = False,
-              zero_copy: bool = True, w0=None, grads_fn=None, lr_schedule=None):
+              zero_copy: bool = True, w0=None, grads_fn=None, lr_schedule=None,
+              partition_bytes: int = 0):
     """Drive P local-group ranks in lock-step through `steps` iterations of
     backward (layers L..1) + step + forward waits. Returns (params [P, D],
     shadows or None, traces, runtimes-closed).
@@ -104,7 +121,8 @@ def run_local(numels, P: int, steps: int, policy: str, buffer_bytes: int, lr: fl
         rt = Runtime(group, r, P, policy=policy, fusion_buffer_bytes=buffer_bytes, lr=lr,
                      momentum=momentum, dampening=dampening, weight_decay=weight_decay,
                      nesterov=nesterov, defer_allgather=defer_allgather,
-                     dear_group_dependency=comm_order is not None, stream=streams[r])
+                     dear_group_dependency=comm_order is not None and policy.startswith("DEAR"),
+                     stream=streams[r], partition_bytes=partition_bytes)
         ps, gs, ss = [], [], []
         if flat:
             pflat = torch.zeros(aoffs[-1] + 64, device=dev)

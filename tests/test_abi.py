@@ -53,8 +53,9 @@ def test_invalid_arguments_without_gpu():
     ctx = C.c_void_p()
     assert L.dear_create(None, 0, 1, None, C.byref(cfg), C.byref(ctx)) == _lib.DEAR_EINVAL
     assert "requires fusion_buffer_bytes > 0" in L.dear_last_error().decode()
-    cfg = _lib.DearCfg(2, 1, 0, 0.1, 0, 0, 0, 0, 0)
+    cfg = _lib.DearCfg(2, 1, 0, 0.1, 0, 0, 0, 0, 0, 0)  # PRIORITY_PARTITION without parts
     assert L.dear_create(None, 0, 1, None, C.byref(cfg), C.byref(ctx)) == _lib.DEAR_EINVAL
+    assert "PRIORITY_PARTITION requires partition_bytes > 0" in L.dear_last_error().decode()
     cfg = _lib.DearCfg(3, 0, 0, 0.1, 0, 0, 0, 0, 0)
     assert L.dear_create(None, 0, 2, None, C.byref(cfg), C.byref(ctx)) == _lib.DEAR_EINVAL
     assert "NCCL communicator is required" in L.dear_last_error().decode()
@@ -69,4 +70,4 @@ def test_runtime_rejects_unknown_policy():
     from paper_2302_12445_b200 import Runtime
 
     with pytest.raises(ValueError, match="unknown policy"):
-        Runtime(policy="PRIORITY_PARTITION")
+        Runtime(policy="BYTESCHEDULER")

@@ -168,3 +168,41 @@ def test_direct_update_p1_matches_pipeline(restated, monkeypatch, policy, buf):
     assert np.array_equal(sh, sh_ref)
     exp32 = oracle_run(restated, RAGGED, 1, 3, policy, buf, 0.05, f32=True, **kw)
     assert np.array_equal(got[0], exp32)
+
+
+def _pp_order(numels, P, pb):
+    """The reference scheduler's PRIORITY_PARTITION dispatch sequence
+    (task_graph.cpp:215-258 + simulate.cpp:65-159) on nominal times."""
+    from paper_2302_12445_b200 import costmodel as cm
+
+    L = len(numels)
+    return cm.predict_iteration([4 * n for n in numels], [1.0] * L, [2.0] * L,
+                                "PRIORITY_PARTITION", 0, P, 1e-3, 1e-9,
+                                partition_bytes=pb)["comm_order"]
+
+
+@pytest.mark.parametrize("P,transport", [(1, "ring"), (2, "ring"), (3, "ring"), (2, "peer"),
+                                         (4, "peer")])
+@pytest.mark.parametrize("ordered", [False, True])
+def test_priority_partition(restated, P, transport, ordered):
+    """PRIORITY_PARTITION: every layer's all-reduce in ceil(bytes / 40 KB)
+    parts, each its own bucket. Parameters bit-exact with the fp32 ring
+    restatement over the same parts; with the reference scheduler's dispatch
+    sequence the rank's comm trace is exactly that sequence ("AR l<l> p<k>")."""
+    from paper_2302_12445_b200 import costmodel as cm
+
+    pb = 40_000
+    order = _pp_order(RAGGED, P, pb) if ordered else None
+    got, _, traces, same = run_local(RAGGED, P, 3, "PRIORITY_PARTITION", 0, 0.05,
+                                     transport=transport, flat=transport == "peer",
+                                     comm_order=order, partition_bytes=pb, shadow=True)
+    exp32 = oracle_run(restated, RAGGED, P, 3, "PRIORITY_PARTITION", 0, 0.05, f32=True,
+                       partition_bytes=pb)
+    assert all(same)
+    for r in range(P):
+        assert np.array_equal(got[r], exp32)
+    parts = [(l, k + 1) for l, n in cm.partition_plan([4 * n for n in RAGGED], pb)
+             for k in range(n)]
+    seq = order if ordered else list(range(1, len(parts) + 1))
+    assert traces[-1][0] == ["AR l%d p%d" % parts[g - 1] for g in seq]
+    assert len(parts) > len(RAGGED)  # some layers really are split
