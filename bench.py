@@ -79,6 +79,9 @@ def parse():
     ap.add_argument("--extra-workload", default="bert_large",
                     help="also measure DeAR vs WFBP on this workload (north-star "
                          "comparison); 'none' to skip")
+    ap.add_argument("--partition-bytes", type=int, default=4_000_000,
+                    help="PRIORITY_PARTITION ablation (north star, N > 1): part size")
+    ap.add_argument("--no-priority-partition", action="store_true")
     ap.add_argument("--no-parity", action="store_true",
                     help="skip the post-timing oracle parity check of one bucket")
     ap.add_argument("--parity-steps", type=int, default=3)
@@ -921,6 +924,57 @@ def _policy_pair(a, model, comm, world, rank, stream, batch, steps, warm, backen
     return res
 
 
+def _priority_partition(a, model, comm, world, rank, stream, batch, steps, warm):
+    """The ByteScheduler baseline of the reference (PRIORITY_PARTITION,
+    task_graph.cpp:215-258) on the same kernels: every layer's all-reduce in
+    parts of --partition-bytes, dispatched in the order the reference scheduler
+    gives on this run's measured per-layer GEMM times and per-part comm-only
+    stage times (the negotiation has no runtime counterpart)."""
+    import torch
+
+    import paper_2302_12445_b200 as dear
+    from paper_2302_12445_b200 import costmodel
+
+    rt = dear.Runtime(comm, rank, world, policy="PRIORITY_PARTITION", lr=a.lr,
+                      momentum=a.momentum, backend=a.backend, stream=stream,
+                      partition_bytes=a.partition_bytes,
+                      heap=model.heap if a.backend == "nvls" else None)
+    for l in range(1, model.L + 1):
+        rt.register(l, model.params[l - 1], model.grads[l - 1], model.shadows[l - 1])
+    rt.finalize()
+    rt.set_timing(True)
+    for _ in range(3):
+        with torch.cuda.stream(stream):
+            for l in range(1, model.L + 1):
+                rt.param_wait(l, stream)
+            for l in range(model.L, 0, -1):
+                rt.grad_ready(l, stream)
+            rt.step(stream)
+        rt.synchronize()
+    st = rt.timings()
+    rt.set_timing(False)
+    ar = [sum(v for v in (x["pack"], x["rs"], x["update"], x["ag"], x["unpack"]) if v) * 1e-3
+          for x in st]
+    L = model.L
+    t_ff = [model.tiles["ff"]["us"] * 1e-6] * L
+    t_bp = [model.tiles["bp_group_us"] * 1e-6] * L
+    sim = costmodel.predict_iteration([4 * n for n in model.numels], t_ff, t_bp,
+                                      "PRIORITY_PARTITION", 0, world, 0.0, 0.0,
+                                      partition_bytes=a.partition_bytes,
+                                      negotiation_rounds=0, ar_times=ar)
+    order = torch.tensor(sim["comm_order"], dtype=torch.int32, device="cuda")
+    if world > 1:
+        torch.distributed.broadcast(order, 0)
+    rt.set_comm_order(order.cpu().tolist())
+    run = make_runner(Step(model, rt, stream), True, stream)
+    ms = time_loop(run, steps, warm, stream, world > 1)
+    rt.synchronize()
+    rt.close()
+    return {"partition_bytes": a.partition_bytes, "parts": len(st), "ms_per_step": ms,
+            "samples_per_s": batch * world / (ms / 1e3),
+            "predicted_ms": sim["iteration_seconds"] * 1e3}
+
+
 def compare_policies(a, wl_name, comm, world, rank, stream):
     """DeAR vs WFBP (same kernels, same fusion buffer) and compute-only on a
     second workload: the north-star comparison (BERT-Large-shaped layers).
@@ -987,6 +1041,10 @@ def compare_policies(a, wl_name, comm, world, rank, stream):
                                "eq_ratio": eq["baseline"] / eq["dear"] if eq["dear"] else None,
                                "t_ag_over_t_ff": t_ag / t_ff if t_ff else None}
             if be is None:
+                if with_nccl and world > 1 and not a.no_priority_partition:
+                    pp = _priority_partition(a, m, comm, world, rank, stream, batch, steps, warm)
+                    pp["dear_over_pp"] = pp["ms_per_step"] / res[a.policy]["ms_per_step"]
+                    res["priority_partition"] = pp
                 out.update(res)
             else:
                 out[be] = res
