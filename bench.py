@@ -1022,12 +1022,20 @@ def compare_policies(a, wl_name, comm, world, rank, stream):
             extra.append("nvls")
         for be in [None] + extra:
             m = model
-            if be == "nvls":
-                m = SyntheticModel(preset_param_counts(wl["preset"]), wl["hidden"],
-                                   batch * wl["tokens_per_sample"], seed=4321, symmetric=True)
-            res = _policy_pair(a, m, comm, world, rank, stream, batch, steps, warm, be)
-            if m is not model:
-                m.close()
+            try:
+                if be == "nvls":
+                    m = SyntheticModel(preset_param_counts(wl["preset"]), wl["hidden"],
+                                       batch * wl["tokens_per_sample"], seed=4321,
+                                       symmetric=True)
+                res = _policy_pair(a, m, comm, world, rank, stream, batch, steps, warm, be)
+            except Exception as e:  # an optional transport must not sink the line
+                if be is None:
+                    raise
+                out[be] = {"error": f"{type(e).__name__}: {e}"[:300]}
+                continue
+            finally:
+                if m is not model:
+                    m.close()
             d, w = res[a.policy]["ms_per_step"], res[a.baseline_policy]["ms_per_step"]
             res.update({"dear_over_wfbp": w / d,
                         "exposed_comm_pct": max(0.0, 100 * (d - comp) / d),
@@ -1042,8 +1050,12 @@ def compare_policies(a, wl_name, comm, world, rank, stream):
                                "t_ag_over_t_ff": t_ag / t_ff if t_ff else None}
             if be is None:
                 if with_nccl and world > 1 and not a.no_priority_partition:
-                    pp = _priority_partition(a, m, comm, world, rank, stream, batch, steps, warm)
-                    pp["dear_over_pp"] = pp["ms_per_step"] / res[a.policy]["ms_per_step"]
+                    try:
+                        pp = _priority_partition(a, m, comm, world, rank, stream, batch, steps,
+                                                 warm)
+                        pp["dear_over_pp"] = pp["ms_per_step"] / res[a.policy]["ms_per_step"]
+                    except Exception as e:
+                        pp = {"error": f"{type(e).__name__}: {e}"[:300]}
                     res["priority_partition"] = pp
                 out.update(res)
             else:
