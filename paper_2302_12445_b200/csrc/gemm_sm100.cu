@@ -102,14 +102,6 @@ struct alignas(64) Problem {
   int32_t b_boxes;
   uint32_t idesc;
   uint32_t tx_bytes;
-  // Wide tiles (bn > 256, builds with DEAR_GEMM_BN_MAX = 512): one MMA is at
-  // most N = 256, so each k-step issues n_sub MMAs of N = bn / n_sub into
-  // adjacent TMEM column ranges; B is fetched in n_sub pieces (per CTA of a
-  // pair: the quarter rows the pair MMA reads from this SM), piece j landing
-  // at b_piece_bytes * j in the stage.
-  int32_t n_sub;
-  int32_t b_piece;        // K-major: rows per piece; MN-major: 64-column boxes per piece
-  uint32_t b_piece_bytes;
   // Thread-block cluster of cm x cn CTAs sharing operands through TMA
   // multicast: CTA (i, j) computes tile (mg*cm + i, ng*cn + j); the A tile
   // of row i is fetched once, in cn pieces of a_rows rows, and multicast to
@@ -572,22 +564,16 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           uint8_t* sA = smem + s * stage_bytes;
           uint8_t* sB = sA + kAStage;
           if (kPair) {
-            // Both CTAs' bytes land on the leader's full barrier. Piece j of
-            // this CTA: columns n0 + j * bn / n_sub + crank * (piece width).
+            // Both CTAs' bytes land on the leader's full barrier.
             if (leader) mbar_expect_tx(&full[s], P.tx_bytes);
             const uint32_t fb = mapa_shared(&full[s], 0);
             tma_load_2d_pair(&P.tmA, fb, sA, kc, static_cast<int32_t>(tc.m0));
-            const int32_t sub_w = P.bn / P.n_sub;
-            for (int j = 0; j < P.n_sub; ++j) {
-              uint8_t* dB = sB + j * P.b_piece_bytes;
-              if (!P.b_mn_major) {
-                const int32_t nh = static_cast<int32_t>(tc.n0) + j * sub_w + crank * P.b_piece;
-                tma_load_2d_pair(&P.tmB, fb, dB, kc, nh);
-              } else {
-                const int32_t nh = static_cast<int32_t>(tc.n0) + j * sub_w + crank * 64 * P.b_piece;
-                for (int b = 0; b < P.b_piece; ++b)
-                  tma_load_2d_pair(&P.tmB, fb, dB + b * 8192, nh + 64 * b, kc);
-              }
+            const int32_t nh = static_cast<int32_t>(tc.n0) + crank * (P.bn / 2);
+            if (!P.b_mn_major) {
+              tma_load_2d_pair(&P.tmB, fb, sB, kc, nh);
+            } else {
+              for (int j = 0; j < P.b_boxes; ++j)
+                tma_load_2d_pair(&P.tmB, fb, sB + j * 8192, nh + 64 * j, kc);
             }
             continue;
           }
@@ -605,8 +591,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             if (P.cm > 1)
               tma_load_2d_mc(&P.tmB, &full[s], dB, kc, bn0, col_mask);
             else
-              for (int j = 0; j < P.n_sub; ++j)  // wide tiles: TMA boxes are <= 256 rows
-                tma_load_2d(&P.tmB, &full[s], dB + j * P.b_piece_bytes, kc, bn0 + j * P.b_piece);
+              tma_load_2d(&P.tmB, &full[s], dB, kc, bn0);
           } else {
             for (int j = 0; j < P.b_boxes; ++j) {
               uint8_t* dB = sB + j * 8192 + ci * P.b_rows * 128;
@@ -656,16 +641,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k) {
             const uint64_t ad = sdesc(a_base + k * 32, 16, 1024);
-            for (int j = 0; j < P.n_sub; ++j) {
-              const uint32_t bj = b_base + j * P.b_piece_bytes;
-              const uint64_t bd = P.b_mn_major ? sdesc(bj + k * 2048, 8192, 1024)
-                                               : sdesc(bj + k * 32, 16, 1024);
-              const uint32_t dj = d_tmem + static_cast<uint32_t>(j * (P.bn / P.n_sub));
-              if (kPair)
-                umma2_bf16(dj, ad, bd, P.idesc, (i != 0 || k != 0) ? 1u : 0u);
-              else
-                umma_bf16(dj, ad, bd, P.idesc, (i != 0 || k != 0) ? 1u : 0u);
-            }
+            const uint64_t bd = P.b_mn_major ? sdesc(b_base + k * 2048, 8192, 1024)
+                                             : sdesc(b_base + k * 32, 16, 1024);
+            if (kPair)
+              umma2_bf16(d_tmem, ad, bd, P.idesc, (i != 0 || k != 0) ? 1u : 0u);
+            else
+              umma_bf16(d_tmem, ad, bd, P.idesc, (i != 0 || k != 0) ? 1u : 0u);
           }
           if (kPair)
             umma2_commit_both(&empty[s]);
@@ -940,15 +921,8 @@ void configure(dear_gemm_plan* plan, const TileChoice& tch) {
   p.n_tiles = static_cast<int32_t>((p.N + bn - 1) / bn);
   p.pair = tch.pair;
   const uint32_t mma_m = p.pair ? 2 * kBM : kBM;
-  p.n_sub = bn > 256 ? 2 : 1;
-  const int sub_n = bn / p.n_sub;
   p.idesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(p.b_mn_major) << 16) |
-            (static_cast<uint32_t>(sub_n >> 3) << 17) | ((mma_m >> 4) << 24);
-  // B pieces per CTA: K-major rows / MN-major 64-column boxes.
-  const int piece_w = sub_n / (p.pair ? 2 : 1);
-  p.b_piece = mn ? piece_w / 64 : piece_w;
-  p.b_piece_bytes = mn ? static_cast<uint32_t>(p.b_piece) * 8192u
-                       : static_cast<uint32_t>(piece_w) * kBK * 2;
+            (static_cast<uint32_t>(bn >> 3) << 17) | ((mma_m >> 4) << 24);
   if (p.pair) {
     // Per CTA: 128 rows of A and half of B; the leader's barrier counts both.
     p.b_boxes = mn ? bn / 2 / 64 : 1;
@@ -972,8 +946,7 @@ void configure(dear_gemm_plan* plan, const TileChoice& tch) {
            static_cast<uint64_t>(plan->lda), kBK, static_cast<uint32_t>(p.a_rows));
   if (!mn)
     make_map(&p.tmB, plan->B, static_cast<uint64_t>(plan->K), static_cast<uint64_t>(p.N),
-             static_cast<uint64_t>(plan->ldb), kBK,
-             static_cast<uint32_t>(p.n_sub > 1 || p.pair ? p.b_piece : p.b_rows));
+             static_cast<uint64_t>(plan->ldb), kBK, static_cast<uint32_t>(p.b_rows));
   else
     make_map(&p.tmB, plan->B, static_cast<uint64_t>(p.N), static_cast<uint64_t>(plan->K),
              static_cast<uint64_t>(plan->ldb), 64, static_cast<uint32_t>(p.b_rows));
@@ -1264,19 +1237,9 @@ int dear_gemm_plan_set_tile(dear_gemm_plan* plan, int32_t bn, int32_t pair) {
   using namespace dear::gemm;
   if (!plan) throw Error(DEAR_EINVAL, "null plan");
   if (bn < 16 || bn > kBNMax || bn % 16)
-    throw Error(DEAR_EINVAL, "dear_gemm_plan_set_tile: bn must be a multiple of 16 in [16, " +
-                                 std::to_string(kBNMax) + "]");
-  if (pair && plan->p.b_mn_major && bn != 128 && bn != 256 && bn != 512)
-    throw Error(DEAR_EINVAL, "dear_gemm_plan_set_tile: MN-major B in CTA pairs needs bn 128, 256 or 512");
-  if (bn > 256) {
-    // two sub-MMAs of bn / 2 (a multiple of 16; per pair CTA of 8 rows; MN-major
-    // B in whole 64-column boxes)
-    const bool mn = plan->p.b_mn_major != 0;
-    const int q = mn ? (pair ? 256 : 128) : (pair ? 64 : 32);
-    if (bn % q)
-      throw Error(DEAR_EINVAL, "dear_gemm_plan_set_tile: bn > 256 must be a multiple of " +
-                                   std::to_string(q) + " here");
-  }
+    throw Error(DEAR_EINVAL, "dear_gemm_plan_set_tile: bn must be a multiple of 16 in [16, 256]");
+  if (pair && plan->p.b_mn_major && bn != 128 && bn != 256)
+    throw Error(DEAR_EINVAL, "dear_gemm_plan_set_tile: MN-major B in CTA pairs needs bn 128 or 256");
   configure(plan, TileChoice{bn, 1, 1, pair ? 1 : 0});
   DEAR_API_END
 }

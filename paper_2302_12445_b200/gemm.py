@@ -157,12 +157,8 @@ def tile_candidates(M: int, N: int, mn_major: bool) -> list[tuple[int, int]]:
         if pair and M <= 128:
             continue
         for bn in range(64, max_bn + 1, 16):
-            if pair and mn_major and bn not in (128, 256, 512):
+            if pair and mn_major and bn not in (128, 256):
                 continue
-            if bn > 256:  # wide tiles (DEAR_GEMM_BN_MAX=512 builds): two sub-MMAs
-                q = (256 if pair else 128) if mn_major else (64 if pair else 32)
-                if bn % q:
-                    continue
             nt = -(-N // bn)
             if nt > 1 and (nt - 1) * bn >= N:  # a fully padded last tile
                 continue

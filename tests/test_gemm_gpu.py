@@ -169,61 +169,3 @@ def test_gemm_group_wgrad_dgrad():
     err = (dx.float() - ref_dx).abs()
     assert torch.all(err <= ref_dx.abs() * 2.0**-8 + 4e-3 * ref_dx.abs().max()), err.max()
 
-
-def _wide_ok(plan, bn, pair):
-    """set_tile(bn > 256) needs a DEAR_GEMM_BN_MAX=512 build (skip otherwise)."""
-    from paper_2302_12445_b200 import InvalidArgument
-
-    try:
-        plan.set_tile(bn, pair)
-        return True
-    except InvalidArgument:
-        return False
-
-
-@pytest.mark.parametrize("bn,pair", [(256, 0), (320, 0), (384, 0), (512, 0), (320, 1), (512, 1)])
-@pytest.mark.parametrize("M,N,K", [(10240, 311, 512), (1000, 520, 513)])
-def test_gemm_wide_tiles_kmajor(M, N, K, bn, pair, tile_mode):
-    """Tiles wider than one MMA (bn > 256: two sub-MMAs into adjacent TMEM
-    columns, B fetched in pieces; in CTA pairs each SM holds the quarter rows
-    the pair MMA reads from it) against torch fp32."""
-    if tile_mode != "auto":
-        pytest.skip("tile chosen explicitly")
-    from paper_2302_12445_b200.gemm import GemmPlan
-
-    torch.manual_seed(5)
-    a = torch.randn(M, K, device="cuda").to(torch.bfloat16)
-    ldk = (K + 7) // 8 * 8
-    astore = torch.zeros(M, ldk, device="cuda", dtype=torch.bfloat16)
-    astore[:, :K] = a
-    bstore = torch.zeros(N, ldk, device="cuda", dtype=torch.bfloat16)
-    bstore[:, :K] = torch.randn(N, K, device="cuda").to(torch.bfloat16)
-    d = torch.full((M, N), float("nan"), device="cuda")
-    plan = GemmPlan(astore, bstore, d, M, N, K, lda=ldk, ldb=ldk, ldd=N)
-    if not _wide_ok(plan, bn, pair):
-        pytest.skip("library built without wide tiles")
-    plan.run()
-    torch.cuda.synchronize()
-    _check(d, astore[:, :K].float() @ bstore[:, :K].float().t(), K)
-
-
-@pytest.mark.parametrize("bn,pair", [(384, 0), (512, 0), (512, 1)])
-def test_gemm_wide_tiles_mn_major(bn, pair, tile_mode):
-    """dgrad shape with MN-major B and wide tiles."""
-    if tile_mode != "auto":
-        pytest.skip("tile chosen explicitly")
-    from paper_2302_12445_b200.gemm import GemmPlan
-
-    torch.manual_seed(6)
-    T, H, R = 10240, 512, 311
-    dy = torch.randn(T, 320, device="cuda").to(torch.bfloat16)
-    W = torch.randn(R, H, device="cuda").to(torch.bfloat16)
-    dx = torch.zeros(T, H, device="cuda", dtype=torch.bfloat16)
-    plan = GemmPlan(dy, W, dx, T, H, R, b_mn_major=True, lda=320, ldb=H, ldd=H)
-    if not _wide_ok(plan, bn, pair):
-        pytest.skip("library built without wide tiles")
-    plan.run()
-    torch.cuda.synchronize()
-    ref = dy[:, :R].float() @ W.float()
-    err = (dx.float() - ref).abs()
-    assert torch.all(err <= ref.abs() * 2.0**-8 + 4e-3 * ref.abs().max()), err.max()
