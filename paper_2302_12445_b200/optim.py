@@ -46,7 +46,7 @@ class DistOptim:
                  *, comm=None, rank: int = 0, policy: str = "DEAR_FUSED",
                  fusion_buffer_bytes: int = 25_000_000, defer_allgather: bool = False,
                  backend: str = "auto", stream: Optional[torch.cuda.Stream] = None,
-                 flatten: bool = True):
+                 flatten: bool = True, partition_bytes: int = 0):
         if not isinstance(optimizer, torch.optim.SGD):
             raise TypeError("DistOptim supports torch.optim.SGD (the reference's update rule)")
         if len(optimizer.param_groups) != 1:
@@ -90,7 +90,7 @@ class DistOptim:
                                weight_decay=float(g.get("weight_decay", 0.0)),
                                nesterov=bool(g.get("nesterov", False)),
                                defer_allgather=defer_allgather, backend=backend,
-                               stream=stream)
+                               stream=stream, partition_bytes=partition_bytes)
         for p in params:
             if p.dtype != torch.float32 or not p.is_cuda or not p.is_contiguous():
                 raise ValueError("DistOptim needs contiguous fp32 CUDA parameters")

@@ -113,9 +113,10 @@ def case_runtime(rank, P):
     o = Restated()
     ok = True
     for policy, buf in (("DEAR_FUSED", 100_000), ("DEAR", 0), ("WFBP_FUSED", 400_000),
-                        ("WFBP", 0), ("DEAR_FUSED", 25_000_000)):
-        w, same, trace = run_runtime(comm, rank, P, policy, buf, 3, 0.05)
-        exp = oracle_run(o, RAGGED, P, 3, policy, buf, 0.05, f32=False)
+                        ("WFBP", 0), ("DEAR_FUSED", 25_000_000), ("PRIORITY_PARTITION", 0)):
+        pb = 40_000 if policy == "PRIORITY_PARTITION" else 0
+        w, same, trace = run_runtime(comm, rank, P, policy, buf, 3, 0.05, partition_bytes=pb)
+        exp = oracle_run(o, RAGGED, P, 3, policy, buf, 0.05, f32=False, partition_bytes=pb)
         allw = [torch.zeros_like(torch.from_numpy(w)).cuda() for _ in range(P)]
         dist.all_gather(allw, torch.from_numpy(w).cuda())
         bit_same = all(torch.equal(allw[0], x) for x in allw)
@@ -166,11 +167,12 @@ def case_peer(rank, P):
     ok = True
     for flat in (False, True):
         for policy, buf in (("DEAR_FUSED", 100_000), ("DEAR", 0), ("WFBP_FUSED", 400_000),
-                            ("WFBP", 0), ("DEAR_FUSED", 25_000_000)):
+                            ("WFBP", 0), ("DEAR_FUSED", 25_000_000), ("PRIORITY_PARTITION", 0)):
+            pb = 40_000 if policy == "PRIORITY_PARTITION" else 0
             w, same, _ = run_runtime(comm, rank, P, policy, buf, 3, 0.05, backend="peer",
-                                     flat=flat)
-            exp32 = oracle_run(o, RAGGED, P, 3, policy, buf, 0.05, f32=True)
-            exp64 = oracle_run(o, RAGGED, P, 3, policy, buf, 0.05, f32=False)
+                                     flat=flat, partition_bytes=pb)
+            exp32 = oracle_run(o, RAGGED, P, 3, policy, buf, 0.05, f32=True, partition_bytes=pb)
+            exp64 = oracle_run(o, RAGGED, P, 3, policy, buf, 0.05, f32=False, partition_bytes=pb)
             good = same and np.array_equal(w, exp32) and close(w.astype(np.float64), exp64)
             if rank == 0:
                 print(f"[peer P={P} {'zero-copy' if flat else 'slots'}] {policy:11s} "
@@ -221,11 +223,12 @@ def case_nvls(rank, P):
     o = Restated()
     ok = True
     for policy, buf in (("DEAR_FUSED", 100_000), ("DEAR", 0), ("WFBP_FUSED", 400_000),
-                        ("WFBP", 0), ("DEAR_FUSED", 25_000_000)):
+                        ("WFBP", 0), ("DEAR_FUSED", 25_000_000), ("PRIORITY_PARTITION", 0)):
+        pb = 40_000 if policy == "PRIORITY_PARTITION" else 0
         w, same, trace = run_runtime(comm, rank, P, policy, buf, 3, 0.05, backend="nvls",
-                                     shadow=True)
-        exp32 = oracle_run(o, RAGGED, P, 3, policy, buf, 0.05, f32=True)
-        exp64 = oracle_run(o, RAGGED, P, 3, policy, buf, 0.05, f32=False)
+                                     shadow=True, partition_bytes=pb)
+        exp32 = oracle_run(o, RAGGED, P, 3, policy, buf, 0.05, f32=True, partition_bytes=pb)
+        exp64 = oracle_run(o, RAGGED, P, 3, policy, buf, 0.05, f32=False, partition_bytes=pb)
         bit = bool(np.array_equal(w, exp32))
         good = same and close(w.astype(np.float64), exp64) and run_runtime.shadow_ok and \
             (bit or P != 2)
