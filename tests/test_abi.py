@@ -71,3 +71,28 @@ def test_runtime_rejects_unknown_policy():
 
     with pytest.raises(ValueError, match="unknown policy"):
         Runtime(policy="BYTESCHEDULER")
+
+
+def test_python_transport_validation_without_gpu():
+    """Host-side argument checks of the transports (no CUDA call is made)."""
+    import paper_2302_12445_b200 as dear
+
+    with pytest.raises(ValueError, match="transport"):
+        dear.LocalGroup(2, "bogus")
+    with pytest.raises(ValueError, match="needs a SymmetricHeap"):
+        dear.Runtime(None, 0, 1, backend="nvls")
+    with pytest.raises(ValueError, match="backend must be"):
+        dear.Runtime(None, 0, 1, backend="gloo")
+    L = _lib.lib()
+    # PRIORITY_PARTITION is a runtime policy now (validated like policy.cpp:58-61)
+    cfg = _lib.DearCfg(2, 0, 0, 0.1, 0, 0, 0, 0, 0, -5)
+    ctx = C.c_void_p()
+    assert L.dear_create(None, 0, 1, None, C.byref(cfg), C.byref(ctx)) == _lib.DEAR_EINVAL
+    # local-group / heap entry points validate their handles first
+    assert L.dear_local_group_connect(None, 1) == _lib.DEAR_EINVAL
+    assert L.dear_nvls_connect(None, None) == _lib.DEAR_EINVAL
+    assert L.dear_symm_join(None, 0, 0) == _lib.DEAR_EINVAL
+    assert L.dear_symm_bind(None) == _lib.DEAR_EINVAL
+    g = C.c_void_p()
+    assert L.dear_local_group_create_ex(2, 7, C.byref(g)) == _lib.DEAR_EINVAL
+    assert L.dear_local_group_create_ex(17, 1, C.byref(g)) == _lib.DEAR_EINVAL
