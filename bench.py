@@ -82,6 +82,8 @@ def parse():
     ap.add_argument("--partition-bytes", type=int, default=4_000_000,
                     help="PRIORITY_PARTITION ablation (north star, N > 1): part size")
     ap.add_argument("--no-priority-partition", action="store_true")
+    ap.add_argument("--north-star-batches", default="64",
+                    help="N > 1: also compare DeAR / WFBP at these per-GPU batches")
     ap.add_argument("--no-parity", action="store_true",
                     help="skip the post-timing oracle parity check of one bucket")
     ap.add_argument("--parity-steps", type=int, default=3)
@@ -1090,6 +1092,20 @@ def compare_policies(a, wl_name, comm, world, rank, stream):
             cal = one(b, False)
             cal["rule"] = "batch with measured t_ag = 1.25 t_ff (SURVEY §7: 1.2-1.33)"
             out["calibrated_batch"] = cal
+    if world > 1 and a.north_star_batches:
+        # DeAR vs WFBP as the compute / comm ratio grows (same kernels, default
+        # transport): per-layer compute scales with the batch, the buckets do not.
+        sweep = {}
+        for b in (int(x) for x in a.north_star_batches.split(",") if x.strip()):
+            if b == base:
+                continue
+            r = one(b, False)
+            d, w = r[a.policy]["ms_per_step"], r[a.baseline_policy]["ms_per_step"]
+            sweep[str(b)] = {"compute_only_ms": r["compute_only_ms"], "DEAR_ms": d, "WFBP_ms": w,
+                             "dear_over_wfbp": w / d, "exposed_comm_pct": r["exposed_comm_pct"],
+                             "wfbp_exposed_comm_pct": r["wfbp_exposed_comm_pct"],
+                             "samples_per_s": r[a.policy]["samples_per_s"]}
+        out["batch_sweep"] = sweep
     return out
 
 
