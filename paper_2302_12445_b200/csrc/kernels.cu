@@ -1231,7 +1231,7 @@ bool pdl_on() {
 
 // <<<grid, kThreads, 0, s>>> with programmatic stream serialization.
 template <typename... KArgs, typename... Args>
-void launch_pdl(void (*k)(KArgs...), int grid, cudaStream_t s, Args... args) {
+cudaError_t launch_pdl(void (*k)(KArgs...), int grid, cudaStream_t s, Args... args) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
@@ -1242,7 +1242,7 @@ void launch_pdl(void (*k)(KArgs...), int grid, cudaStream_t s, Args... args) {
   attr[0].val.programmaticStreamSerializationAllowed = pdl_on() ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
 }
 
 int bucket_grid(int n_slices, int want = 0) {
@@ -1259,9 +1259,8 @@ int bucket_grid(int n_slices, int want = 0) {
 cudaError_t launch_pack(const Unit* units, const Slice* slices, int64_t total, float scale,
                         int grid, cudaStream_t s) {
   if (total <= 0) return cudaSuccess;
-  launch_pdl(pack_kernel<false>, bucket_grid(kPackSlices, grid), s, units, slices, scale,
-             static_cast<BucketFlags*>(nullptr), PeerArgs{}, kPackSlices);
-  return cudaGetLastError();
+  return launch_pdl(pack_kernel<false>, bucket_grid(kPackSlices, grid), s, units, slices, scale,
+                    static_cast<BucketFlags*>(nullptr), PeerArgs{}, kPackSlices);
 }
 
 cudaError_t launch_pack_signal(const Unit* units, const Slice* slices, int64_t total, float scale,
@@ -1467,25 +1466,20 @@ cudaError_t launch_update(const Unit* units, const Slice* slices, int64_t total,
   if (total <= 0) return cudaSuccess;
   const int ug = bucket_grid(kUpdSlices, grid);
   if (use_momentum && use_wd)
-    launch_pdl(update_kernel<true, true>, ug, s, units, slices, hp, has_momentum_buf);
-  else if (use_momentum)
-    launch_pdl(update_kernel<true, false>, ug, s, units, slices, hp, has_momentum_buf);
-  else if (use_wd)
-    launch_pdl(update_kernel<false, true>, ug, s, units, slices, hp, has_momentum_buf);
-  else
-    launch_pdl(update_kernel<false, false>, ug, s, units, slices, hp, has_momentum_buf);
-  return cudaGetLastError();
+    return launch_pdl(update_kernel<true, true>, ug, s, units, slices, hp, has_momentum_buf);
+  if (use_momentum)
+    return launch_pdl(update_kernel<true, false>, ug, s, units, slices, hp, has_momentum_buf);
+  if (use_wd)
+    return launch_pdl(update_kernel<false, true>, ug, s, units, slices, hp, has_momentum_buf);
+  return launch_pdl(update_kernel<false, false>, ug, s, units, slices, hp, has_momentum_buf);
 }
 
 cudaError_t launch_unpack(const Unit* units, const Slice* slices, int64_t total, int with_shadow,
                           int grid, cudaStream_t s) {
   if (total <= 0) return cudaSuccess;
   const int ug = bucket_grid(kUnpackSlices, grid);
-  if (with_shadow)
-    launch_pdl(unpack_kernel<true>, ug, s, units, slices);
-  else
-    launch_pdl(unpack_kernel<false>, ug, s, units, slices);
-  return cudaGetLastError();
+  if (with_shadow) return launch_pdl(unpack_kernel<true>, ug, s, units, slices);
+  return launch_pdl(unpack_kernel<false>, ug, s, units, slices);
 }
 
 cudaError_t launch_update_direct(const Unit* units, const Slice* slices, int64_t total,
@@ -1494,14 +1488,10 @@ cudaError_t launch_update_direct(const Unit* units, const Slice* slices, int64_t
   if (total <= 0) return cudaSuccess;
   const int grid = bucket_grid(kDirSlices);
   if (use_wd && with_shadow)
-    launch_pdl(update_direct_kernel<true, true>, grid, s, units, slices, hp);
-  else if (use_wd)
-    launch_pdl(update_direct_kernel<true, false>, grid, s, units, slices, hp);
-  else if (with_shadow)
-    launch_pdl(update_direct_kernel<false, true>, grid, s, units, slices, hp);
-  else
-    launch_pdl(update_direct_kernel<false, false>, grid, s, units, slices, hp);
-  return cudaGetLastError();
+    return launch_pdl(update_direct_kernel<true, true>, grid, s, units, slices, hp);
+  if (use_wd) return launch_pdl(update_direct_kernel<true, false>, grid, s, units, slices, hp);
+  if (with_shadow) return launch_pdl(update_direct_kernel<false, true>, grid, s, units, slices, hp);
+  return launch_pdl(update_direct_kernel<false, false>, grid, s, units, slices, hp);
 }
 
 void make_slices(const Unit* units, int n_units, int64_t total, Slice* out, int n_slices,
