@@ -1085,9 +1085,14 @@ def compare_policies(a, wl_name, comm, world, rank, stream):
     out.update(one(base, True))
     eq = out.get("eq78")
     if world > 1 and eq and eq["t_ag_ms"] > 0 and eq["t_ff_ms"] > 0 and not a.no_calibrate:
-        # t_ff scales with the batch, t_ag does not: the batch with t_ag = 1.25 t_ff
+        # t_ff scales with the batch, t_ag does not: the batch with t_ag = 1.25 t_ff.
+        # Rank 0 decides (the measurements are rank-local): every rank must run
+        # the same collectives.
         b = int(round(base * eq["t_ag_ms"] / (1.25 * eq["t_ff_ms"])))
         b = max(4, min(b, 4 * base))
+        bt = torch.tensor([b], dtype=torch.int64, device="cuda")
+        torch.distributed.broadcast(bt, 0)
+        b = int(bt.item())
         if abs(b - base) >= max(2, base // 8):
             cal = one(b, False)
             cal["rule"] = "batch with measured t_ag = 1.25 t_ff (SURVEY §7: 1.2-1.33)"
