@@ -1254,29 +1254,12 @@ int bucket_grid(int n_slices, int want = 0) {
   return g > 0 && g < n_slices ? g : n_slices;
 }
 
-// Local bucket kernels on small ops: at least DEAR_SMALL_CTA_KB (default 64)
-// KB of traffic per CTA, never fewer than one CTA per SM — a 6 MB bucket on
-// the full 592-CTA grid is launch- and tail-bound (CTAs then walk several
-// slices). 0 disables.
-int sized_grid(int n_slices, int64_t bytes, int want) {
-  static const int64_t per = [] {
-    const char* e = std::getenv("DEAR_SMALL_CTA_KB");
-    return static_cast<int64_t>(e ? std::atoi(e) : 64) * 1024;
-  }();
-  int g = bucket_grid(n_slices, want);
-  if (per > 0 && want == 0) {
-    const int64_t need = std::max<int64_t>(kSms, (bytes + per - 1) / per);
-    if (need < g) g = static_cast<int>(need);
-  }
-  return g;
-}
-
 }  // namespace
 
 cudaError_t launch_pack(const Unit* units, const Slice* slices, int64_t total, float scale,
                         int grid, cudaStream_t s) {
   if (total <= 0) return cudaSuccess;
-  return launch_pdl(pack_kernel<false>, sized_grid(kPackSlices, 8 * total, grid), s, units, slices, scale,
+  return launch_pdl(pack_kernel<false>, bucket_grid(kPackSlices, grid), s, units, slices, scale,
                     static_cast<BucketFlags*>(nullptr), PeerArgs{}, kPackSlices);
 }
 
@@ -1481,7 +1464,7 @@ cudaError_t launch_update(const Unit* units, const Slice* slices, int64_t total,
                           const HyperParams* hp, int has_momentum_buf, int use_momentum,
                           int use_wd, int grid, cudaStream_t s) {
   if (total <= 0) return cudaSuccess;
-  const int ug = sized_grid(kUpdSlices, (use_momentum ? 20 : 12) * total, grid);
+  const int ug = bucket_grid(kUpdSlices, grid);
   if (use_momentum && use_wd)
     return launch_pdl(update_kernel<true, true>, ug, s, units, slices, hp, has_momentum_buf);
   if (use_momentum)
@@ -1494,7 +1477,7 @@ cudaError_t launch_update(const Unit* units, const Slice* slices, int64_t total,
 cudaError_t launch_unpack(const Unit* units, const Slice* slices, int64_t total, int with_shadow,
                           int grid, cudaStream_t s) {
   if (total <= 0) return cudaSuccess;
-  const int ug = sized_grid(kUnpackSlices, (with_shadow ? 10 : 8) * total, grid);
+  const int ug = bucket_grid(kUnpackSlices, grid);
   if (with_shadow) return launch_pdl(unpack_kernel<true>, ug, s, units, slices);
   return launch_pdl(unpack_kernel<false>, ug, s, units, slices);
 }
@@ -1503,7 +1486,7 @@ cudaError_t launch_update_direct(const Unit* units, const Slice* slices, int64_t
                                  const HyperParams* hp, int use_wd, int with_shadow,
                                  cudaStream_t s) {
   if (total <= 0) return cudaSuccess;
-  const int grid = sized_grid(kDirSlices, 14 * total, 0);
+  const int grid = bucket_grid(kDirSlices);
   if (use_wd && with_shadow)
     return launch_pdl(update_direct_kernel<true, true>, grid, s, units, slices, hp);
   if (use_wd) return launch_pdl(update_direct_kernel<true, false>, grid, s, units, slices, hp);
