@@ -197,6 +197,14 @@ int dear_synchronize(dear_ctx* ctx);
  * their cross-GPU waits with DEAR_PEER_TIMEOUT_S (default 600 s; they trap). */
 int dear_comm_error(dear_ctx* ctx, int32_t* failed);
 
+/* Profiling aid: the zero-copy reduce-scatter / all-gather CTAs append 40-byte
+ * records {u64 t_start, u64 t_peers_arrived, u64 t_end (%globaltimer ns),
+ * u32 kind (0 RS, 1 AG), u32 bucket tag, u32 epoch, u32 cta} to a device
+ * buffer of `capacity` records (NULL = off); dear_comm_trace_count reads how
+ * many were written since the last dear_set_comm_trace (process-wide). */
+int dear_set_comm_trace(void* device_buffer, int64_t capacity);
+int dear_comm_trace_count(int64_t* n);
+
 int dear_destroy(dear_ctx* ctx);
 
 /* Learning-rate change (device-resident; CUDA-graph safe). */

@@ -91,6 +91,8 @@ _SIGNATURES = {
     "dear_nvls_connect": [_P, _P],
     "dear_nvls_enabled": [_P, C.POINTER(C.c_int32)],
     "dear_comm_error": [_P, C.POINTER(C.c_int32)],
+    "dear_set_comm_trace": [_P, C.c_int64],
+    "dear_comm_trace_count": [C.POINTER(C.c_int64)],
 }
 DEAR_PEER_HANDLE_BYTES = 256
 

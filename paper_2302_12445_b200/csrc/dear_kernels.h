@@ -179,6 +179,11 @@ cudaError_t launch_rs_update_zc(const Unit* units, const Slice* slices, const Hy
                                 int use_wd, int with_shadow, const PeerArgs& pa,
                                 const PeerArgs& ga, BucketFlags* flags, cudaStream_t s);
 
+// Comm-kernel phase trace (profiling): records of 40 B {t0, t_arrived, t_end,
+// kind, tag, epoch, cta}; buf = null turns it off; the count restarts at 0.
+cudaError_t set_comm_trace(void* buf, uint32_t cap);
+cudaError_t comm_trace_count(uint32_t* n);
+
 // hp->lr = lr, stream-ordered (dear_set_lr; graph-capturable).
 cudaError_t launch_set_lr(HyperParams* hp, float lr, cudaStream_t s);
 

@@ -256,6 +256,53 @@ __device__ __forceinline__ void pdl_enter() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+// ------------------------------------------------ comm-kernel phase trace ----
+// Profiling aid (dear_set_comm_trace): the zero-copy reduce-scatter and
+// all-gather CTAs record %globaltimer at entry, when every peer has arrived,
+// and at exit, so an in-step trace separates waiting on other GPUs from
+// moving data. Off (null) by default: one predicated load per CTA.
+struct CommTraceRec {
+  unsigned long long t0, t_arrived, t_end;
+  uint32_t kind;   // 0 reduce-scatter, 1 all-gather
+  uint32_t tag;    // low bits of the bucket's counter block (identifies the bucket)
+  uint32_t epoch;  // the bucket's iteration count on this rank
+  uint32_t cta;
+};
+__device__ CommTraceRec* g_comm_trace = nullptr;
+__device__ uint32_t g_comm_trace_cap = 0;
+__device__ uint32_t g_comm_trace_n = 0;
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// The two stamps live in shared memory (thread 0 only), not registers: the
+// register-capped peer kernels must not spill for a profiling aid.
+__device__ __forceinline__ unsigned long long* trace_slots() {
+  __shared__ unsigned long long t[2];
+  return t;
+}
+__device__ __forceinline__ void trace_stamp(int which) {
+  if (threadIdx.x == 0 && g_comm_trace) trace_slots()[which] = gtimer();
+}
+__device__ __forceinline__ void trace_finish(uint32_t kind, const void* flags, uint32_t epoch,
+                                             int cta) {
+  if (threadIdx.x != 0 || !g_comm_trace) return;
+  const uint32_t i = atomicAdd(&g_comm_trace_n, 1u);
+  if (i >= g_comm_trace_cap) return;
+  CommTraceRec r;
+  r.t0 = trace_slots()[0];
+  r.t_arrived = trace_slots()[1];
+  r.t_end = gtimer();
+  r.kind = kind;
+  r.tag = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(flags) & 0xffffffffu);
+  r.epoch = epoch;
+  r.cta = static_cast<uint32_t>(cta);
+  g_comm_trace[i] = r;
+}
+
 // ------------------------------------------------------ peer signalling ----
 __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
   uint32_t v;
@@ -755,7 +802,10 @@ __device__ __forceinline__ void rs_update_zc_body(const Unit* __restrict__ units
                                                   const HyperParams* __restrict__ hpp, int has_buf,
                                                   float* mom_base, const PeerArgs& pa,
                                                   const PeerArgs& ga, BucketFlags* flags, Blk blk) {
+  trace_stamp(0);
+  const uint32_t epoch = g_comm_trace ? *reinterpret_cast<volatile uint32_t*>(&flags->updated) : 0u;
   cta_announce_and_wait(flags, pa, blk);
+  trace_stamp(1);
   const HyperParams hp = *hpp;
   const int P = PC > 0 ? PC : pa.P;
   const int k0 = (pa.rank + 1) % P;
@@ -851,6 +901,7 @@ __device__ __forceinline__ void rs_update_zc_body(const Unit* __restrict__ units
     }
     for (int64_t i = head + n4 * 4 + threadIdx.x; i < n; i += kThreads) scalar(i);
   }, blk);
+  trace_finish(0, flags, epoch, blk.id);
   signal_done(&flags->done[1], &flags->updated, blk);
 }
 
@@ -871,7 +922,10 @@ __device__ __forceinline__ void ag_unpack_peer_body(const Unit* __restrict__ uni
                                                     const Slice* __restrict__ slices,
                                                     const PeerArgs& pa, const PeerArgs& sa,
                                                     BucketFlags* flags, int n_slices, Blk blk) {
+  trace_stamp(0);
+  const uint32_t epoch = g_comm_trace ? *reinterpret_cast<volatile uint32_t*>(&flags->updated) : 0u;
   cta_wait_peers(&flags->updated, &flags->updated, pa);  // every owner updated its shard
+  trace_stamp(1);
   walk_slice(units, slices, n_slices, [&](const Unit& U, int64_t off, int64_t n) {
     const float* src = at_peer(U.a + off, sa.delta[U.peer]);
     float* dst = U.b + off;
@@ -888,6 +942,7 @@ __device__ __forceinline__ void ag_unpack_peer_body(const Unit* __restrict__ uni
           if (kShadow && sh) store_bf16x4(sh + head, q, v);
         });
   }, blk);
+  trace_finish(1, flags, epoch, blk.id);
   signal_done(&flags->done[2], &flags->gathered, blk);
 }
 
@@ -1537,6 +1592,19 @@ cudaError_t launch_local_all_gather(float* const* bufs_dev, int P, int64_t strid
   if (count <= 0) return cudaSuccess;
   local_ag_kernel<<<kSms * 4, 256, 0, s>>>(bufs_dev, P, stride, count);
   return cudaGetLastError();
+}
+
+cudaError_t set_comm_trace(void* buf, uint32_t cap) {
+  CommTraceRec* p = static_cast<CommTraceRec*>(buf);
+  const uint32_t zero = 0;
+  cudaError_t e = cudaMemcpyToSymbol(g_comm_trace, &p, sizeof p);
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_comm_trace_cap, &cap, sizeof cap);
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_comm_trace_n, &zero, sizeof zero);
+  return e;
+}
+
+cudaError_t comm_trace_count(uint32_t* n) {
+  return cudaMemcpyFromSymbol(n, g_comm_trace_n, sizeof *n);
 }
 
 cudaError_t launch_set_lr(HyperParams* hp, float lr, cudaStream_t s) {

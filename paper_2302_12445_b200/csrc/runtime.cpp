@@ -1405,6 +1405,23 @@ int dear_synchronize(dear_ctx* ctx) {
   DEAR_API_END
 }
 
+int dear_set_comm_trace(void* device_buffer, int64_t capacity) {
+  DEAR_API_BEGIN
+  if (capacity < 0 || capacity > 0xffffffffLL) invalid("dear_set_comm_trace: bad capacity");
+  cuda_check(set_comm_trace(device_buffer, device_buffer ? static_cast<uint32_t>(capacity) : 0u),
+             "dear_set_comm_trace");
+  DEAR_API_END
+}
+
+int dear_comm_trace_count(int64_t* n) {
+  DEAR_API_BEGIN
+  if (!n) invalid("dear_comm_trace_count: null output");
+  uint32_t v = 0;
+  cuda_check(comm_trace_count(&v), "dear_comm_trace_count");
+  *n = v;
+  DEAR_API_END
+}
+
 int dear_comm_error(dear_ctx* ctx, int32_t* failed) {
   DEAR_API_BEGIN
   need(ctx, true);
