@@ -60,7 +60,7 @@ def main():
     for _ in range(3):
         run()
     torch.cuda.synchronize()
-    bufs = [torch.zeros(8 * 160, dtype=torch.int64, device="cuda") for _ in range(a.launches)]
+    bufs = [torch.zeros(8 * 320, dtype=torch.int64, device="cuda") for _ in range(a.launches)]
     for b in bufs:
         set_trace(b)
         run()
