@@ -41,8 +41,8 @@ def main():
                     early_operands=True) for G in Gs]
     s = torch.cuda.Stream()
     out = []
-    for wbn, wpair in ((128, 0), (256, 0), (128, 1), (256, 1)):
-        for sp in (2, 4, 6, 8, 12, 16, 24):
+    for wbn, wpair in ((128, 0), (256, 0)):
+        for sp in (1, 2, 4, 8, 16, 24):
             try:
                 for w in wgs:
                     w.set_tile(wbn, wpair)
@@ -65,8 +65,17 @@ def main():
             idx = range(len(t))
             wend = max((end[i] for i in idx if ok[i] and i < n_w), default=0.0)
             dend = max((end[i] for i in idx if ok[i] and i >= n_w), default=0.0)
+            import numpy as np
+            wi = [i for i in idx if ok[i] and i < n_w]
+            rel = (t - t0) / 1e3
+            first = np.median([rel[i, 3] for i in wi]) if wi else 0.0
+            mma = np.median([rel[i, 4] - rel[i, 3] for i in wi]) if wi else 0.0
+            epi = np.median([rel[i, 5] - rel[i, 4] for i in wi]) if wi else 0.0
+            epi_max = max([rel[i, 5] - rel[i, 4] for i in wi], default=0.0)
             rec = {"wgrad_bn": wbn, "pair": wpair, "splits": items["splits"], "wgrad_items": n_w,
                    "chain_us": us, "traced_wgrad_end_us": wend, "traced_dgrad_end_us": dend,
+                   "wgrad_first_stage_us": float(first), "wgrad_mainloop_us": float(mma),
+                   "wgrad_epilogue_us_median": float(epi), "wgrad_epilogue_us_max": float(epi_max),
                    "ctas": int(ok.sum())}
             out.append(rec)
             print(json.dumps(rec), flush=True)
