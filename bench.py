@@ -97,46 +97,66 @@ def parse():
 
 # --------------------------------------------------------------- helpers ----
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks / throttle reasons sampled during the timed region.
+
+    The sampler runs from before the region (its first sample is awaited, so
+    the region is covered from its start) to after it; every sample carries its
+    arrival time and the summary keeps the ones inside [start, end] of the
+    timed region (time_loop marks them), falling back to all samples when the
+    region is shorter than the sampling period."""
 
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, period_ms: int = 25):
         self.index, self.proc, self.rows = index, None, []
+        self.period_ms = period_ms
+        self.start = self.end = None
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", str(self.period_ms)],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.monotonic()
+            while not self.rows and time.monotonic() - t0 < 3.0:
+                time.sleep(0.01)
         except FileNotFoundError:
             self.proc = None
         return self
 
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+            self.rows.append((time.monotonic(), [x.strip() for x in line.split(",")]))
+
+    def mark(self, which: str) -> None:
+        setattr(self, which, time.monotonic())
 
     def __exit__(self, *a):
         if self.proc:
-            time.sleep(0.25)
+            time.sleep(2 * self.period_ms / 1e3)
             self.proc.terminate()
             self.proc.wait(timeout=5)
 
     def summary(self) -> dict:
-        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
+        rows = [r for t, r in self.rows if self.start is not None and self.end is not None
+                and self.start <= t <= self.end + self.period_ms / 1e3]
+        in_region = len(rows)
+        if not rows:
+            rows = [r for _, r in self.rows]
+        sm = [float(r[0]) for r in rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows if len(r) >= 7
+        reasons = sorted({names[i] for r in rows if len(r) >= 7
                           for i in range(4) if r[3 + i].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+                "samples": len(rows), "samples_in_timed_region": in_region,
+                "period_ms": self.period_ms}
 
 
 def peaks():
@@ -259,7 +279,7 @@ class Step:
                 self.out_host.copy_(m.result_scalar(), non_blocking=True)
 
 
-def time_loop(fn, steps, warmup, stream, dist_on):
+def time_loop(fn, steps, warmup, stream, dist_on, clock=None):
     import torch
 
     for _ in range(warmup):
@@ -269,11 +289,15 @@ def time_loop(fn, steps, warmup, stream, dist_on):
         torch.distributed.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if clock is not None:
+        clock.mark("start")
     e0.record(stream)
     for _ in range(steps):
         fn()
     e1.record(stream)
     torch.cuda.synchronize()
+    if clock is not None:
+        clock.mark("end")
     ms = e0.elapsed_time(e1)
     if dist_on:
         t = torch.tensor([ms], device="cuda")
@@ -454,7 +478,7 @@ def gpu_arm(a, wl, world, rank, local_rank):
             print(json.dumps({"profile_steps": a.profile_steps}), flush=True)
         return None
     with ClockSampler(local_rank) as clk:
-        ms = time_loop(run, a.steps, a.warmup, stream, dist_on)
+        ms = time_loop(run, a.steps, a.warmup, stream, dist_on, clock=clk)
     res["dear_ms"] = ms
     clocks = clk.summary()
 
