@@ -97,37 +97,65 @@ def parse():
 
 # --------------------------------------------------------------- helpers ----
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region.
-
-    The sampler runs from before the region (its first sample is awaited, so
-    the region is covered from its start) to after it; every sample carries its
-    arrival time and the summary keeps the ones inside [start, end] of the
-    timed region (time_loop marks them), falling back to all samples when the
-    region is shorter than the sampling period."""
+    """SM clocks and throttle reasons sampled during the timed region: NVML
+    polled from a thread every `period_ms` (nvidia-smi's own sampling is too
+    coarse for a region of a few tens of ms; it remains the fallback). Samples
+    carry their time; the summary keeps the ones inside [start, end] of the
+    timed region (time_loop marks them)."""
 
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
-    def __init__(self, index: int, period_ms: int = 25):
+    def __init__(self, index: int, period_ms: float = 2.0):
         self.index, self.proc, self.rows = index, None, []
         self.period_ms = period_ms
         self.start = self.end = None
+        self.source = None
+        self._stop = threading.Event()
 
     def __enter__(self):
         try:
+            import pynvml as N
+
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+            bits = [N.nvmlClocksEventReasonHwSlowdown, N.nvmlClocksEventReasonHwThermalSlowdown,
+                    N.nvmlClocksEventReasonSwThermalSlowdown, N.nvmlClocksEventReasonSwPowerCap]
+            mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+
+            def poll():
+                while not self._stop.is_set():
+                    try:
+                        sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+                        rs = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    except Exception:
+                        break
+                    flags = ["Active" if rs & b else "Not Active" for b in bits]
+                    self.rows.append((time.monotonic(), [str(sm), str(mx), "0", *flags]))
+                    time.sleep(self.period_ms / 1e3)
+            self.t = threading.Thread(target=poll, daemon=True)
+            self.t.start()
+            self.source = "nvml"
+        except Exception:
+            self._start_smi()
+        t0 = time.monotonic()
+        while not self.rows and time.monotonic() - t0 < 3.0:
+            time.sleep(0.005)
+        return self
+
+    def _start_smi(self):
+        try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", str(self.period_ms)],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
-            t0 = time.monotonic()
-            while not self.rows and time.monotonic() - t0 < 3.0:
-                time.sleep(0.01)
+            self.source = "nvidia-smi"
         except FileNotFoundError:
             self.proc = None
-        return self
 
     def _read(self):
         for line in self.proc.stdout:
@@ -137,26 +165,25 @@ class ClockSampler:
         setattr(self, which, time.monotonic())
 
     def __exit__(self, *a):
+        self._stop.set()
         if self.proc:
-            time.sleep(2 * self.period_ms / 1e3)
             self.proc.terminate()
             self.proc.wait(timeout=5)
 
     def summary(self) -> dict:
         rows = [r for t, r in self.rows if self.start is not None and self.end is not None
-                and self.start <= t <= self.end + self.period_ms / 1e3]
+                and self.start <= t <= self.end]
         in_region = len(rows)
         if not rows:
             rows = [r for _, r in self.rows]
         sm = [float(r[0]) for r in rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
         mx = [float(r[1]) for r in rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows if len(r) >= 7
+        reasons = sorted({self.NAMES[i] for r in rows if len(r) >= 7
                           for i in range(4) if r[3 + i].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
                 "samples": len(rows), "samples_in_timed_region": in_region,
-                "period_ms": self.period_ms}
+                "source": self.source}
 
 
 def peaks():

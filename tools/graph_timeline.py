@@ -107,7 +107,7 @@ def main():
             torch.cuda.synchronize()
             wall = _t.time() - t0
         clocks = dict(clk.summary(), wall_ms_per_step=1e3 * wall / a.clock_steps)
-        pw = [float(r[2]) for _, r in clk.rows if len(r) >= 7 and r[2].replace(".", "").isdigit()]
+        pw = [float(r[2]) for _, r in clk.rows if len(r) >= 7 and r[2].replace(".", "").isdigit() and float(r[2]) > 0]
         clocks["power_w_median"] = sorted(pw)[len(pw) // 2] if pw else None
     marks = {k: ev["base"].elapsed_time(ev[k]) for k in ("ff", "bp", "end")}
     out = {"rank": rank, "policy": a.policy, "gd": a.group_dependency, "marks_ms": marks,
