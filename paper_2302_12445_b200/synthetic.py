@@ -197,6 +197,22 @@ class SyntheticModel:
             trials.append((time_chain(bp_real, L, s, reps=2), wc, sp, red, dc))
         trials.sort(key=lambda t: t[0])
         us, best_wg, best_sp, best_red, best_dg = trials[0]
+        # Multi-rank: every rank runs rank 0's choice. Per-rank tuning noise
+        # would otherwise give the ranks different layer times, and the
+        # reduce-scatter of every bucket waits for the slowest rank.
+        import torch.distributed as dist
+
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+            pick = [(best_ff, self.ff_transposed, best_wg, best_sp, best_red, best_dg, us,
+                     ff[0][0])]
+            dist.broadcast_object_list(pick, 0)
+            best_ff, transposed, best_wg, best_sp, best_red, best_dg, us, ff_us = pick[0]
+            if transposed != self.ff_transposed:
+                self.ff, self.ff_t = self.ff_t, self.ff
+                self.ff_transposed = transposed
+            for l in range(self.L):
+                self.ff[l].set_tile(*best_ff)
+            ff = [(ff_us,) + tuple(best_ff)] + list(ff[1:])
         set_bp(best_wg, best_sp, best_red, best_dg)
         self.zero_grad()
         torch.cuda.synchronize()
