@@ -42,9 +42,13 @@ constexpr int kThreads = DEAR_KTHREADS;
 #define DEAR_HBM_UNROLL 4
 #endif
 constexpr int kUnroll = DEAR_HBM_UNROLL;
-// Remote (NVLink) source streams keep more loads in flight per lane.
+// Remote (NVLink) source streams: float4 loads in flight per lane in the
+// all-gather. 4, not the 8 that minimise the kernel in isolation: the comm
+// kernels run next to L2-bound GEMMs, and a gentler stream costs the GEMMs less
+// than it costs itself (BERT-L N = 4 step 8.25 vs 8.96 ms with KU below,
+// profiles/r02v2_comm_throttle.log).
 #ifndef DEAR_PEER_UNROLL
-#define DEAR_PEER_UNROLL 8
+#define DEAR_PEER_UNROLL 4
 #endif
 constexpr int kPeerUnroll = DEAR_PEER_UNROLL;
 constexpr int kSms = 148;
@@ -775,12 +779,17 @@ __device__ __forceinline__ void store_bf16x4(__nv_bfloat16* sh, int64_t q, float
 // order, so Unit::start + offset is the chunk position). Parameters and
 // gradients share their 16 B phase (registration requires 16 B alignment),
 // so after a scalar head every stream is float4-aligned.
-// Vectors per lane per round (each with P gradient loads in flight).
+// Vectors per lane per round (each with P gradient loads in flight). One:
+// throttled for the same reason as DEAR_PEER_UNROLL — in the step, the
+// reduce-scatter's NVLink / L2 pressure slows the concurrent backprop GEMMs
+// more than a faster reduce-scatter saves. Measured in-step (comm_trace,
+// profiles/r02v2_comm_throttle.log): BERT-L N = 4 8.95 -> 7.58 ms (KU 2 -> 1
+// with unroll 4), N = 2 8.27 -> 7.46 ms (KU 4 -> 1).
 #ifndef DEAR_ZC_KU2
-#define DEAR_ZC_KU2 4
+#define DEAR_ZC_KU2 1
 #endif
 #ifndef DEAR_ZC_KU4
-#define DEAR_ZC_KU4 2
+#define DEAR_ZC_KU4 1
 #endif
 #ifndef DEAR_ZC_KU8
 #define DEAR_ZC_KU8 1
