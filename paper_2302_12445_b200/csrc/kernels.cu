@@ -766,7 +766,7 @@ __device__ __forceinline__ void store_bf16x4(__nv_bfloat16* sh, int64_t q, float
   uint2 packed;
   packed.x = *reinterpret_cast<uint32_t*>(&lo);
   packed.y = *reinterpret_cast<uint32_t*>(&hi);
-#ifdef DEAR_ZC_EVICT
+#ifndef DEAR_ZC_NO_EVICT
   __stcs(reinterpret_cast<uint2*>(sh) + q, packed);
 #else
   reinterpret_cast<uint2*>(sh)[q] = packed;
@@ -794,9 +794,10 @@ __device__ __forceinline__ void store_bf16x4(__nv_bfloat16* sh, int64_t q, float
 #ifndef DEAR_ZC_KU8
 #define DEAR_ZC_KU8 1
 #endif
-// DEAR_ZC_EVICT (experiment): evict-first hints on every zero-copy stream so
-// the comm traffic does not push the backprop GEMMs' operands out of L2.
-#ifdef DEAR_ZC_EVICT
+// Evict-first hints on every zero-copy stream so the comm traffic does not
+// push the backprop GEMMs' operands out of L2 (in-step BERT-L, P = 4: 7.48 ->
+// 7.33 ms, tools/micro/var_sweep2.sh); DEAR_ZC_NO_EVICT restores plain accesses.
+#ifndef DEAR_ZC_NO_EVICT
 #define ZC_LDR(p) __ldcs(p)
 #define ZC_LDW(p) __ldcs(p)
 #define ZC_ST(p, v) __stcs(p, v)
