@@ -53,11 +53,16 @@ constexpr int kSlices = 148 * DEAR_SLICES_PER_SM;
 #ifndef DEAR_UNPACK_CTAS_PER_SM
 #define DEAR_UNPACK_CTAS_PER_SM 4
 #endif
-constexpr int kPackSlices = 148 * DEAR_PACK_CTAS_PER_SM;
-constexpr int kUnpackSlices = 148 * DEAR_UNPACK_CTAS_PER_SM;
+// Waves of CTAs per launch (slices = resident CTAs x waves; > 1 lets the
+// block scheduler balance short slices as CTAs retire).
+#ifndef DEAR_HBM_WAVES
+#define DEAR_HBM_WAVES 1
+#endif
+constexpr int kPackSlices = 148 * DEAR_PACK_CTAS_PER_SM * DEAR_HBM_WAVES;
+constexpr int kUnpackSlices = 148 * DEAR_UNPACK_CTAS_PER_SM * DEAR_HBM_WAVES;
 static_assert(kPackSlices <= kSlices && kUnpackSlices <= kSlices, "slice regions are kSlices long");
-constexpr int kUpdSlices = 148 * DEAR_UPD_CTAS_PER_SM;
-constexpr int kDirSlices = 148 * DEAR_DIR_CTAS_PER_SM;
+constexpr int kUpdSlices = 148 * DEAR_UPD_CTAS_PER_SM * DEAR_HBM_WAVES;
+constexpr int kDirSlices = 148 * DEAR_DIR_CTAS_PER_SM * DEAR_HBM_WAVES;
 static_assert(kUpdSlices <= kSlices && kDirSlices <= kSlices, "slice regions are kSlices long");
 // NVLink-bound peer kernels need far fewer CTAs to saturate the links
 // (~1.2 MB in flight); a small grid leaves the SMs to the concurrent GEMMs.

@@ -76,10 +76,22 @@ __device__ __forceinline__ float4 realign(float4 a, float4 b) {
 
 enum class Hint { kStream, kKeep };
 
+// Streaming (evict-first) stores for the pack / unpack destinations:
+// graph-chained ResNet-50 buckets, pack 0.636 -> 0.660 and unpack 0.666 ->
+// 0.708 of HBM peak (tools/micro/hbm_stage.py, profiles/r02h5_hbm_ab.log).
+#ifndef DEAR_HBM_NO_ST_CS
+#define HBM_ST4(p, v) __stcs(p, v)
+#else
+#define HBM_ST4(p, v) (*(p) = (v))
+#endif
 template <Hint H>
 __device__ __forceinline__ float4 ld4(const float4* p) {
   if constexpr (H == Hint::kStream) {
+#ifdef DEAR_HBM_LD_PLAIN  // experiment: default-policy loads
+    return *p;
+#else
     return __ldcs(p);
+#endif
   } else {
     return __ldg(p);
   }
@@ -419,7 +431,7 @@ __global__ void __launch_bounds__(kThreads, (kSignal && kPeerPackLight) ? 1 : DE
           v.y = __fmul_rn(v.y, scale);
           v.z = __fmul_rn(v.z, scale);
           v.w = __fmul_rn(v.w, scale);
-          reinterpret_cast<float4*>(dst + head)[q] = v;
+          HBM_ST4(reinterpret_cast<float4*>(dst + head) + q, v);
         });
   });
   if (kSignal) signal_done(&flags->done[0], &flags->packed);
@@ -535,7 +547,7 @@ __global__ void __launch_bounds__(kThreads, DEAR_UNPACK_CTAS_PER_SM) unpack_kern
           if (kShadow && sh) sh[i] = __float2bfloat16_rn(v);
         },
         [&](int64_t head, int64_t q, float4 v) {
-          reinterpret_cast<float4*>(dst + head)[q] = v;
+          HBM_ST4(reinterpret_cast<float4*>(dst + head) + q, v);
           if (kShadow && sh) {
             __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y);
             __nv_bfloat162 hi = __floats2bfloat162_rn(v.z, v.w);
