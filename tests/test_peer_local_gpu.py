@@ -23,7 +23,8 @@ def _close(a, b, tol=1e-5):
     return np.all(np.abs(a - b) <= tol * np.maximum(1.0, np.abs(b)))
 
 
-@pytest.mark.parametrize("P", [2, 3, 4])
+# P = 8 runs the compile-time 8-rank kernel instances (the 8-GPU bench path).
+@pytest.mark.parametrize("P", [2, 3, 4, 8])
 @pytest.mark.parametrize("zero_copy", [True, False])
 @pytest.mark.parametrize("policy,buf", POLICIES)
 def test_peer_kernels_bit_exact(restated, P, zero_copy, policy, buf):
