@@ -76,6 +76,9 @@ def parse():
     ap.add_argument("--no-calibrate", action="store_true",
                     help="north star: skip the t_ag = 1.25 t_ff batch comparison (N > 1)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--buffer-sweep-bytes", default="5000000,10000000,25000000,50000000",
+                    help="N > 1: BASELINE config 3 (BERT-Base) DeAR vs WFBP at these fusion "
+                         "buffers ('' to skip)")
     ap.add_argument("--extra-workload", default="bert_large",
                     help="also measure DeAR vs WFBP on this workload (north-star "
                          "comparison); 'none' to skip")
@@ -551,6 +554,9 @@ def gpu_arm(a, wl, world, rank, local_rank):
     extra = None
     if a.extra_workload != "none" and a.extra_workload != a.workload:
         extra = compare_policies(a, a.extra_workload, comm, world, rank, stream)
+    config3 = None
+    if world > 1 and a.buffer_sweep_bytes:
+        config3 = buffer_sweep(a, "bert_base", comm, world, rank, stream)
     # Post-timing checks (nothing below is timed): one measured iteration in the
     # reference's trace schema, validated; oracle parity of one full bucket at
     # the bench configuration.
@@ -644,6 +650,8 @@ def gpu_arm(a, wl, world, rank, local_rank):
         line["busbw_gbs"] = busbw
     if extra is not None:
         line["north_star"] = extra
+    if config3 is not None:
+        line["config3_buffer_sweep"] = config3
     if parity is not None:
         line["parity"] = parity
     if timeline is not None:
@@ -1026,6 +1034,42 @@ def _priority_partition(a, model, comm, world, rank, stream, batch, steps, warm)
     return {"partition_bytes": a.partition_bytes, "parts": len(st), "ms_per_step": ms,
             "samples_per_s": batch * world / (ms / 1e3),
             "predicted_ms": sim["iteration_seconds"] * 1e3}
+
+
+def buffer_sweep(a, wl_name, comm, world, rank, stream):
+    """BASELINE config 3: DeAR vs WFBP on the BERT-Base-shaped layers over a
+    fusion-buffer sweep (same kernels, default transport), each measured step
+    beside the reference scheduler's prediction on this run's measured stage
+    times (simulate.cpp:65-159)."""
+    import torch
+
+    from paper_2302_12445_b200.presets import preset_param_counts
+    from paper_2302_12445_b200.synthetic import SyntheticModel
+
+    wl = WORKLOADS[wl_name]
+    steps, warm = max(5, a.steps // 2), max(3, a.warmup)
+    batch = wl["batch"]
+    model = SyntheticModel(preset_param_counts(wl["preset"]), wl["hidden"],
+                           batch * wl["tokens_per_sample"], seed=4321)
+    run = make_runner(Step(model, None, stream), True, stream)
+    comp = time_loop(run, steps, warm, stream, True)
+    out = {"workload": wl["config"], "batch_per_gpu": batch, "compute_only_ms": comp,
+           "steps": steps, "warmup": warm, "buffers": {}}
+    for buf in (int(x) for x in a.buffer_sweep_bytes.split(",") if x.strip()):
+        r = _policy_pair(a, model, comm, world, rank, stream, batch, steps, warm, buffer=buf)
+        d, w = r[a.policy]["ms_per_step"], r[a.baseline_policy]["ms_per_step"]
+        row = {"DEAR_ms": d, "WFBP_ms": w, "dear_over_wfbp": w / d,
+               "exposed_comm_pct": max(0.0, 100 * (d - comp) / d),
+               "wfbp_exposed_comm_pct": max(0.0, 100 * (w - comp) / w),
+               "collectives": r.get("collectives")}
+        if "simulated" in r:
+            row["predicted_DEAR_ms"] = r["simulated"][a.policy]["predicted_ms"]
+            row["predicted_WFBP_ms"] = r["simulated"][a.baseline_policy]["predicted_ms"]
+        out["buffers"][str(buf)] = row
+    model.close()
+    del model
+    torch.cuda.empty_cache()
+    return out
 
 
 def compare_policies(a, wl_name, comm, world, rank, stream):
