@@ -236,7 +236,12 @@ int dear_peer_handle(dear_ctx* ctx, uint8_t out[DEAR_PEER_HANDLE_BYTES]);
  * environment variable DEAR_ZERO_COPY=0 disables it. Gradients are then
  * "consumed" (dear_step's fence) once every rank's reduce-scatters finished. */
 int dear_peer_connect(dear_ctx* ctx, const uint8_t* handles, int32_t n);
-/* *on = 1 when dear_peer_connect enabled the zero-copy path. */
+/* *on = 1 when dear_peer_connect enabled the zero-copy path, 2 when it also
+ * took the push reduce-scatter (DEAR_PUSH_RS=1 set on every rank before
+ * dear_finalize: each rank writes every chunk of its gradients into slot
+ * `rank` of the chunk owner's push buffer over NVLink; the owner sums its P
+ * slots locally in ring order — same sums, same bits; the all-gather stays
+ * the zero-copy pull). */
 int dear_peer_zero_copy(dear_ctx* ctx, int32_t* on);
 
 /* ---------------------------------------------------------------------------

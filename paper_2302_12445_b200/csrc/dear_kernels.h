@@ -158,6 +158,12 @@ cudaError_t launch_update_direct(const Unit* units, const Slice* slices, int64_t
 // `slices` holds kPackPeerSlices entries (one per CTA).
 cudaError_t launch_pack_signal(const Unit* units, const Slice* slices, int64_t total, float scale,
                                BucketFlags* flags, const PeerArgs& pa, cudaStream_t s);
+// Push reduce-scatter (DEAR_PUSH_RS=1 on the zero-copy layout): every chunk of
+// our gradients (x scale) to slot `rank` of its owner's bucket buffer (unit
+// peer = owner, reached at U.b + pa.delta[owner]) once every owner reduced
+// our previous push; then flags->packed += 1. `slices`: kPackPeerSlices.
+cudaError_t launch_pack_push(const Unit* units, const Slice* slices, float scale,
+                             BucketFlags* flags, const PeerArgs& pa, cudaStream_t s);
 // Fused reduce-scatter + shard SGD update: for each own-shard element, sum the
 // peers' slot-`rank` values in ring order (rank+1, ..., rank), update, write
 // w' into the own slot; then flags->updated += 1.
@@ -179,10 +185,13 @@ cudaError_t launch_ag_unpack_peer(const Unit* units, const Slice* slices, int64_
 // gradients (at ga.delta[k]) summed in ring order, 1/P, SGD, written into
 // the own parameters (+ bf16 copy); announces / waits on flags->packed and
 // bumps flags->updated. mom_base: the bucket's momentum shard (or null).
+// announce = 0 (push reduce-scatter): the pack already announced; ga then
+// holds the local slot offsets (slot k = rank k's pushed contribution).
 cudaError_t launch_rs_update_zc(const Unit* units, const Slice* slices, const HyperParams* hp,
                                 int has_momentum_buf, float* mom_base, int use_momentum,
                                 int use_wd, int with_shadow, const PeerArgs& pa,
-                                const PeerArgs& ga, BucketFlags* flags, cudaStream_t s);
+                                const PeerArgs& ga, BucketFlags* flags, cudaStream_t s,
+                                int announce = 1);
 
 // Comm-kernel phase trace (profiling): records of 40 B {t0, t_arrived, t_end,
 // kind, tag, epoch, cta}; buf = null turns it off; the count restarts at 0.

@@ -402,29 +402,40 @@ __device__ __forceinline__ void cta_wait_peers(const uint32_t* mine, const uint3
 #define DEAR_PACK_PEER_UNROLL 16
 #endif
 constexpr int kPackPeerUnroll = DEAR_PACK_PEER_UNROLL;
+// Push reduce-scatter pack: vectors per lane per round (posted NVLink stores);
+// in-step BERT-L N = 4: 16 -> 8.92 ms, 4 -> 8.43, 1 -> 8.15 (pull: 7.47-7.60).
+#ifndef DEAR_PUSH_UNROLL
+#define DEAR_PUSH_UNROLL 1
+#endif
 #ifdef DEAR_PEER_PACK_FULL
 constexpr bool kPeerPackLight = false;  // experiment: peer pack on the full grid
 #else
 constexpr bool kPeerPackLight = true;
 #endif
-template <bool kSignal>
 #ifndef DEAR_PACK_UNROLL
 #define DEAR_PACK_UNROLL kUnroll
 #endif
 #ifndef DEAR_UNPACK_UNROLL
 #define DEAR_UNPACK_UNROLL kUnroll
 #endif
+// kPush (push reduce-scatter, DEAR_PUSH_RS): the destination is slot `rank`
+// of the chunk owner's bucket buffer, U.b + pa.delta[U.peer] (posted stores
+// over NVLink; the own chunk stays local).
+template <bool kSignal, bool kPush = false>
 __global__ void __launch_bounds__(kThreads, (kSignal && kPeerPackLight) ? 1 : DEAR_PACK_CTAS_PER_SM) pack_kernel(const Unit* __restrict__ units,
                                                            const Slice* __restrict__ slices,
                                                            float scale, BucketFlags* flags,
                                                            PeerArgs pa, int n_slices) {
   if (!kSignal) pdl_enter();
   // Peer backend: our slots may be rewritten once every peer gathered them.
-  if (kSignal) cta_wait_peers(&flags->packed, &flags->gathered, pa);
+  // Push: the owners' slots may be rewritten once every owner has reduced
+  // (and so read) what we pushed last time.
+  if (kSignal) cta_wait_peers(&flags->packed, kPush ? &flags->updated : &flags->gathered, pa);
   walk_slice(units, slices, n_slices, [&](const Unit& U, int64_t off, int64_t n) {
     const float* src = U.a + off;
-    float* dst = U.b + off;
-    run_unit<Hint::kStream, (kSignal && kPeerPackLight) ? kPackPeerUnroll : DEAR_PACK_UNROLL>(
+    float* dst = kPush ? const_cast<float*>(at_peer(U.b + off, pa.delta[U.peer])) : U.b + off;
+    run_unit<Hint::kStream, kPush ? DEAR_PUSH_UNROLL
+                                  : ((kSignal && kPeerPackLight) ? kPackPeerUnroll : DEAR_PACK_UNROLL)>(
         src, dst, n, [&](int64_t i) { dst[i] = __fmul_rn(src[i], scale); },
         [&](int64_t head, int64_t q, float4 v) {
           v.x = __fmul_rn(v.x, scale);
@@ -434,6 +445,11 @@ __global__ void __launch_bounds__(kThreads, (kSignal && kPeerPackLight) ? 1 : DE
           HBM_ST4(reinterpret_cast<float4*>(dst + head) + q, v);
         });
   });
+  if (kPush) {
+    // Remote stores: every CTA fences at system scope before it counts.
+    __syncthreads();
+    if (threadIdx.x == 0) __threadfence_system();
+  }
   if (kSignal) signal_done(&flags->done[0], &flags->packed);
 }
 
@@ -751,9 +767,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 // last CTA finishes, after every CTA passed its wait, so it is this
 // iteration's epoch on every rank.
 __device__ __forceinline__ void cta_announce_and_wait(BucketFlags* flags, const PeerArgs& pa,
-                                                      Blk b) {
+                                                      Blk b, bool announce = true) {
   if (threadIdx.x < 32) {
-    if (b.id == 0 && threadIdx.x == 0) {
+    if (announce && b.id == 0 && threadIdx.x == 0) {
       __threadfence_system();
       atomicAdd_system(&flags->packed, 1u);
     }
@@ -823,10 +839,11 @@ __device__ __forceinline__ void rs_update_zc_body(const Unit* __restrict__ units
                                                   const Slice* __restrict__ slices,
                                                   const HyperParams* __restrict__ hpp, int has_buf,
                                                   float* mom_base, const PeerArgs& pa,
-                                                  const PeerArgs& ga, BucketFlags* flags, Blk blk) {
+                                                  const PeerArgs& ga, BucketFlags* flags, Blk blk,
+                                                  bool announce = true) {
   trace_stamp(0);
   const uint32_t epoch = g_comm_trace ? *reinterpret_cast<volatile uint32_t*>(&flags->updated) : 0u;
-  cta_announce_and_wait(flags, pa, blk);
+  cta_announce_and_wait(flags, pa, blk, announce);
   trace_stamp(1);
   const HyperParams hp = *hpp;
   const int P = PC > 0 ? PC : pa.P;
@@ -931,9 +948,9 @@ template <int PC, bool kMom, bool kWd, bool kShadow>
 __global__ void DEAR_ZC_BOUNDS
     rs_update_zc_kernel(const Unit* __restrict__ units, const Slice* __restrict__ slices,
                         const HyperParams* __restrict__ hpp, int has_buf, float* mom_base,
-                        PeerArgs pa, PeerArgs ga, BucketFlags* flags) {
+                        PeerArgs pa, PeerArgs ga, BucketFlags* flags, int announce) {
   rs_update_zc_body<PC, kMom, kWd, kShadow>(units, slices, hpp, has_buf, mom_base, pa, ga, flags,
-                                            this_blk());
+                                            this_blk(), announce != 0);
 }
 
 // ------------------------------------------- fused peer AG+unpack ---------
@@ -1352,6 +1369,13 @@ cudaError_t launch_pack_signal(const Unit* units, const Slice* slices, int64_t t
   return cudaGetLastError();
 }
 
+cudaError_t launch_pack_push(const Unit* units, const Slice* slices, float scale,
+                             BucketFlags* flags, const PeerArgs& pa, cudaStream_t s) {
+  pack_kernel<true, true><<<bucket_grid(kPackPeerSlices), kThreads, 0, s>>>(units, slices, scale,
+                                                                           flags, pa, kPackPeerSlices);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_wait_peers(const uint32_t* mine, const uint32_t* watch, const PeerArgs& pa,
                               cudaStream_t s) {
   wait_peers_kernel<<<1, 32, 0, s>>>(mine, watch, pa);
@@ -1402,40 +1426,42 @@ cudaError_t launch_ag_unpack_peer(const Unit* units, const Slice* slices, int64_
 template <int PC, bool kMom, bool kWd>
 void launch_rs_zc_p(const Unit* units, const Slice* slices, const HyperParams* hp, int has_buf,
                     float* mom_base, int with_shadow, const PeerArgs& pa, const PeerArgs& ga,
-                    BucketFlags* flags, cudaStream_t s) {
+                    BucketFlags* flags, int announce, cudaStream_t s) {
   const int grid = bucket_grid(kZcSlices);
   const size_t smem = 0;
   if (with_shadow)
-    rs_update_zc_kernel<PC, kMom, kWd, true><<<grid, kThreads, smem, s>>>(units, slices, hp, has_buf,
-                                                                        mom_base, pa, ga, flags);
+    rs_update_zc_kernel<PC, kMom, kWd, true><<<grid, kThreads, smem, s>>>(
+        units, slices, hp, has_buf, mom_base, pa, ga, flags, announce);
   else
-    rs_update_zc_kernel<PC, kMom, kWd, false><<<grid, kThreads, smem, s>>>(units, slices, hp, has_buf,
-                                                                         mom_base, pa, ga, flags);
+    rs_update_zc_kernel<PC, kMom, kWd, false><<<grid, kThreads, smem, s>>>(
+        units, slices, hp, has_buf, mom_base, pa, ga, flags, announce);
 }
 
 template <int PC>
 void launch_rs_zc_pc(const Unit* units, const Slice* slices, const HyperParams* hp, int has_buf,
                      float* mom_base, int use_momentum, int use_wd, int with_shadow,
-                     const PeerArgs& pa, const PeerArgs& ga, BucketFlags* flags, cudaStream_t s) {
+                     const PeerArgs& pa, const PeerArgs& ga, BucketFlags* flags, int announce,
+                     cudaStream_t s) {
   if (use_momentum && use_wd)
-    launch_rs_zc_p<PC, true, true>(units, slices, hp, has_buf, mom_base, with_shadow, pa, ga, flags, s);
+    launch_rs_zc_p<PC, true, true>(units, slices, hp, has_buf, mom_base, with_shadow, pa, ga, flags, announce, s);
   else if (use_momentum)
-    launch_rs_zc_p<PC, true, false>(units, slices, hp, has_buf, mom_base, with_shadow, pa, ga, flags, s);
+    launch_rs_zc_p<PC, true, false>(units, slices, hp, has_buf, mom_base, with_shadow, pa, ga, flags, announce, s);
   else if (use_wd)
-    launch_rs_zc_p<PC, false, true>(units, slices, hp, has_buf, mom_base, with_shadow, pa, ga, flags, s);
+    launch_rs_zc_p<PC, false, true>(units, slices, hp, has_buf, mom_base, with_shadow, pa, ga, flags, announce, s);
   else
-    launch_rs_zc_p<PC, false, false>(units, slices, hp, has_buf, mom_base, with_shadow, pa, ga, flags, s);
+    launch_rs_zc_p<PC, false, false>(units, slices, hp, has_buf, mom_base, with_shadow, pa, ga, flags, announce, s);
 }
 
 cudaError_t launch_rs_update_zc(const Unit* units, const Slice* slices, const HyperParams* hp,
                                 int has_momentum_buf, float* mom_base, int use_momentum,
                                 int use_wd, int with_shadow, const PeerArgs& pa,
-                                const PeerArgs& ga, BucketFlags* flags, cudaStream_t s) {
+                                const PeerArgs& ga, BucketFlags* flags, cudaStream_t s,
+                                int announce) {
   switch (pa.P) {
-    case 2: launch_rs_zc_pc<2>(units, slices, hp, has_momentum_buf, mom_base, use_momentum, use_wd, with_shadow, pa, ga, flags, s); break;
-    case 4: launch_rs_zc_pc<4>(units, slices, hp, has_momentum_buf, mom_base, use_momentum, use_wd, with_shadow, pa, ga, flags, s); break;
-    case 8: launch_rs_zc_pc<8>(units, slices, hp, has_momentum_buf, mom_base, use_momentum, use_wd, with_shadow, pa, ga, flags, s); break;
-    default: launch_rs_zc_pc<0>(units, slices, hp, has_momentum_buf, mom_base, use_momentum, use_wd, with_shadow, pa, ga, flags, s); break;
+    case 2: launch_rs_zc_pc<2>(units, slices, hp, has_momentum_buf, mom_base, use_momentum, use_wd, with_shadow, pa, ga, flags, announce, s); break;
+    case 4: launch_rs_zc_pc<4>(units, slices, hp, has_momentum_buf, mom_base, use_momentum, use_wd, with_shadow, pa, ga, flags, announce, s); break;
+    case 8: launch_rs_zc_pc<8>(units, slices, hp, has_momentum_buf, mom_base, use_momentum, use_wd, with_shadow, pa, ga, flags, announce, s); break;
+    default: launch_rs_zc_pc<0>(units, slices, hp, has_momentum_buf, mom_base, use_momentum, use_wd, with_shadow, pa, ga, flags, announce, s); break;
   }
   return cudaGetLastError();
 }

@@ -120,6 +120,17 @@ struct Bucket {
   int n_dir = 0;
   int64_t e_dir = 0;
   Slice* dir_s = nullptr;                          // kSlices
+  // Push reduce-scatter: P slots of pstride fp32 (slot k = rank k's pushed
+  // copy of this rank's chunk; pieces padded so each starts in its
+  // parameter's 16 B phase), pack units (a = grad, b = slot `rank` in the
+  // owner's buffer, peer = owner) and RS units (a = slot 0 position, b =
+  // param, c = bf16 copy).
+  int64_t pstride = 0;
+  float* pbuf = nullptr;
+  Unit *ppk_u = nullptr, *prs_u = nullptr;
+  int n_ppk = 0, n_prs = 0;
+  int64_t e_ppk = 0, e_prs = 0;
+  Slice *ppk_ps = nullptr, *prs_ps = nullptr;
   BucketFlags* flags = nullptr;  // peer backend completion counters (in the arena)
   bool any_shadow = false;
   bool mom_init = false;
@@ -191,6 +202,12 @@ struct dear_ctx {
   bool zc = false;
   bool zc_tables = false;  // finalize built the zero-copy unit tables
   PeerArgs ga{}, qa{};
+  // Push reduce-scatter (DEAR_PUSH_RS=1, multi-process zero-copy): each rank
+  // writes every chunk of its gradients into slot `rank` of the chunk owner's
+  // push buffer (posted NVLink stores); the owner sums its P slots locally in
+  // ring order and updates. The all-gather stays the zero-copy pull.
+  bool push_tables = false;
+  bool push = false;
   // Same-device peer group (dear_local_group_create_ex(.., DEAR_LOCAL_PEER)):
   // the P ranks are contexts of this process on one device, and the peer
   // kernels address each other's memory with in-process deltas instead of
@@ -468,6 +485,13 @@ void dear_ctx::exec(const Op& op) {
     case OP_PACK:
       if (direct && !nvls) break;  // P = 1: the update reads the gradients in place
       record_t(op.bucket, T_PACK0);
+      if (push) {
+        cuda_check(launch_pack_push(B->ppk_u, B->ppk_ps, pack_scale, B->flags, pa, comm_stream),
+                   "push pack kernel");
+        cuda_check(cudaEventRecord(packed_ev, comm_stream), "cudaEventRecord");
+        record_t(op.bucket, T_PACK1);
+        break;
+      }
       if (zc || nvls) {  // zero-copy: the reduce-scatter reads the gradients in place
         record_t(op.bucket, T_PACK1);
         break;
@@ -503,6 +527,17 @@ void dear_ctx::exec(const Op& op) {
                                          cfg.momentum != 0.0, cfg.weight_decay != 0.0,
                                          nvls_args(op.bucket), B->flags, comm_stream),
                    "nvls rs+update kernel");
+        if (cfg.momentum != 0.0) B->mom_init = true;
+      } else if (push) {
+        // Our P slots (slot k = rank k's push), summed in ring order; the
+        // pack already announced, so the kernel only waits.
+        PeerArgs sa = pa;
+        for (int k = 0; k < P; ++k)
+          sa.delta[k] = static_cast<int64_t>(k) * B->pstride * static_cast<int64_t>(sizeof(float));
+        cuda_check(launch_rs_update_zc(B->prs_u, B->prs_ps, hp_dev, B->mom_init ? 1 : 0, B->mom,
+                                       cfg.momentum != 0.0, cfg.weight_decay != 0.0,
+                                       B->any_shadow ? 1 : 0, pa, sa, B->flags, comm_stream, 0),
+                   "push rs+update kernel");
         if (cfg.momentum != 0.0) B->mom_init = true;
       } else if (zc) {
         cuda_check(launch_rs_update_zc(B->zrs_u, B->zrs_ps, hp_dev, B->mom_init ? 1 : 0, B->mom,
@@ -591,7 +626,7 @@ void dear_ctx::exec(const Op& op) {
                                             comm_stream),
                    "nvls wait kernel");
         cuda_check(cudaEventRecord(packed_ev, comm_stream), "cudaEventRecord");
-      } else if (zc && !buckets.empty()) {
+      } else if (zc && !push && !buckets.empty()) {
         // Zero-copy: peers read our gradients in their reduce-scatters, so
         // "consumed" means every rank's last (plan-order) RS has finished.
         const BucketFlags* f = buckets.back().flags;
@@ -957,12 +992,36 @@ int dear_finalize(dear_ctx* ctx) {
   // Zero-copy tables for a later dear_peer_connect (multi-process only).
   // (also at P = 1 outside local groups: the NVLS kernels run on one GPU too)
   c.zc_tables = (!c.local && !c.same_dev) || (c.same_dev && c.P > 1);
+  const char* push_env = std::getenv("DEAR_PUSH_RS");
+  c.push_tables = !c.local && !c.same_dev && c.P > 1 && push_env && push_env[0] == '1';
   // Unit tables.
   std::vector<Unit> host_units;
   struct Span { size_t pack, upd, unpack; };
   std::vector<Span> spans(plan.size());
   std::vector<std::vector<int64_t>> begins(plan.size());
   for (size_t g = 0; g < plan.size(); ++g) begins[g] = chunk_begins(c.buckets[g].d, c.P);
+  // Push slot position of a piece: the running offset advanced to the phase
+  // of the piece's parameter (layer offset j; tensors are 16 B aligned).
+  auto push_pos = [](int64_t& so, int64_t j, int64_t len) {
+    so += ((j - so) % 4 + 4) % 4;
+    const int64_t at = so;
+    so += len;
+    return at;
+  };
+  if (c.push_tables) {
+    for (size_t g = 0; g < plan.size(); ++g) {
+      Bucket& B = c.buckets[g];
+      int64_t mx = 0;
+      for (int ch = 0; ch < c.P; ++ch) {
+        int64_t so = 0;
+        for_each_piece(c, B, begins[g][static_cast<size_t>(ch)], begins[g][static_cast<size_t>(ch) + 1],
+                       [&](int, int64_t j, int64_t len, int64_t) { push_pos(so, j, len); });
+        mx = std::max(mx, so);
+      }
+      B.pstride = (mx + 63) / 64 * 64;
+      floats += static_cast<size_t>(B.pstride) * static_cast<size_t>(c.P);
+    }
+  }
   // First pass only counts; pointers are filled once the arena exists.
   for (size_t g = 0; g < plan.size(); ++g) {
     const Bucket& B = c.buckets[g];
@@ -975,13 +1034,15 @@ int dear_finalize(dear_ctx* ctx) {
     size_t nu = 0;
     for_each_piece(c, B, bg[static_cast<size_t>(own)], bg[static_cast<size_t>(own) + 1],
                    [&](int, int64_t, int64_t, int64_t) { ++nu; });
-    units += 2 * n + nu + (c.direct ? n : 0) + (c.zc_tables ? 2 * n : 0);
+    units += 2 * n + nu + (c.direct ? n : 0) + (c.zc_tables ? 2 * n : 0) +
+             (c.push_tables ? n + nu : 0);
   }
   const size_t float_bytes = (floats * sizeof(float) + 255) / 256 * 256;
   const size_t unit_bytes = (units * sizeof(Unit) + 255) / 256 * 256;
   const size_t per_bucket_slices = 3 * static_cast<size_t>(kSlices) + 2 * kPeerSlices +
                                    kPackPeerSlices + (c.direct ? kSlices : 0) +
-                                   (c.zc_tables ? 2 * kZcSlices : 0);
+                                   (c.zc_tables ? 2 * kZcSlices : 0) +
+                                   (c.push_tables ? kPackPeerSlices + kZcSlices : 0);
   const size_t n_slices = plan.size() * per_bucket_slices;
   const size_t slice_bytes = (n_slices * sizeof(Slice) + 255) / 256 * 256;
   // Layout: [bucket buffers + momentum][flags] is identical on every rank (the
@@ -1010,6 +1071,10 @@ int dear_finalize(dear_ctx* ctx) {
     if (mom) {
       B.mom = fp;
       fp += B.stride;
+    }
+    if (c.push_tables) {
+      B.pbuf = fp;
+      fp += B.pstride * c.P;
     }
   }
   host_units.reserve(units);
@@ -1118,6 +1183,41 @@ int dear_finalize(dear_ctx* ctx) {
                   kZcSlices, 2);
       B.zrs_ps = B.pack_s + z0;
       B.zag_ps = B.zrs_ps + kZcSlices;
+    }
+    if (c.push_tables) {
+      // Push pack: chunk ch to slot `rank` of its owner's push buffer.
+      B.ppk_u = up + host_units.size();
+      for (int ch = 0; ch < c.P; ++ch) {
+        const int owner = (ch - 1 + c.P) % c.P;
+        int64_t so = 0;
+        for_each_piece(c, B, bg[static_cast<size_t>(ch)], bg[static_cast<size_t>(ch) + 1],
+                       [&](int l, int64_t j, int64_t len, int64_t) {
+                         const LayerReg& R = c.layers[static_cast<size_t>(l - 1)];
+                         const int64_t at = push_pos(so, j, len);
+                         host_units.push_back({R.grad + j, B.pbuf + c.rank * B.pstride + at, nullptr,
+                                               len, 0, owner, 0});
+                       });
+      }
+      B.n_ppk = static_cast<int>(host_units.size() - static_cast<size_t>(B.ppk_u - up));
+      B.e_ppk = set_starts(host_units, static_cast<size_t>(B.ppk_u - up));
+      // Push RS: the own chunk, slot 0 position -> parameter (+ bf16 copy).
+      B.prs_u = up + host_units.size();
+      int64_t so = 0;
+      for_each_piece(c, B, bg[static_cast<size_t>(own)], bg[static_cast<size_t>(own) + 1],
+                     [&](int l, int64_t j, int64_t len, int64_t) {
+                       const LayerReg& R = c.layers[static_cast<size_t>(l - 1)];
+                       void* sh = R.shadow ? static_cast<void*>(static_cast<uint16_t*>(R.shadow) + j) : nullptr;
+                       host_units.push_back({B.pbuf + push_pos(so, j, len), R.param + j, sh, len, 0, 0, 0});
+                     });
+      B.n_prs = static_cast<int>(host_units.size() - static_cast<size_t>(B.prs_u - up));
+      B.e_prs = set_starts(host_units, static_cast<size_t>(B.prs_u - up));
+      const size_t p0 = 3 * kSlices + 2 * kPeerSlices + kPackPeerSlices + (c.direct ? kSlices : 0) +
+                        (c.zc_tables ? 2 * kZcSlices : 0);
+      make_slices(host_units.data() + (B.ppk_u - up), B.n_ppk, B.e_ppk, hs + p0, kPackPeerSlices, 0);
+      make_slices(host_units.data() + (B.prs_u - up), B.n_prs, B.e_prs, hs + p0 + kPackPeerSlices,
+                  kZcSlices, 2);
+      B.ppk_ps = B.pack_s + p0;
+      B.prs_ps = B.ppk_ps + kPackPeerSlices;
     }
     B.ag_done = new_event(false);
     for (int k = 0; k < T_COUNT; ++k) B.t[k] = new_event(true);
@@ -1541,8 +1641,10 @@ void enable_peer(dear_ctx& c, PeerArgs pa, PeerArgs ga, PeerArgs qa, bool zc) {
   if (zc) {
     // No pack, so no pre-scaling: the update applies 1/P after the ring sum
     // (collective.cpp:159-164's order; for P = 2^k the same bits either way).
+    // The push reduce-scatter's pack pre-scales like the slot path.
     c.zc = true;
-    c.hp_host.prescaled = 0;
+    c.push = c.push_tables;
+    c.hp_host.prescaled = c.push && (c.P & (c.P - 1)) == 0 ? 1 : 0;
     cuda_check(cudaMemcpy(c.hp_dev, &c.hp_host, sizeof(HyperParams), cudaMemcpyHostToDevice),
                "cudaMemcpy(hp)");
   }
@@ -1809,7 +1911,7 @@ int dear_peer_zero_copy(dear_ctx* ctx, int32_t* on) {
   DEAR_API_BEGIN
   need(ctx, true);
   if (!on) invalid("dear_peer_zero_copy: null output");
-  *on = ctx->zc ? 1 : 0;
+  *on = ctx->zc ? (ctx->push ? 2 : 1) : 0;
   DEAR_API_END
 }
 

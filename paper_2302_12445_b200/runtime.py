@@ -281,6 +281,15 @@ class Runtime:
         check(lib().dear_peer_zero_copy(self._ctx, C.byref(on)))
         return bool(on.value)
 
+    @property
+    def push_rs(self) -> bool:
+        """The zero-copy path runs the push reduce-scatter (DEAR_PUSH_RS=1)."""
+        if not self._ctx.value:
+            return False
+        on = C.c_int32()
+        check(lib().dear_peer_zero_copy(self._ctx, C.byref(on)))
+        return on.value == 2
+
     def _connect_peers(self) -> None:
         """Exchange arena IPC handles over torch.distributed and map the peers."""
         import torch.distributed as dist

@@ -82,6 +82,8 @@ def run_runtime(comm, rank, P, policy, buf, steps, lr, backend="nccl", comm_orde
     rt.finalize()
     if flat and backend == "peer" and os.environ.get("DEAR_ZERO_COPY", "1") != "0":
         assert rt.zero_copy, "flat parameters/gradients must enable the zero-copy peer path"
+        if os.environ.get("DEAR_PUSH_RS") == "1":
+            assert rt.push_rs, "DEAR_PUSH_RS=1 must take the push reduce-scatter"
     if comm_order is not None:
         rt.set_comm_order(comm_order)
     with torch.cuda.stream(s):
@@ -212,6 +214,25 @@ def case_peer(rank, P):
     comm.close()
     return ok
 
+
+
+def case_push(rank, P):
+    """Push reduce-scatter (DEAR_PUSH_RS=1): every rank writes each chunk of
+    its gradients into its owner's push buffer over NVLink and the owner sums
+    its slots in ring order — the peer case's checks, bit-exact, plus the bf16
+    copy written by the push RS."""
+    os.environ["DEAR_PUSH_RS"] = "1"
+    ok = case_peer(rank, P)
+    comm = dear.init()
+    o = Restated()
+    w, same, _ = run_runtime(comm, rank, P, "DEAR_FUSED", 100_000, 3, 0.05, backend="peer",
+                             flat=True, shadow=True)
+    exp32 = oracle_run(o, RAGGED, P, 3, "DEAR_FUSED", 100_000, 0.05, f32=True)
+    good = same and np.array_equal(w, exp32) and run_runtime.shadow_ok
+    if rank == 0:
+        print(f"[push P={P}] bf16 copy + bit_exact={good}", flush=True)
+    comm.close()
+    return ok and good
 
 
 def case_nvls(rank, P):
@@ -351,7 +372,7 @@ def main():
     torch.cuda.set_device(int(os.environ["LOCAL_RANK"]))
     dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ["LOCAL_RANK"])))
     ok = {"runtime": case_runtime, "distoptim": case_distoptim, "peer": case_peer,
-          "nvls": case_nvls, "distoptim_nvls": case_distoptim_nvls,
+          "nvls": case_nvls, "distoptim_nvls": case_distoptim_nvls, "push": case_push,
           "timeout": case_timeout}[case](rank, P)
     t = torch.tensor([0 if ok else 1], device="cuda")
     dist.all_reduce(t)
