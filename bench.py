@@ -76,7 +76,8 @@ def parse():
     ap.add_argument("--no-calibrate", action="store_true",
                     help="north star: skip the t_ag = 1.25 t_ff batch comparison (N > 1)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--buffer-sweep-bytes", default="5000000,10000000,25000000,50000000",
+    ap.add_argument("--buffer-sweep-bytes",
+                    default="1000000,5000000,10000000,25000000,50000000,100000000",
                     help="N > 1: BASELINE config 3 (BERT-Base) DeAR vs WFBP at these fusion "
                          "buffers ('' to skip)")
     ap.add_argument("--extra-workload", default="bert_large",

@@ -8,6 +8,8 @@ DeAR runtime, per collective transport:
         in ring order and applies the update; AG pulls the owners' parameters)
   slot  peer kernels over IPC-mapped bucket slots (pack, RS+update, AG+unpack)
   nvls  NVLink SHARP: multimem.ld_reduce RS+update, multicast-store AG
+  push  zero-copy with the push reduce-scatter (DEAR_PUSH_RS=1): pack writes
+        each chunk into its owner's slot over NVLink, the owner sums locally
 
     torchrun --nproc-per-node P tools/sweep_collectives.py [--backends nccl,zc,slot,nvls]
         [--min-kb 64] [--max-mb 256]
@@ -35,7 +37,7 @@ def main():
     ap.add_argument("--max-mb", type=int, default=256)
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--backends", default="nccl,zc,slot,nvls")
+    ap.add_argument("--backends", default="nccl,zc,slot,nvls,push")
     a = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -65,7 +67,8 @@ def main():
             pbuf = torch.zeros(maxn, device="cuda")
             gbuf = torch.zeros(maxn, device="cuda")
         os.environ["DEAR_ZERO_COPY"] = "0" if backend == "slot" else "1"
-        rt_backend = {"zc": "peer", "slot": "peer"}.get(backend, backend)
+        os.environ["DEAR_PUSH_RS"] = "1" if backend == "push" else "0"
+        rt_backend = {"zc": "peer", "slot": "peer", "push": "peer"}.get(backend, backend)
         size = a.min_kb * 1024
         points = []
         while size <= a.max_mb * 1024 * 1024:
@@ -77,8 +80,9 @@ def main():
                               heap=heap if backend == "nvls" else None)
             rt.register(1, p, g)
             rt.finalize()
-            if backend in ("zc", "slot"):
-                assert rt.zero_copy == (backend == "zc"), backend
+            if backend in ("zc", "slot", "push"):
+                assert rt.zero_copy == (backend != "slot"), backend
+                assert rt.push_rs == (backend == "push"), backend
             rt.set_timing(True)
             st = {k: [] for k in ("pack", "rs", "update", "ag", "unpack")}
             for it in range(a.warmup + a.reps):
@@ -98,6 +102,8 @@ def main():
                                device="cuda")
             dist.all_reduce(med, op=dist.ReduceOp.MAX)
             m = dict(zip(st, med.tolist()))
+            if backend == "push":  # the pack moves the data over NVLink
+                m["rs"] += m["pack"]
             bus = (P - 1) * stride * 4
             pt = {"backend": backend, "bytes": size, "P": P, "rs_ms": m["rs"], "ag_ms": m["ag"],
                   "pack_ms": m["pack"], "update_ms": m["update"], "unpack_ms": m["unpack"],
@@ -107,7 +113,9 @@ def main():
                            "zc": "rs: fused RS+update kernel; ag: pull all-gather kernel",
                            "slot": "rs: fused RS+update after pack; ag: fused AG+unpack",
                            "nvls": "rs: multimem.ld_reduce RS+update; ag: multicast-store "
-                                   "broadcast + arrival wait"}[backend]}
+                                   "broadcast + arrival wait",
+                           "push": "rs: pack (posted stores into the owners' slots) + local "
+                                   "ring-order sum + update; ag: pull all-gather"}[backend]}
             points.append(pt)
             if rank == 0:
                 print(json.dumps(pt), flush=True)
