@@ -178,10 +178,9 @@ cudaError_t launch_rs_update_peer(const Unit* units, const Slice* slices, int64_
 // slots; the parameter-allocation deltas for zero-copy).
 // `n_slices`: entries of `slices` (kPeerSlices, or kZcSlices for zero-copy),
 // one CTA each.
-// ff = 1: an all-gather issued for the forward (the kPeerUnrollFF instance).
 cudaError_t launch_ag_unpack_peer(const Unit* units, const Slice* slices, int64_t total,
                                   int with_shadow, const PeerArgs& pa, const PeerArgs& sa,
-                                  BucketFlags* flags, int n_slices, cudaStream_t s, int ff = 0);
+                                  BucketFlags* flags, int n_slices, cudaStream_t s);
 // Zero-copy fused reduce-scatter + update: the owned chunk of every rank's
 // gradients (at ga.delta[k]) summed in ring order, 1/P, SGD, written into
 // the own parameters (+ bf16 copy); announces / waits on flags->packed and

@@ -51,13 +51,7 @@ constexpr int kUnroll = DEAR_HBM_UNROLL;
 #define DEAR_PEER_UNROLL 4
 #endif
 constexpr int kPeerUnroll = DEAR_PEER_UNROLL;
-// All-gathers issued for the forward (dear_step / deferred into the next
-// forward) gate the layers behind them, so they may run less throttled than
-// the ones back-filled into backprop (DEAR_FF_AG_FAST).
-#ifndef DEAR_PEER_UNROLL_FF
-#define DEAR_PEER_UNROLL_FF 8
-#endif
-constexpr int kPeerUnrollFF = DEAR_PEER_UNROLL_FF;
+
 constexpr int kSms = 148;
 
 __device__ __forceinline__ float4 shfl_down4(float4 v) {
@@ -963,7 +957,7 @@ __global__ void DEAR_ZC_BOUNDS
 // ------------------------------------------- fused peer AG+unpack ---------
 // Source element of a unit: U.a + off on rank U.peer, i.e. at sa.delta[U.peer]
 // (sa = arena deltas for bucket slots, parameter deltas for zero-copy).
-template <bool kShadow, int KU = kPeerUnroll>
+template <bool kShadow>
 __device__ __forceinline__ void ag_unpack_peer_body(const Unit* __restrict__ units,
                                                     const Slice* __restrict__ slices,
                                                     const PeerArgs& pa, const PeerArgs& sa,
@@ -976,7 +970,7 @@ __device__ __forceinline__ void ag_unpack_peer_body(const Unit* __restrict__ uni
     const float* src = at_peer(U.a + off, sa.delta[U.peer]);
     float* dst = U.b + off;
     __nv_bfloat16* sh = (kShadow && U.c) ? static_cast<__nv_bfloat16*>(U.c) + off : nullptr;
-    run_unit<Hint::kStream, KU>(
+    run_unit<Hint::kStream, kPeerUnroll>(
         src, dst, n,
         [&](int64_t i) {
           const float v = src[i];
@@ -992,11 +986,11 @@ __device__ __forceinline__ void ag_unpack_peer_body(const Unit* __restrict__ uni
   signal_done(&flags->done[2], &flags->gathered, blk);
 }
 
-template <bool kShadow, int KU = kPeerUnroll>
+template <bool kShadow>
 __global__ void DEAR_ZC_BOUNDS
     ag_unpack_peer_kernel(const Unit* __restrict__ units, const Slice* __restrict__ slices,
                           PeerArgs pa, PeerArgs sa, BucketFlags* flags, int n_slices) {
-  ag_unpack_peer_body<kShadow, KU>(units, slices, pa, sa, flags, n_slices, this_blk());
+  ag_unpack_peer_body<kShadow>(units, slices, pa, sa, flags, n_slices, this_blk());
 }
 
 // ------------------------------------------------ NVLS (multimem) --------
@@ -1420,15 +1414,11 @@ cudaError_t launch_rs_update_peer(const Unit* units, const Slice* slices, int64_
 
 cudaError_t launch_ag_unpack_peer(const Unit* units, const Slice* slices, int64_t total,
                                   int with_shadow, const PeerArgs& pa, const PeerArgs& sa,
-                                  BucketFlags* flags, int n_slices, cudaStream_t s, int ff) {
+                                  BucketFlags* flags, int n_slices, cudaStream_t s) {
   (void)total;
   const size_t smem = 0;
   const int g = bucket_grid(n_slices);
-  if (ff && with_shadow)
-    ag_unpack_peer_kernel<true, kPeerUnrollFF><<<g, kThreads, smem, s>>>(units, slices, pa, sa, flags, n_slices);
-  else if (ff)
-    ag_unpack_peer_kernel<false, kPeerUnrollFF><<<g, kThreads, smem, s>>>(units, slices, pa, sa, flags, n_slices);
-  else if (with_shadow)
+  if (with_shadow)
     ag_unpack_peer_kernel<true><<<g, kThreads, smem, s>>>(units, slices, pa, sa, flags, n_slices);
   else
     ag_unpack_peer_kernel<false><<<g, kThreads, smem, s>>>(units, slices, pa, sa, flags, n_slices);

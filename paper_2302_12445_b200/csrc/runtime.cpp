@@ -240,26 +240,13 @@ struct dear_ctx {
   void complete_bucket(int b);
   void enqueue_backpipe(int b);
   void enqueue_feedpipe(cudaStream_t fence_stream);
-  void enqueue_ag(int g, bool ff = false);
+  void enqueue_ag(int g);
   void enqueue_ordered_ags();
   void record_t(int b, int which);
   std::string label(const char* kind, int b) const;
 };
 
 namespace {
-
-// DEAR_FF_AG_FAST=1 (experiment): the all-gathers issued for the forward run
-// the less throttled kernel instance (kPeerUnrollFF). Measured negative: the
-// forward GEMMs slow down and the all-gathers do not get faster in the step
-// (BERT-L N = 4 7.56-7.61 ms at the backprop setting, 7.77-7.95 at 8 / 16
-// vectors per lane; profiles/r02ffag_ab.log).
-bool ff_ag_fast() {
-  static const bool on = [] {
-    const char* e = std::getenv("DEAR_FF_AG_FAST");
-    return e && e[0] == '1';
-  }();
-  return on;
-}
 
 void free_events(std::vector<cudaEvent_t>& evs) {
   for (cudaEvent_t e : evs)
@@ -603,8 +590,7 @@ void dear_ctx::exec(const Op& op) {
       } else if (zc) {
         // Each owner's updated parameters, read over NVLink into ours.
         cuda_check(launch_ag_unpack_peer(B->zag_u, B->zag_ps, B->e_zag, B->any_shadow ? 1 : 0,
-                                         pa, qa, B->flags, kZcSlices, comm_stream,
-                                         op.value != 0.f && ff_ag_fast() ? 1 : 0),
+                                         pa, qa, B->flags, kZcSlices, comm_stream),
                    "zero-copy ag kernel");
       } else if (peer) {
         // Fused all-gather + unpack over NVLink (OP_UNPACK becomes a no-op);
@@ -694,19 +680,19 @@ void dear_ctx::enqueue_feedpipe(cudaStream_t fence_stream) {
     // Group dependency: the all-gathers not dispatched during backprop, in
     // the simulated dispatch order.
     for (; order_cursor < comm_order.size(); ++order_cursor)
-      enqueue_ag(-comm_order[order_cursor] - 1, true);
+      enqueue_ag(-comm_order[order_cursor] - 1);
     order_cursor = 0;
   } else {
     // Reverse plan order = feed-forward order (task_graph.cpp:199-206).
-    for (int g = static_cast<int>(buckets.size()) - 1; g >= 0; --g) enqueue_ag(g, true);
+    for (int g = static_cast<int>(buckets.size()) - 1; g >= 0; --g) enqueue_ag(g);
   }
   ags_deferred = false;
   if (local) group->drain();
 }
 
-void dear_ctx::enqueue_ag(int g, bool ff) {
+void dear_ctx::enqueue_ag(int g) {
   Bucket& B = buckets[static_cast<size_t>(g)];
-  enqueue({OP_AG, g, nullptr, ff ? 1.f : 0.f});
+  enqueue({OP_AG, g, nullptr});
   enqueue({OP_UNPACK, g, nullptr});
   enqueue({OP_AG_DONE, g, nullptr});
   trace.push_back(label("AG", g));
