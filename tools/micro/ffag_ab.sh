@@ -1,4 +1,5 @@
 # Forward-phase all-gathers at unroll 4 (= backprop setting) / 8 / 16, in-step
+# (The forward-phase instance, DEAR_PEER_UNROLL_FF, was removed from the product after this measurement.)
 # BERT-L traces at P = 4 and P = 2.
 mkdir -p gpurun_out
 i=0
