@@ -1612,7 +1612,7 @@ TensorSpan tensor_span(const dear_ctx& c, bool grads, bool need_alloc = true) {
 //   [208,216) grad lo - base  [216,224) param lo - base
 //   [224,232) gradient layout hash  [232,240) parameter layout hash
 constexpr size_t kH_ZC = 76, kH_G = 80, kH_Q = 144, kH_GOFF = 208, kH_QOFF = 216,
-                 kH_GLAY = 224, kH_QLAY = 232;
+                 kH_GLAY = 224, kH_QLAY = 232, kH_PUSH = 240;
 }  // namespace
 
 namespace {
@@ -1755,6 +1755,8 @@ int dear_peer_handle(dear_ctx* ctx, uint8_t out[DEAR_PEER_HANDLE_BYTES]) {
     cudaGetLastError();  // a non-exportable allocation only disables zero-copy
   }
   memcpy(out + kH_ZC, &zc, 4);
+  const int32_t push = ctx->push_tables ? 1 : 0;
+  memcpy(out + kH_PUSH, &push, 4);
   if (zc) {
     memcpy(out + kH_G, &gh, 64);
     memcpy(out + kH_Q, &qh, 64);
@@ -1788,6 +1790,11 @@ int dear_peer_connect(dear_ctx* ctx, const uint8_t* handles, int32_t n) {
     int32_t z = 0;
     uint64_t gl = 0, ql = 0, go = 0, qo = 0;
     memcpy(&z, h + kH_ZC, 4);
+    int32_t push = 0;
+    memcpy(&push, h + kH_PUSH, 4);
+    if ((push != 0) != c.push_tables)
+      invalid("dear_peer_connect: ranks disagree on DEAR_PUSH_RS (set it on every rank before "
+              "dear_finalize)");
     memcpy(&gl, h + kH_GLAY, 8);
     memcpy(&ql, h + kH_QLAY, 8);
     memcpy(&go, h + kH_GOFF, 8);

@@ -235,6 +235,22 @@ def case_push(rank, P):
     return ok and good
 
 
+def case_push_mismatch(rank, P):
+    """DEAR_PUSH_RS set on rank 0 only: every rank's connect must fail with a
+    clear error instead of running mismatched protocols."""
+    os.environ["DEAR_PUSH_RS"] = "1" if rank == 0 else "0"
+    comm = dear.init()
+    try:
+        run_runtime(comm, rank, P, "DEAR_FUSED", 100_000, 1, 0.05, backend="peer", flat=True)
+        ok = False
+    except dear.InvalidArgument as e:
+        ok = "disagree on DEAR_PUSH_RS" in str(e)
+        if rank == 0:
+            print(f"[push mismatch] rejected: {e}", flush=True)
+    comm.close()
+    return ok
+
+
 def case_nvls(rank, P):
     """NVLS backend: the switch sums each owned chunk (multimem.ld_reduce) and
     the owners broadcast with multicast stores. P = 2: a + b is order-free, so
@@ -373,6 +389,7 @@ def main():
     dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ["LOCAL_RANK"])))
     ok = {"runtime": case_runtime, "distoptim": case_distoptim, "peer": case_peer,
           "nvls": case_nvls, "distoptim_nvls": case_distoptim_nvls, "push": case_push,
+          "push_mismatch": case_push_mismatch,
           "timeout": case_timeout}[case](rank, P)
     t = torch.tensor([0 if ok else 1], device="cuda")
     dist.all_reduce(t)

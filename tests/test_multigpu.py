@@ -16,7 +16,8 @@ def _nproc():
     return min(torch.cuda.device_count(), int(os.environ.get("DEAR_TEST_NPROC", "4")))
 
 
-@pytest.mark.parametrize("case", ["runtime", "peer", "push", "distoptim", "nvls", "distoptim_nvls"])
+@pytest.mark.parametrize("case", ["runtime", "peer", "push", "push_mismatch", "distoptim", "nvls",
+                                  "distoptim_nvls"])
 def test_nccl_parity(case):
     n = _nproc()
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
