@@ -470,7 +470,12 @@ def gpu_arm(a, wl, world, rank, local_rank):
     if dist_on:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+        import datetime
+
+        # A healthy run never waits minutes in one collective: fail instead of
+        # hanging the job if a rank dies.
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"),
+                                timeout=datetime.timedelta(minutes=5))
         comm = dear.init()
     batch = a.batch or wl["batch"]
     tokens = batch * wl["tokens_per_sample"]
@@ -552,17 +557,38 @@ def gpu_arm(a, wl, world, rank, local_rank):
     runc = make_runner(Step(model, None, stream), use_graph, stream)
     res["compute_ms"] = time_loop(runc, a.steps, a.warmup, stream, dist_on)
 
+    # Everything below runs after the headline measurement. A failure in one
+    # of these sections is recorded in the line instead of losing it; after a
+    # CUDA error the context is unusable, so the remaining GPU sections are
+    # skipped and the process exits right after printing (main()).
+    broken = []
+
+    def guarded(name, fn):
+        if broken:
+            return {"skipped": f"after the error in {broken[0]}"}
+        try:
+            return fn()
+        except Exception as e:  # noqa: BLE001 - reported in the JSON line
+            broken.append(name)
+            print(f"[bench] {name} failed: {type(e).__name__}: {e}", file=sys.stderr, flush=True)
+            return {"error": f"{type(e).__name__}: {e}"[:400]}
+
     extra = None
     if a.extra_workload != "none" and a.extra_workload != a.workload:
-        extra = compare_policies(a, a.extra_workload, comm, world, rank, stream)
+        extra = guarded("north_star", lambda: compare_policies(a, a.extra_workload, comm, world,
+                                                               rank, stream))
     config3 = None
     if world > 1 and a.buffer_sweep_bytes:
-        config3 = buffer_sweep(a, "bert_base", comm, world, rank, stream)
+        config3 = guarded("config3", lambda: buffer_sweep(a, "bert_base", comm, world, rank,
+                                                          stream))
     # Post-timing checks (nothing below is timed): one measured iteration in the
     # reference's trace schema, validated; oracle parity of one full bucket at
     # the bench configuration.
-    timeline = None if a.no_timeline else _measured_timeline(a, model, comm, rank, world, stream)
-    parity = None if a.no_parity else _bench_parity(a, model, comm, rank, world, stream)
+    timeline = None if a.no_timeline else guarded(
+        "timeline", lambda: _measured_timeline(a, model, comm, rank, world, stream))
+    parity = None if a.no_parity else guarded(
+        "parity", lambda: _bench_parity(a, model, comm, rank, world, stream))
+    gpu_arm.broken = broken
     if rank != 0:
         return None
     samples = batch * world
@@ -1222,6 +1248,12 @@ def main():
     line = gpu_arm(a, wl, world, rank, local_rank)
     if line is not None:
         print(json.dumps(line), flush=True)
+    if getattr(gpu_arm, "broken", None):
+        # A post-headline section hit an error (recorded in the line); the
+        # CUDA context / communicators may be unusable: leave without teardown.
+        sys.stdout.flush()
+        sys.stderr.flush()
+        os._exit(0)
     if world > 1:
         import torch.distributed as dist
 
