@@ -310,6 +310,24 @@ class Step:
                 self.out_host.copy_(m.result_scalar(), non_blocking=True)
 
 
+def _mark(name):
+    """DEAR_BENCH_TRACE=1: device-synchronise and log a section marker to
+    stderr (localises an asynchronous CUDA error to the section before it)."""
+    if os.environ.get("DEAR_BENCH_TRACE") != "1":
+        return
+    import time
+
+    import torch
+
+    try:
+        torch.cuda.synchronize()
+        status = "ok"
+    except Exception as e:  # noqa: BLE001
+        status = f"{type(e).__name__}: {e}"[:200]
+    print(f"[bench-trace {time.strftime('%H:%M:%S')} rank {os.environ.get('RANK', '0')}] "
+          f"{name}: {status}", file=sys.stderr, flush=True)
+
+
 def time_loop(fn, steps, warmup, stream, dist_on, clock=None):
     import torch
 
@@ -543,7 +561,9 @@ def gpu_arm(a, wl, world, rank, local_rank):
     rt.close()
 
     # --- HBM kernels in isolation: comm-only iterations (no GEMMs) -----------
+    _mark("main DeAR step measured")
     iso = _isolated_stage_times(model, runtime, stream, a.policy)
+    _mark("isolated stage times")
 
     # --- ablation: same kernels, WFBP schedule; compute-only ------------------
     if not a.no_ablation:
@@ -554,6 +574,7 @@ def gpu_arm(a, wl, world, rank, local_rank):
         rtw.close()
     # Compute-only step (the layer GEMM chain, no runtime): also the GEMM
     # roofline's timed region.
+    _mark("ablation done")
     runc = make_runner(Step(model, None, stream), use_graph, stream)
     res["compute_ms"] = time_loop(runc, a.steps, a.warmup, stream, dist_on)
 
@@ -573,6 +594,7 @@ def gpu_arm(a, wl, world, rank, local_rank):
             print(f"[bench] {name} failed: {type(e).__name__}: {e}", file=sys.stderr, flush=True)
             return {"error": f"{type(e).__name__}: {e}"[:400]}
 
+    _mark("headline measured")
     extra = None
     if a.extra_workload != "none" and a.extra_workload != a.workload:
         extra = guarded("north_star", lambda: compare_policies(a, a.extra_workload, comm, world,
@@ -1126,12 +1148,15 @@ def compare_policies(a, wl_name, comm, world, rank, stream):
     nvls_ok = world > 1 and dear.nvls_supported()
 
     def one(batch, with_nccl):
+        _mark(f"north_star batch {batch}: start")
         model = SyntheticModel(preset_param_counts(wl["preset"]), wl["hidden"],
                                batch * wl["tokens_per_sample"], seed=4321,
                                symmetric=a.backend == "nvls" and world > 1)
+        _mark("north_star: model built (tiles tuned)")
         out = {"batch_per_gpu": batch}
         run = make_runner(Step(model, None, stream), True, stream)
         comp = time_loop(run, steps, warm, stream, dist_on)
+        _mark("north_star: compute-only timed")
         out["compute_only_ms"] = comp
         tiles = model.tiles or {}
         t_ff = tiles.get("ff", {}).get("us", 0.0) * model.L / 1e3
@@ -1151,6 +1176,7 @@ def compare_policies(a, wl_name, comm, world, rank, stream):
                     m = SyntheticModel(preset_param_counts(wl["preset"]), wl["hidden"],
                                        batch * wl["tokens_per_sample"], seed=4321,
                                        symmetric=True)
+                _mark(f"north_star: policy pair on {be or 'default'}")
                 res = _policy_pair(a, m, comm, world, rank, stream, batch, steps, warm, be)
             except Exception as e:  # an optional transport must not sink the line
                 if be is None:
