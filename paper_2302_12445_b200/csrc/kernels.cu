@@ -77,6 +77,14 @@ __device__ __forceinline__ float4 realign(float4 a, float4 b) {
 
 enum class Hint { kStream, kKeep };
 
+// Realignment of a source that is not in the destination's 16 B phase by a
+// second (cache-hit) load per vector in the local HBM kernels (pack, update,
+// direct update, unpack); 0 keeps the shuffle exchange.
+#ifndef DEAR_REALIGN_LD2
+#define DEAR_REALIGN_LD2 1
+#endif
+constexpr bool kRealignLd2 = DEAR_REALIGN_LD2 != 0;
+
 // Streaming (evict-first) stores for the pack / unpack destinations:
 // graph-chained ResNet-50 buckets, pack 0.636 -> 0.660 and unpack 0.666 ->
 // 0.708 of HBM peak (tools/micro/hbm_stage.py, profiles/r02h5_hbm_ab.log).
@@ -108,7 +116,10 @@ __device__ __forceinline__ float4 ld4(const float4* p) {
 // (pre[q] pairs with destination vector q), loaded in the same round as the
 // source so the body never starts a dependent second memory trip; the body
 // then receives it as its third argument.
-template <int M, Hint H, int kUnroll, bool kPre = false, typename Body>
+// kLd2 (local sources only): each lane loads its next source vector itself
+// (an L1 / L2 hit — the neighbour lane loads it too) instead of taking it
+// from the neighbour with 8 shuffles per vector.
+template <int M, Hint H, int kUnroll, bool kPre = false, bool kLd2 = false, typename Body>
 __device__ __forceinline__ void warp_stream(const float* src_floor, int64_t n4, int64_t qmax,
                                             Body&& body, const float4* pre = nullptr) {
   const float4* s4 = reinterpret_cast<const float4*>(src_floor);
@@ -120,14 +131,17 @@ __device__ __forceinline__ void warp_stream(const float* src_floor, int64_t n4, 
        base += static_cast<int64_t>(kWarps) * 32 * kUnroll) {
     float4 a[kUnroll];
     float4 p[kPre ? kUnroll : 1];
+    constexpr bool kTwo = kLd2 && M != 0;
+    float4 a2[kTwo ? kUnroll : 1];
 #pragma unroll
     for (int k = 0; k < kUnroll; ++k) {
       const int64_t q = base + k * 32 + lane;
       a[k] = q <= qmax ? ld4<H>(s4 + q) : zero;
+      if constexpr (kTwo) a2[k] = q + 1 <= qmax ? ld4<H>(s4 + q + 1) : zero;
       if constexpr (kPre) p[k] = q < n4 ? __ldcs(pre + q) : zero;
     }
     float4 extra = zero;
-    if constexpr (M != 0) {
+    if constexpr (M != 0 && !kTwo) {
       const int64_t qx = base + kUnroll * 32;
       if (lane == 31 && qx <= qmax) extra = ld4<H>(s4 + qx);
     }
@@ -135,7 +149,9 @@ __device__ __forceinline__ void warp_stream(const float* src_floor, int64_t n4, 
     for (int k = 0; k < kUnroll; ++k) {
       const int64_t q = base + k * 32 + lane;
       float4 b = a[k];
-      if constexpr (M != 0) {
+      if constexpr (kTwo) {
+        b = a2[k];
+      } else if constexpr (M != 0) {
         b = shfl_down4(a[k]);
         float4 nxt = extra;
         if (k + 1 < kUnroll) {
@@ -157,7 +173,7 @@ __device__ __forceinline__ void warp_stream(const float* src_floor, int64_t n4, 
 
 // Peels `dst` to 16 B alignment (scalar head via head_fn), then dispatches the
 // vector walk on the source misalignment, then the scalar tail.
-template <Hint H, int KU = kUnroll, typename HeadFn, typename VecFn>
+template <Hint H, int KU = kUnroll, bool kLd2 = false, typename HeadFn, typename VecFn>
 __device__ __forceinline__ void run_unit(const float* src, const float* dst, int64_t len,
                                          HeadFn&& scalar_fn, VecFn&& vec_fn) {
   int64_t head = ((16 - (reinterpret_cast<uintptr_t>(dst) & 15)) & 15) >> 2;
@@ -172,16 +188,16 @@ __device__ __forceinline__ void run_unit(const float* src, const float* dst, int
     const int64_t qmax = (m + rest - 1) >> 2;
     switch (m) {
       case 0:
-        warp_stream<0, H, KU>(floor, n4, qmax, [&](int64_t q, float4 v) { vec_fn(head, q, v); });
+        warp_stream<0, H, KU, false, kLd2>(floor, n4, qmax, [&](int64_t q, float4 v) { vec_fn(head, q, v); });
         break;
       case 1:
-        warp_stream<1, H, KU>(floor, n4, qmax, [&](int64_t q, float4 v) { vec_fn(head, q, v); });
+        warp_stream<1, H, KU, false, kLd2>(floor, n4, qmax, [&](int64_t q, float4 v) { vec_fn(head, q, v); });
         break;
       case 2:
-        warp_stream<2, H, KU>(floor, n4, qmax, [&](int64_t q, float4 v) { vec_fn(head, q, v); });
+        warp_stream<2, H, KU, false, kLd2>(floor, n4, qmax, [&](int64_t q, float4 v) { vec_fn(head, q, v); });
         break;
       default:
-        warp_stream<3, H, KU>(floor, n4, qmax, [&](int64_t q, float4 v) { vec_fn(head, q, v); });
+        warp_stream<3, H, KU, false, kLd2>(floor, n4, qmax, [&](int64_t q, float4 v) { vec_fn(head, q, v); });
         break;
     }
   }
@@ -190,7 +206,7 @@ __device__ __forceinline__ void run_unit(const float* src, const float* dst, int
 
 // run_unit with a second destination-aligned input stream `pre` (element i
 // of `pre` pairs with dst[i]); vec_fn(head, q, v_src, v_pre).
-template <Hint H, int KU = kUnroll, typename HeadFn, typename VecFn>
+template <Hint H, int KU = kUnroll, bool kLd2 = false, typename HeadFn, typename VecFn>
 __device__ __forceinline__ void run_unit_pre(const float* src, const float* dst, const float* pre,
                                              int64_t len, HeadFn&& scalar_fn, VecFn&& vec_fn) {
   int64_t head = ((16 - (reinterpret_cast<uintptr_t>(dst) & 15)) & 15) >> 2;
@@ -198,7 +214,7 @@ __device__ __forceinline__ void run_unit_pre(const float* src, const float* dst,
   if ((reinterpret_cast<uintptr_t>(pre + head) & 15) != 0) {
     // `pre` out of phase with the destination (not produced by the runtime's
     // layouts): per-lane scalar gathers of it inside the body.
-    run_unit<H, KU>(src, dst, len, scalar_fn, [&](int64_t h, int64_t q, float4 v) {
+    run_unit<H, KU, kLd2>(src, dst, len, scalar_fn, [&](int64_t h, int64_t q, float4 v) {
       const float* pp = pre + h + 4 * q;
       vec_fn(h, q, v, make_float4(pp[0], pp[1], pp[2], pp[3]));
     });
@@ -215,10 +231,10 @@ __device__ __forceinline__ void run_unit_pre(const float* src, const float* dst,
     const float4* p4 = reinterpret_cast<const float4*>(pre + head);
     auto body = [&](int64_t q, float4 v, float4 w) { vec_fn(head, q, v, w); };
     switch (m) {
-      case 0: warp_stream<0, H, KU, true>(floor, n4, qmax, body, p4); break;
-      case 1: warp_stream<1, H, KU, true>(floor, n4, qmax, body, p4); break;
-      case 2: warp_stream<2, H, KU, true>(floor, n4, qmax, body, p4); break;
-      default: warp_stream<3, H, KU, true>(floor, n4, qmax, body, p4); break;
+      case 0: warp_stream<0, H, KU, true, kLd2>(floor, n4, qmax, body, p4); break;
+      case 1: warp_stream<1, H, KU, true, kLd2>(floor, n4, qmax, body, p4); break;
+      case 2: warp_stream<2, H, KU, true, kLd2>(floor, n4, qmax, body, p4); break;
+      default: warp_stream<3, H, KU, true, kLd2>(floor, n4, qmax, body, p4); break;
     }
   }
   for (int64_t i = head + n4 * 4 + threadIdx.x; i < len; i += kThreads) scalar_fn(i);
@@ -435,8 +451,10 @@ __global__ void __launch_bounds__(kThreads, (kSignal && kPeerPackLight) ? 1 : DE
   walk_slice(units, slices, n_slices, [&](const Unit& U, int64_t off, int64_t n) {
     const float* src = U.a + off;
     float* dst = kPush ? const_cast<float*>(at_peer(U.b + off, pa.delta[U.peer])) : U.b + off;
-    run_unit<Hint::kStream, kPush ? DEAR_PUSH_UNROLL
-                                  : ((kSignal && kPeerPackLight) ? kPackPeerUnroll : DEAR_PACK_UNROLL)>(
+    run_unit<Hint::kStream,
+             kPush ? DEAR_PUSH_UNROLL
+                   : ((kSignal && kPeerPackLight) ? kPackPeerUnroll : DEAR_PACK_UNROLL),
+             kRealignLd2>(
         src, dst, n, [&](int64_t i) { dst[i] = __fmul_rn(src[i], scale); },
         [&](int64_t head, int64_t q, float4 v) {
           v.x = __fmul_rn(v.x, scale);
@@ -483,7 +501,7 @@ __global__ void __launch_bounds__(kThreads, DEAR_UPD_CTAS_PER_SM) update_kernel(
     const float* w = U.a + off;
     float* g = U.b + off;
     float* mom = kMom ? static_cast<float*>(U.c) + off : nullptr;
-    run_unit_pre<Hint::kKeep>(
+    run_unit_pre<Hint::kKeep, kUnroll, kRealignLd2>(
         w, g, g, n,
         [&](int64_t i) {
           float m = kMom ? mom[i] : 0.f;
@@ -519,7 +537,7 @@ __global__ void __launch_bounds__(kThreads, DEAR_DIR_CTAS_PER_SM) update_direct_
     const float* g = U.a + off;
     float* w = U.b + off;
     __nv_bfloat16* sh = (kShadow && U.c) ? static_cast<__nv_bfloat16*>(U.c) + off : nullptr;
-    run_unit_pre<Hint::kStream>(
+    run_unit_pre<Hint::kStream, kUnroll, kRealignLd2>(
         g, w, w, n,
         [&](int64_t i) {
           float m = 0.f;
@@ -556,7 +574,7 @@ __global__ void __launch_bounds__(kThreads, DEAR_UNPACK_CTAS_PER_SM) unpack_kern
     const float* src = U.a + off;
     float* dst = U.b + off;
     __nv_bfloat16* sh = (kShadow && U.c) ? static_cast<__nv_bfloat16*>(U.c) + off : nullptr;
-    run_unit<Hint::kStream, DEAR_UNPACK_UNROLL>(
+    run_unit<Hint::kStream, DEAR_UNPACK_UNROLL, kRealignLd2>(
         src, dst, n,
         [&](int64_t i) {
           const float v = src[i];

@@ -19,6 +19,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="resnet50")
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--align4", action="store_true",
+                    help="round every tensor to a multiple of 4 elements (every layer "
+                         "starts 16 B aligned in its bucket: no realignment)")
     a = ap.parse_args()
     import torch
 
@@ -29,6 +32,8 @@ def main():
     torch.cuda.set_device(0)
     wl = bench.WORKLOADS[a.workload]
     counts = preset_param_counts(wl["preset"])
+    if a.align4:
+        counts = [(c + 3) // 4 * 4 for c in counts]
     model = SyntheticModel(counts, wl["hidden"], wl["batch"] * wl["tokens_per_sample"], seed=1)
     stream = torch.cuda.Stream()
     ns = argparse.Namespace(group_dependency=0, buffer=25_000_000, lr=0.05, momentum=0.0,
@@ -54,7 +59,8 @@ def main():
         elem_bytes[name] = 8 * n * nb
     out = {k: {"gbs_best": max(v), "frac_best": max(v) / hbm, "us_per_launch":
                elem_bytes[k] / max(v) / 1e3 / 5} for k, v in res.items()}
-    print(json.dumps({"lib": os.environ.get("DEAR_LIB", "libdear.so"), "peak": hbm, **out}))
+    print(json.dumps({"lib": os.environ.get("DEAR_LIB", "libdear.so"), "align4": a.align4,
+                      "peak": hbm, **out}))
 
 
 def _chain_gbs(torch, stream, src, dst, op, reps):
