@@ -96,11 +96,7 @@ constexpr bool kRealignLd2 = DEAR_REALIGN_LD2 != 0;
 template <Hint H>
 __device__ __forceinline__ float4 ld4(const float4* p) {
   if constexpr (H == Hint::kStream) {
-#ifdef DEAR_HBM_LD_PLAIN  // experiment: default-policy loads
-    return *p;
-#else
     return __ldcs(p);
-#endif
   } else {
     return __ldg(p);
   }
