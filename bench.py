@@ -886,9 +886,10 @@ def _bench_parity(a, model, comm, rank, world, stream):
 
 def _ncu_traffic(workload):
     """DRAM bytes per GEMM launch from the committed ncu --set full capture
-    (profiles/r01_ncu_traffic.json), or None when none was taken for this workload."""
+    (profiles/r02z_ncu_traffic.json, the final tree's), or None when none was
+    taken for this workload."""
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
-                        "r01_ncu_traffic.json")
+                        "r02z_ncu_traffic.json")
     try:
         with open(path) as f:
             return json.load(f)[workload]["gemm_traffic_bytes_per_launch"]
